@@ -1,0 +1,426 @@
+"""Pins for the CPU oracle against what the paper and mathematics fix.
+
+Each test names the passage it checks.  None of them re-types the oracle's
+formula: they use closed forms printed in the paper, the paper's worked
+example, brute-force values on tiny inputs, a library routine (torch fp64
+SDPA) on exact-size inputs, and invariants between independent code paths.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from paper_2511_12031_b200 import synth
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _gold(name):
+    with open(os.path.join(GOLD, name)) as f:
+        return json.load(f)
+
+
+def _f32(x):
+    return np.ascontiguousarray(np.asarray(x, dtype=np.float32))
+
+
+def _run_decode(policy, *, B, H_kv, H_q, D, N, r, dtype="f32", seed=1, sdpa=True, layer=0):
+    """Decode N tokens from an empty cache: append, then SDPA."""
+    dt = O.F32 if dtype == "f32" else O.BF16
+    orc = O.Oracle(B, H_kv, H_q, D, r, N, dtype=dt, policy=policy)
+    outs = []
+    for n in range(1, N + 1):
+        x = synth.step_inputs(seed, layer, n, B=B, H_kv=H_kv, H_q=H_q, D=D, dtype=dtype)
+        orc.append(x["k"], x["v"])
+        if sdpa:
+            outs.append(orc.sdpa(x["q"], n))
+    return orc, outs
+
+
+# --------------------------------------------------------- closed forms (ledger)
+
+@pytest.mark.parametrize("N", [4, 16, 64, 256])
+def test_iterative_copy_closed_form(oracle_mod, N):
+    """total elements moved by iterative allocation over N tokens,
+    K and V, all L layers = B*L*N*(N+1)*D (copy of n-1 rows + the new row)."""
+    B, H, d, L = 2, 3, 4, 2
+    eb = 4
+    total = 0
+    for layer in range(L):
+        orc, _ = _run_decode(O.POLICY_ITERATIVE, B=B, H_kv=H, H_q=H, D=d, N=N, r=1,
+                             sdpa=False, layer=layer)
+        s = orc.stats()
+        total += (s["copied_bytes"] + s["append_written_bytes"]) // eb
+        assert s["alloc_events"] == N                       # one allocation per token
+    D = H * d
+    assert total == B * L * N * (N + 1) * D
+
+
+@pytest.mark.parametrize("N", [4, 16, 64])
+def test_sdpa_mac_closed_forms(oracle_mod, N):
+    """P:L405-410 iterative MACs L*B*N*(N+1)*D; P:L435-437 upfront 2L*B*N^2*D;
+    BMC sums 2*B*L*((i+1)r)*D over r iterations per chunk
+    = L*B*N*(N+r)*D for r | N."""
+    B, H, d, L = 2, 2, 4, 1
+    D = H * d
+    it, _ = _run_decode(O.POLICY_ITERATIVE, B=B, H_kv=H, H_q=H, D=d, N=N, r=1)
+    assert it.stats()["macs"] == L * B * N * (N + 1) * D
+    up, _ = _run_decode(O.POLICY_UPFRONT, B=B, H_kv=H, H_q=H, D=d, N=N, r=N)
+    assert up.stats()["macs"] == 2 * L * B * N * N * D
+    for r in (1, 2, 4, N):
+        bm, _ = _run_decode(O.POLICY_BMC, B=B, H_kv=H, H_q=H, D=d, N=N, r=r)
+        assert bm.stats()["macs"] == L * B * N * (N + r) * D
+
+
+@pytest.mark.parametrize("N,r", [(37, 5), (64, 8), (50, 50), (9, 1), (100, 7)])
+def test_bmc_allocation_counts(oracle_mod, N, r):
+    """P:L609-611 (allocate once every r iterations, T = N/r) with the ragged
+    last chunk of reading R12: after n appends alloc_events = ceil(n/r), the
+    i-th growth copies i*r rows, the capacity law cap - valid in [0, r-1]
+     holds after every append."""
+    B, H, d = 1, 2, 2
+    orc = O.Oracle(B, H, H, d, r, N, dtype=O.F32, policy=O.POLICY_BMC)
+    for n in range(1, N + 1):
+        x = synth.step_inputs(3, 0, n, B=B, H_kv=H, H_q=H, D=d, dtype="f32")
+        orc.append(x["k"], x["v"])
+        s = orc.stats()
+        assert s["alloc_events"] == math.ceil(n / r)
+        assert 0 <= s["capacity"] - n <= r - 1 or s["capacity"] == N
+        c = math.ceil(n / r)
+        assert s["copied_bytes"] == 2 * B * H * d * 4 * r * (c - 1) * c // 2
+        assert s["init_written_bytes"] == 2 * B * H * d * 4 * sum(
+            min((i + 1) * r, N) for i in range(c))
+
+
+def test_copy_ratio_T_minus_1_over_N_plus_1(oracle_mod):
+    """S:L537 / P:L392: BMC realloc copies over iterative copies+writes
+    = (T-1)/(N+1) exactly at N=1024, T=32."""
+    N, T = 1024, 32
+    r = N // T
+    bm, _ = _run_decode(O.POLICY_BMC, B=1, H_kv=1, H_q=1, D=1, N=N, r=r, sdpa=False)
+    it, _ = _run_decode(O.POLICY_ITERATIVE, B=1, H_kv=1, H_q=1, D=1, N=N, r=1, sdpa=False)
+    sb, si = bm.stats(), it.stats()
+    num = sb["copied_bytes"]
+    den = si["copied_bytes"] + si["append_written_bytes"]
+    assert num * (N + 1) == den * (T - 1)
+
+
+def test_toy_config_counters(oracle_mod):
+    """tests/golden/toy_counters.json (BASELINE configs[0]; closed forms)."""
+    g = _gold("toy_counters.json")
+    c = g["config"]
+    kw = dict(B=c["B"], H_kv=c["H"], H_q=c["H"], D=c["d"], N=c["N"])
+    s16 = _run_decode(O.POLICY_BMC, r=16, **kw)[0].stats()
+    for key, val in g["bmc_r16"].items():
+        assert s16[key] == val, key
+    s1 = _run_decode(O.POLICY_BMC, r=1, sdpa=False, **kw)[0].stats()
+    for key in ("alloc_events", "copy_events", "copied_bytes"):
+        assert s1[key] == g["bmc_r1"][key], key
+    assert s1["init_written_bytes"] // c["eb"] == g["bmc_r1"]["init_written_elems"]
+    su = _run_decode(O.POLICY_UPFRONT, r=c["N"], **kw)[0].stats()
+    for key, val in g["upfront"].items():
+        assert su[key] == val, key
+
+
+# ----------------------------------------------------------- worked example
+
+def test_sd_worked_example(oracle_mod):
+    """P:L863-866 (wasted rows 7 -> 3 -> 1 -> 0), admission P:L867-869, no
+    reallocation during speculation P:L904."""
+    g = _gold("sd_worked_example.json")
+    B, H, d = 1, 1, 2
+    r = 8
+    orc = O.Oracle(B, H, H, d, r, 64, dtype=O.F32, policy=O.POLICY_BMC)
+    x = synth.step_inputs(5, 0, 0, B=B, H_kv=H, H_q=H, D=d, dtype="f32")
+    orc.append(x["k"], x["v"])                      # cap 8, valid 1 -> 7 free rows
+    s = orc.stats()
+    assert s["capacity"] - s["valid_max"] == g["initial_free_rows"]
+    allocs = s["alloc_events"]
+    for i, step in enumerate(g["iterations"]):
+        k = step["k"]
+        xd = synth.step_inputs(5, 0, 100 + i, B=B, H_kv=H, H_q=H, D=d, k_draft=k,
+                               dtype="f32")
+        k_adm = orc.spec_write(xd["kd"], xd["vd"], k)
+        assert k_adm == k
+        s = orc.stats()
+        wasted = s["capacity"] - s["valid_max"] - s["staged"]
+        assert wasted == step["wasted_after_place"]
+        orc.commit(step["accept"])
+    assert orc.stats()["alloc_events"] - allocs == g["extra_alloc_events_during_sd"]
+
+
+def test_admission_limits_to_free_rows(oracle_mod):
+    """fewer free rows than k -> admit only the free rows, no growth;
+    zero free rows -> k_adm = 0 (plain decode iteration)."""
+    B, H, d, r = 2, 1, 2, 4
+    orc = O.Oracle(B, H, H, d, r, 64, dtype=O.F32, policy=O.POLICY_BMC)
+    for n in range(1, 3):
+        x = synth.step_inputs(6, 0, n, B=B, H_kv=H, H_q=H, D=d, dtype="f32")
+        orc.append(x["k"], x["v"])
+    xd = synth.step_inputs(6, 0, 50, B=B, H_kv=H, H_q=H, D=d, k_draft=5, dtype="f32")
+    assert orc.spec_write(xd["kd"], xd["vd"], 5) == 2
+    assert orc.stats()["alloc_events"] == 1
+    orc.commit(2)
+    assert orc.spec_write(xd["kd"], xd["vd"], 5) == 0
+
+
+# -------------------------------------------------------- attention values
+
+def _one_row_oracle(case):
+    d = case["d"]
+    K, V = np.asarray(case["K"]), np.asarray(case["V"])
+    n = K.shape[0]
+    orc = O.Oracle(1, 1, 1, d, 1, n, dtype=O.F32, policy=O.POLICY_UPFRONT)
+    for j in range(n):
+        orc.append(_f32(K[j]), _f32(V[j]))
+    return orc.sdpa(_f32(case["q"]), n).reshape(d)
+
+
+@pytest.mark.parametrize("name", ["d2_identity", "single_row", "equal_scores", "one_hot"])
+def test_sdpa_brute_force_cases(oracle_mod, name):
+    """tests/golden/sdpa_brute_force.json."""
+    case = next(c for c in _gold("sdpa_brute_force.json")["cases"] if c["name"] == name)
+    exp = np.asarray(case["expected"])
+    got = _one_row_oracle(case)
+    np.testing.assert_allclose(got, exp, rtol=0, atol=1e-15)
+    got2 = O.exact_sdpa(case["q"], case["K"], case["V"])
+    np.testing.assert_allclose(got2, exp, rtol=0, atol=1e-15)
+    if name == "d2_identity":
+        e = math.exp(1 / math.sqrt(2))
+        np.testing.assert_allclose(got, [e / (e + 1), 1 / (e + 1)], rtol=0, atol=1e-15)
+
+
+def test_scale_uses_head_dim(oracle_mod):
+    """Reading R4: the 1/sqrt(D) of P:L275 is 1/sqrt(d), d = head dim, after
+    the MHA reshape to [B*H, 1, d].  Two rows, scores q.k/sqrt(d)
+    = (8/sqrt(4), 0) = (4, 0) -> p = (e^4, 1)/(e^4+1)."""
+    d = 4
+    K = [[2.0, 2.0, 2.0, 2.0], [0.0, 0.0, 0.0, 0.0]]
+    V = [[1.0, 0.0, 0.0, 0.0], [0.0, 1.0, 0.0, 0.0]]
+    got = _one_row_oracle({"d": d, "q": [1.0, 1.0, 1.0, 1.0], "K": K, "V": V})
+    e = math.exp(4.0)
+    np.testing.assert_allclose(got[:2], [e / (e + 1), 1 / (e + 1)], rtol=0, atol=1e-15)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_matches_torch_fp64_sdpa_with_drafts(oracle_mod, dtype):
+    """Library special case: exact-size (no padding) SDPA with a chain-causal
+    boolean mask = torch.nn.functional.scaled_dot_product_attention in fp64
+    (SD query block P:L446; reading R7)."""
+    B, H_kv, H_q, d, n0, k = 2, 2, 4, 8, 11, 3
+    dt = O.F32 if dtype == "f32" else O.BF16
+    orc = O.Oracle(B, H_kv, H_q, d, 1, 64, dtype=dt, policy=O.POLICY_ITERATIVE)
+    Ks, Vs = [], []
+    for n in range(n0):
+        x = synth.step_inputs(7, 0, n, B=B, H_kv=H_kv, H_q=H_q, D=d, dtype=dtype)
+        orc.append(x["k"], x["v"])
+        Ks.append(x["k"]); Vs.append(x["v"])
+    xd = synth.step_inputs(7, 0, 99, B=B, H_kv=H_kv, H_q=H_q, D=d, t=1 + k, k_draft=k,
+                           dtype=dtype)
+    assert orc.spec_write(xd["kd"], xd["vd"], k) == k
+    got = orc.sdpa(xd["q"], n0)
+    Kall = torch.cat([torch.stack(Ks, 2), xd["kd"]], 2).double()     # [B][H_kv][n0+k][d]
+    Vall = torch.cat([torch.stack(Vs, 2), xd["vd"]], 2).double()
+    G = H_q // H_kv
+    Kq = Kall.repeat_interleave(G, dim=1)
+    Vq = Vall.repeat_interleave(G, dim=1)
+    t = 1 + k
+    mask = torch.zeros(t, n0 + k, dtype=torch.bool)
+    for tau in range(t):
+        mask[tau, : n0 + tau] = True
+    ref = torch.nn.functional.scaled_dot_product_attention(
+        xd["q"].double(), Kq, Vq, attn_mask=mask)
+    np.testing.assert_allclose(got, ref.numpy(), rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("r", [1, 3, 8, 16, 40])
+def test_mask_invariance_bit_exact(oracle_mod, r):
+    """the -1e9 bias on padded rows leaves SDPA equal to exact-
+    prefix SDPA.  In fp64 the masked p_j are exactly 0 and trail the sums, so
+    the result is bit-identical for every r; padded mass < 1e-30."""
+    B, H, d, N = 1, 2, 8, 40
+    orc = O.Oracle(B, H, H, d, r, N, dtype=O.F32, policy=O.POLICY_BMC)
+    Ks, Vs = [], []
+    for n in range(1, N + 1):
+        x = synth.step_inputs(11, 0, n, B=B, H_kv=H, H_q=H, D=d, dtype="f32",
+                              variant="peaky" if n % 3 == 0 else "normal")
+        orc.append(x["k"], x["v"])
+        Ks.append(x["k"].numpy()); Vs.append(x["v"].numpy())
+        if n % 5 != 0 and n != N:
+            continue
+        got = orc.sdpa(x["q"], n)
+        for hh in range(H):
+            K = np.stack([k[0, hh] for k in Ks]).astype(np.float64)
+            V = np.stack([v[0, hh] for v in Vs]).astype(np.float64)
+            ref = O.exact_sdpa(x["q"].numpy()[0, hh, 0], K, V)
+            assert np.array_equal(got[0, hh, 0], ref)
+    assert math.exp(-1e9 + 50.0) < 1e-30
+
+
+def test_gqa_equals_replicated_mha(oracle_mod):
+    """P:L834-844 / S:L173: GQA output equals MHA with every KV head
+    replicated G times (query head h reads KV head floor(h/G), reading R6)."""
+    B, H_kv, H_q, d, N, r = 2, 2, 8, 4, 13, 4
+    G = H_q // H_kv
+    gq = O.Oracle(B, H_kv, H_q, d, r, N, dtype=O.BF16, policy=O.POLICY_BMC)
+    mh = O.Oracle(B, H_q, H_q, d, r, N, dtype=O.BF16, policy=O.POLICY_BMC)
+    for n in range(1, N + 1):
+        x = synth.step_inputs(13, 0, n, B=B, H_kv=H_kv, H_q=H_q, D=d, dtype="bf16")
+        gq.append(x["k"], x["v"])
+        mh.append(x["k"].repeat_interleave(G, 1), x["v"].repeat_interleave(G, 1))
+        assert np.array_equal(gq.sdpa(x["q"], n), mh.sdpa(x["q"], n))
+
+
+# ------------------------------------------------------- policy degeneracy
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_bmc_r1_equals_iterative(oracle_mod, dtype):
+    """T = N/r: r=1 reallocates every token like iterative
+    allocation: same contents, allocation/copy counts and
+    bit-identical fp64 outputs from independent code paths."""
+    kw = dict(B=2, H_kv=2, H_q=4, D=8, N=24, dtype=dtype)
+    bm, ob = _run_decode(O.POLICY_BMC, r=1, **kw)
+    it, oi = _run_decode(O.POLICY_ITERATIVE, r=1, **kw)
+    for a, b in zip(ob, oi):
+        assert np.array_equal(a, b)
+    sb, si = bm.stats(), it.stats()
+    for key in ("alloc_events", "copy_events", "copied_bytes", "init_written_bytes",
+                "append_written_bytes", "capacity", "macs"):
+        assert sb[key] == si[key], key
+    for x, y in zip(bm.read_cache(), it.read_cache()):
+        assert np.array_equal(x, y)
+
+
+def test_bmc_rN_equals_upfront(oracle_mod):
+    """r = N gives T = 1 allocation, i.e. upfront."""
+    kw = dict(B=2, H_kv=1, H_q=2, D=8, N=20, dtype="bf16")
+    bm, ob = _run_decode(O.POLICY_BMC, r=20, **kw)
+    up, ou = _run_decode(O.POLICY_UPFRONT, r=20, **kw)
+    for a, b in zip(ob, ou):
+        assert np.array_equal(a, b)
+    sb, su = bm.stats(), up.stats()
+    assert sb["alloc_events"] == su["alloc_events"] == 1
+    assert sb["copied_bytes"] == su["copied_bytes"] == 0
+    assert sb["macs"] == su["macs"]
+    for x, y in zip(bm.read_cache(), up.read_cache()):
+        assert np.array_equal(x, y)
+
+
+def test_content_equivalence_across_policies(oracle_mod):
+    """after identical appends the committed rows are bitwise identical
+    across iterative, upfront and BMC(r); padded rows are zero."""
+    kw = dict(B=2, H_kv=2, H_q=2, D=4, N=19, dtype="bf16", sdpa=False)
+    caches = []
+    for pol, r in ((O.POLICY_ITERATIVE, 1), (O.POLICY_UPFRONT, 19), (O.POLICY_BMC, 5),
+                   (O.POLICY_BMC, 7)):
+        orc, _ = _run_decode(pol, r=r, N=19, **{k: v for k, v in kw.items() if k != "N"})
+        K, V = orc.read_cache()
+        assert not K[:, 19:].any() and not V[:, 19:].any()
+        caches.append((K[:, :19], V[:, :19]))
+    for K, V in caches[1:]:
+        assert np.array_equal(K, caches[0][0]) and np.array_equal(V, caches[0][1])
+
+
+def test_unmasked_upfront_is_wrong(oracle_mod):
+    """Negative test: without the mask the e^0 = 1 terms of zero rows
+    change the output; with it the output matches the exact prefix."""
+    d = 2
+    q = np.array([1.0, 0.5]); K = np.array([[1.0, 0.0]]); V = np.array([[2.0, -1.0]])
+    masked = _one_row_oracle({"d": d, "q": q, "K": K, "V": V})   # exact, 1 row
+    Kpad = np.vstack([K, np.zeros((3, d))]); Vpad = np.vstack([V, np.zeros((3, d))])
+    unmasked = O.exact_sdpa(q, Kpad, Vpad)                        # softmax over zeros too
+    assert np.array_equal(masked, V[0])
+    assert not np.allclose(unmasked, V[0])
+
+
+# -------------------------------------------------------- speculative commit
+
+def test_commit_equals_sequential_appends(oracle_mod):
+    """S:L362-366 / P:L447: committing the m accepted chain drafts gives the
+    cache that m plain appends of the same rows give; rejected rows are zero
+    again (reading R9), capacity unchanged during speculation."""
+    B, H, d, r, N = 2, 2, 4, 8, 64
+    a = O.Oracle(B, H, H, d, r, N, dtype=O.BF16, policy=O.POLICY_BMC)
+    b = O.Oracle(B, H, H, d, r, N, dtype=O.BF16, policy=O.POLICY_BMC)
+    for n in range(3):
+        x = synth.step_inputs(17, 0, n, B=B, H_kv=H, H_q=H, D=d, dtype="bf16")
+        a.append(x["k"], x["v"]); b.append(x["k"], x["v"])
+    k, m = 4, 2
+    xd = synth.step_inputs(17, 0, 77, B=B, H_kv=H, H_q=H, D=d, k_draft=k, t=1 + k,
+                           dtype="bf16")
+    cap0 = a.stats()["capacity"]
+    assert a.spec_write(xd["kd"], xd["vd"], k) == k
+    a.sdpa(xd["q"], 3)
+    a.commit(m)
+    assert a.stats()["capacity"] == cap0
+    for i in range(m):
+        b.append(xd["kd"][:, :, i].contiguous(), xd["vd"][:, :, i].contiguous())
+    for x, y in zip(a.read_cache(), b.read_cache()):
+        assert np.array_equal(x, y)
+    K, V = a.read_cache()
+    assert not K[:, 3 + m:].any() and not V[:, 3 + m:].any()
+
+
+def test_commit_rows_per_row_lengths(oracle_mod):
+    """Reading R11: per-row acceptance at B > 1; masks use each row's length."""
+    B, H, d, r, N = 3, 1, 4, 16, 64
+    orc = O.Oracle(B, H, H, d, r, N, dtype=O.F32, policy=O.POLICY_BMC)
+    x = synth.step_inputs(19, 0, 0, B=B, H_kv=H, H_q=H, D=d, dtype="f32")
+    orc.append(x["k"], x["v"])
+    xd = synth.step_inputs(19, 0, 1, B=B, H_kv=H, H_q=H, D=d, k_draft=3, t=4, dtype="f32")
+    orc.spec_write(xd["kd"], xd["vd"], 3)
+    orc.commit_rows([0, 3, 1])
+    assert list(orc.valid()) == [1, 4, 2]
+    q = synth.step_inputs(19, 0, 2, B=B, H_kv=H, H_q=H, D=d, dtype="f32")["q"]
+    with pytest.raises(O.OracleError):
+        orc.sdpa(q, 1)                                  # not uniform -> STATE
+    out = orc.sdpa(q, -1)
+    K, V = orc.read_cache()
+    for b, n in enumerate([1, 4, 2]):
+        ref = O.exact_sdpa(q.numpy()[b, 0, 0], K[b, :n].astype(np.float64),
+                           V[b, :n].astype(np.float64))
+        assert np.array_equal(out[b, 0, 0], ref)
+
+
+def test_error_codes(oracle_mod):
+    """Boundary errors: CAPACITY at N_max, STATE for a
+    second spec_write / append while staged, ARG for bad commits and n_valid=0."""
+    orc = O.Oracle(1, 1, 1, 2, 2, 2, dtype=O.F32, policy=O.POLICY_BMC)
+    z = _f32([0.5, 0.5])
+    orc.append(z, z); orc.append(z, z)
+    with pytest.raises(O.OracleError) as e:
+        orc.append(z, z)
+    assert e.value.code == -3
+    with pytest.raises(O.OracleError) as e:
+        orc.commit(1)
+    assert e.value.code == -2
+    with pytest.raises(O.OracleError) as e:
+        orc.sdpa(_f32([1, 1]), 0)
+    assert e.value.code == -1
+    with pytest.raises(O.OracleError) as e:
+        O.Oracle(1, 3, 4, 2, 2, 2)
+    assert e.value.code == -1
+    o2 = O.Oracle(1, 1, 1, 2, 4, 8, dtype=O.F32, policy=O.POLICY_BMC)
+    o2.append(z, z)
+    kd = _f32([[1, 2], [3, 4]])
+    assert o2.spec_write(kd, kd, 2) == 2
+    with pytest.raises(O.OracleError) as e:
+        o2.spec_write(kd, kd, 2)
+    assert e.value.code == -2
+    with pytest.raises(O.OracleError) as e:
+        o2.append(z, z)
+    assert e.value.code == -2
+    with pytest.raises(O.OracleError) as e:
+        o2.commit(3)
+    assert e.value.code == -1
+
+
+def test_footprint_example():
+    """B=64, L=64, D=4096, N=2048 half precision K and V need ~137 GB
+    (the layout's bytes per row x rows, 2 tensors)."""
+    B, L, D, N, eb = 64, 64, 4096, 2048, 2
+    assert abs(2 * B * L * N * D * eb / 1e9 - 137.4) < 0.1
