@@ -1,0 +1,168 @@
+/*
+ * bmc.h -- C ABI of the B200-native BMC decode hot path (libbmc.so).
+ *
+ * BMC = "Balancing Memory and Compute" (arXiv 2511.12031; PAPER.md is cited
+ * as P:L<line>).  One handle holds ONE layer's K and V cache, each laid out
+ * [B*H_kv][cap][D] row-major, contiguous per (batch, kv-head) unit, grown in
+ * r-row chunks.  A model is L handles.
+ *
+ * Conventions for every call
+ *   - Returns 0 (BMC_OK) or a negative bmc_status.  All argument/state
+ *     validation happens BEFORE anything is enqueued, so an error leaves the
+ *     handle unchanged.  bmc_last_error() gives a thread-local message.
+ *   - Tensor pointers may be CUDA device pointers on the handle's device
+ *     (the fast path) or host pointers (pageable or pinned).  Host inputs are
+ *     copied to a device staging buffer inside the call (stream-ordered; a
+ *     pinned input must not be modified until the stream has passed the
+ *     call).  A pageable host output makes the call wait for its stream
+ *     before returning; a pinned host output is written asynchronously (read
+ *     it after bmc_sync or another stream synchronisation).
+ *   - Work is stream-ordered on the handle's stream; device-pointer calls
+ *     never synchronise the device.  The host tracks every length itself
+ *     (no device->host reads on the hot path).
+ *   - The caller owns K, V, K_draft, V_draft, Q, O and must keep device
+ *     buffers alive until the stream has passed the call.  The library owns
+ *     the cache memory (per-handle arena) and its workspace.
+ *   - Single writer per handle.  Distinct handles are independent.
+ *   - Inputs are stored bit-for-bit (no dtype conversion in append/spec);
+ *     inputs must already be in the cache dtype.
+ *   - Error codes:
+ *       BMC_ERR_ARG        bad dims (<1, H_q % H_kv != 0, r outside [1,N_max]),
+ *                          null pointers, k < 0, n_accepted outside [0, staged],
+ *                          n_valid == 0 or any committed length == 0 at sdpa;
+ *       BMC_ERR_STATE      append/spec_write while drafts are staged, n_valid
+ *                          not equal to the committed length, commit of
+ *                          n_accepted > 0 with nothing staged;
+ *       BMC_ERR_CAPACITY   append when a row already holds N_max tokens;
+ *       BMC_ERR_OOM        device memory exhausted;
+ *       BMC_ERR_CUDA       CUDA error (sticky: the handle is usable only for
+ *                          bmc_destroy);
+ *       BMC_ERR_UNSUPPORTED D not in {64,128}, B > BMC_MAX_B, dtype not built.
+ */
+#ifndef BMC_H
+#define BMC_H
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct bmc_ctx* bmc_t;
+
+typedef enum {
+  BMC_OK = 0,
+  BMC_ERR_ARG = -1,
+  BMC_ERR_STATE = -2,
+  BMC_ERR_CAPACITY = -3,
+  BMC_ERR_OOM = -4,
+  BMC_ERR_CUDA = -5,
+  BMC_ERR_UNSUPPORTED = -6
+} bmc_status;
+
+typedef enum { BMC_F32 = 0, BMC_BF16 = 1 } bmc_dtype;
+
+/* Allocation policy.  BMC: grow by r rows when full.
+   ITERATIVE: exact-size reallocation + copy for every new row block
+   (the HuggingFace baseline).  UPFRONT: one N_max allocation,
+   in-place writes, masked SDPA over all N_max rows. */
+typedef enum { BMC_POLICY_BMC = 0, BMC_POLICY_ITERATIVE = 1, BMC_POLICY_UPFRONT = 2 } bmc_policy;
+
+#define BMC_PER_ROW (-1) /* bmc_sdpa n_valid: use every batch row's own length */
+#define BMC_MAX_B 256    /* batch rows per handle (per GPU shard) */
+
+/* bmc_create: bf16 cache, BMC policy, current device, default stream.
+   B batch rows, H_kv key/value heads, H_q query heads (GQA group
+   G = H_q/H_kv; query head h reads kv head floor(h/G)),
+   D head dim (64 or 128), r chunk rows (1 <= r <= N_max; T = N_max/r
+   allocations), N_max maximum context.  The first allocation
+   of min(r, N_max) zeroed rows happens here (UPFRONT: N_max rows;
+   ITERATIVE: none). */
+int bmc_create(int B, int H_kv, int H_q, int D, int r, int N_max, bmc_t* out);
+
+/* As bmc_create with explicit dtype, policy, CUDA device ordinal (-1 =
+   current) and stream (a cudaStream_t, NULL = the legacy default stream). */
+int bmc_create_ex(int B, int H_kv, int H_q, int D, int r, int N_max, bmc_dtype dt,
+                  bmc_policy pol, int device, void* cuda_stream, bmc_t* out);
+
+/* bmc_append: KV cache update of one decode step.
+   K, V: [B][H_kv][D] in the cache dtype.  Writes row valid_b of every unit
+   of batch row b, then valid_b += 1.  BMC: if max_b valid_b == cap first
+   grows to min(cap + r, N_max): new buffer, strided copy of the cap old rows
+   of every unit, zero-fill of the new rows.  ITERATIVE: always
+   reallocates to exactly max valid + 1 rows.  Errors: STATE if drafts are
+   staged, CAPACITY if max valid == N_max. */
+int bmc_append(bmc_t h, const void* K, const void* V);
+
+/* bmc_spec_write: place k chain-draft rows in the padded rows.
+   K_draft, V_draft: [B][H_kv][k][D].  Admits k_adm = min(k, cap - max valid)
+   drafts (BMC, UPFRONT: never grows) or min(k, N_max - max valid)
+   (ITERATIVE: exact-size reallocation).  Writes rows valid_b .. valid_b+k_adm-1,
+   staged = k_adm.  Returns k_adm >= 0, or < 0 on error (STATE if drafts
+   are already staged). */
+int bmc_spec_write(bmc_t h, const void* K_draft, const void* V_draft, int k);
+
+/* bmc_sdpa: masked scaled-dot-product attention over ALL cap rows of the
+   padded cache (mask P:L846-853).
+   Q: [B][H_q][t][D] in the cache dtype, t = 1 + staged (implicit).  Query
+   row tau of batch row b attends keys [0, valid_b + tau) (row 0 = last
+   committed token, rows >= 1 = chain drafts); every other row of the buffer
+   is masked (it is still read).  O: [B][H_q][t][D] float32 =
+   softmax(q K^T / sqrt(D) + mask) V with fp32 accumulation.
+   n_valid: the committed length (must equal every valid_b), or BMC_PER_ROW. */
+int bmc_sdpa(bmc_t h, const void* Q, int n_valid, float* O);
+
+/* bmc_commit: accept the first n_accepted staged drafts of every row,
+   valid_b += n_accepted; rejected staged rows are zeroed again; staged = 0. */
+int bmc_commit(bmc_t h, int n_accepted);
+
+/* bmc_commit_rows: per-row acceptance, n_accepted_host[B] (host array). */
+int bmc_commit_rows(bmc_t h, const int* n_accepted_host);
+
+/* bmc_destroy: synchronises the handle's stream, frees the cache memory. */
+int bmc_destroy(bmc_t h);
+
+/* Host-side shadow state and cost ledger; no device synchronisation. */
+typedef struct {
+  long long valid_min, valid_max, capacity, staged;
+  long long alloc_events, copy_events;
+  long long copied_bytes;          /* payload moved by reallocation copies, K+V */
+  long long init_written_bytes;    /* bytes written into new buffers (copy + zero) */
+  long long append_written_bytes;  /* rows written by append / spec_write, K+V */
+  long long kv_bytes_read;         /* K+V bytes read by SDPA (all cap rows) */
+  long long macs;                  /* 2*B*H_q*t*cap*D per SDPA call */
+  long long sdpa_calls;
+} bmc_stats_t;
+int bmc_stats(bmc_t h, bmc_stats_t* out);
+
+/* Current cache buffers (device pointers, [B*H_kv][cap][D]) and capacity.
+   Invalidated by the next growth. */
+int bmc_kv_view(bmc_t h, void** K, void** V, int* cap);
+
+/* Copy the whole cache [B*H_kv][cap][D] (cache dtype) into K_dst / V_dst
+   (device or host buffers of bmc_stats().capacity rows); waits for the copy
+   when a destination is host memory.  Inspection only (bit-exact checks). */
+int bmc_read_cache(bmc_t h, void* K_dst, void* V_dst);
+
+/* Committed length of every batch row, valid_host[B]. */
+int bmc_valid(bmc_t h, int* valid_host);
+
+/* Wait for all work enqueued on the handle's stream. */
+int bmc_sync(bmc_t h);
+
+/* Tuning / test options (key, value).  Keys:
+     1 BMC_OPT_ATTN_CTAS      CTAs of the attention kernel (0 = auto)
+     2 BMC_OPT_ATTN_PATH      0 auto, 1 CUDA-core split-K, 2 tcgen05 verify
+     3 BMC_OPT_ARENA          0 VMM arena (default), 1 stream-ordered pool  */
+#define BMC_OPT_ATTN_CTAS 1
+#define BMC_OPT_ATTN_PATH 2
+#define BMC_OPT_ARENA 3
+int bmc_set_option(bmc_t h, int key, long long value);
+
+/* Kernels launched by this library in this process so far (all handles). */
+unsigned long long bmc_launch_count(void);
+
+/* Thread-local message for the last error (empty string if none). */
+const char* bmc_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

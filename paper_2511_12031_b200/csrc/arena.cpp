@@ -1,0 +1,304 @@
+// arena.cpp -- chunk-growth allocator for the BMC KV cache.
+//
+// BMC reallocates every r tokens; the paper's implementation
+// calls the framework allocator each time.  Here a handle
+// (one layer) owns one Arena:
+//   kind 0 (VMM, default): for each tensor (K, V) two ping-pong slots of
+//     reserved virtual address space, each large enough for N_max rows.  A
+//     growth maps physical chunks (cuMemCreate, from a process-wide pool) into
+//     the slot not holding the live buffer, the realloc kernel copies, and the
+//     old slot is released once the stream has passed the copy (CUDA event):
+//     its chunks are unmapped and returned to the pool for any layer's next
+//     growth.  No cudaMalloc/cudaFree on the hot path; virtual addresses of a
+//     handle only ever take two values per tensor.
+//   kind 1 (pool): cudaMallocFromPoolAsync / cudaFreeAsync on a per-device
+//     memory pool with an unbounded release threshold (stream-ordered reuse).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <map>
+#include <mutex>
+#include <set>
+#include <vector>
+
+#include "bmc_internal.h"
+
+namespace bmc {
+
+namespace {
+
+struct ChunkPool {
+  int device = 0;
+  size_t chunk = 0;
+  std::vector<CUmemGenericAllocationHandle> free_list;
+};
+
+struct Slot {
+  std::vector<CUmemGenericAllocationHandle> chunks;  // mapped, in address order
+  cudaEvent_t pending = nullptr;                          // release requested, not yet reclaimed
+};
+
+// Driver entry points resolved through the runtime at first use, so that
+// libbmc.so does not link libcuda.so.1 (it loads on machines without a GPU).
+struct Driver {
+  PFN_cuMemGetAllocationGranularity granularity = nullptr;
+  PFN_cuMemAddressReserve reserve = nullptr;
+  PFN_cuMemAddressFree addr_free = nullptr;
+  PFN_cuMemCreate create = nullptr;
+  PFN_cuMemMap map = nullptr;
+  PFN_cuMemUnmap unmap = nullptr;
+  PFN_cuMemSetAccess set_access = nullptr;
+  PFN_cuDeviceGet device_get = nullptr;
+  PFN_cuDeviceGetAttribute device_attr = nullptr;
+  bool ok = false;
+  bool tried = false;
+};
+Driver g_drv;
+
+template <typename F>
+bool resolve(const char* name, F* fn) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess || !p)
+    return false;
+  *fn = reinterpret_cast<F>(p);
+  return true;
+}
+
+const Driver& drv() {
+  if (!g_drv.tried) {
+    g_drv.tried = true;
+    g_drv.ok = resolve("cuMemGetAllocationGranularity", &g_drv.granularity) &&
+               resolve("cuMemAddressReserve", &g_drv.reserve) &&
+               resolve("cuMemAddressFree", &g_drv.addr_free) &&
+               resolve("cuMemCreate", &g_drv.create) && resolve("cuMemMap", &g_drv.map) &&
+               resolve("cuMemUnmap", &g_drv.unmap) &&
+               resolve("cuMemSetAccess", &g_drv.set_access) &&
+               resolve("cuDeviceGet", &g_drv.device_get) &&
+               resolve("cuDeviceGetAttribute", &g_drv.device_attr);
+  }
+  return g_drv;
+}
+
+std::mutex g_mu;
+std::map<std::pair<int, size_t>, ChunkPool*> g_pools;
+std::map<int, cudaMemPool_t> g_mempools;
+std::set<Arena*> g_arenas;
+
+}  // namespace
+
+struct Arena {
+  int device = 0;
+  size_t slot_bytes = 0;  // reserved VA per slot (multiple of chunk)
+  size_t chunk = 0;
+  CUdeviceptr base = 0;
+  Slot slots[2][2];       // [tensor][slot]
+  int live[2] = {-1, -1}; // live VMM slot per tensor
+  ChunkPool* pool = nullptr;
+  bool vmm_ok = false;
+};
+
+static int cu_ok(CUresult r) { return r == CUDA_SUCCESS ? 0 : BMC_ERR_CUDA; }
+
+static size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+static ChunkPool* pool_for(int device, size_t chunk) {
+  auto key = std::make_pair(device, chunk);
+  auto it = g_pools.find(key);
+  if (it != g_pools.end()) return it->second;
+  ChunkPool* p = new ChunkPool();
+  p->device = device;
+  p->chunk = chunk;
+  g_pools[key] = p;
+  return p;
+}
+
+static cudaMemPool_t mempool_for(int device) {
+  auto it = g_mempools.find(device);
+  if (it != g_mempools.end()) return it->second;
+  cudaMemPoolProps props = {};
+  props.allocType = cudaMemAllocationTypePinned;
+  props.handleTypes = cudaMemHandleTypeNone;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = device;
+  cudaMemPool_t mp = nullptr;
+  if (cudaMemPoolCreate(&mp, &props) != cudaSuccess) return nullptr;
+  unsigned long long thr = ~0ull;
+  cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &thr);
+  g_mempools[device] = mp;
+  return mp;
+}
+
+// Unmap a slot's chunks and give them back to the pool (caller holds g_mu and
+// has established that the GPU is done with the slot).
+static void unmap_slot(Arena* a, Slot& s, int tensor, int slot) {
+  CUdeviceptr va = a->base + (CUdeviceptr)((tensor * 2 + slot) * a->slot_bytes);
+  if (!s.chunks.empty()) drv().unmap(va, s.chunks.size() * a->chunk);
+  for (auto h : s.chunks) a->pool->free_list.push_back(h);
+  s.chunks.clear();
+  if (s.pending) {
+    cudaEventDestroy(s.pending);
+    s.pending = nullptr;
+  }
+}
+
+// Reclaim every released slot whose event has completed (all arenas).
+static void reclaim_locked() {
+  for (Arena* a : g_arenas) {
+    for (int t = 0; t < 2; ++t)
+      for (int s = 0; s < 2; ++s) {
+        Slot& sl = a->slots[t][s];
+        if (sl.pending && cudaEventQuery(sl.pending) == cudaSuccess) unmap_slot(a, sl, t, s);
+      }
+  }
+}
+
+Arena* arena_create(int device, size_t max_bytes_per_tensor, int* err) {
+  *err = 0;
+  Arena* a = new Arena();
+  a->device = device;
+  std::lock_guard<std::mutex> lk(g_mu);
+  // VMM setup (kind 0); falls back to pool-only if unsupported.
+  int vmm = 0;
+  CUdevice dev = 0;
+  if (drv().ok && drv().device_get(&dev, device) == CUDA_SUCCESS &&
+      drv().device_attr(&vmm, CU_DEVICE_ATTRIBUTE_VIRTUAL_MEMORY_MANAGEMENT_SUPPORTED, dev) ==
+          CUDA_SUCCESS &&
+      vmm) {
+    CUmemAllocationProp prop = {};
+    prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    prop.location.id = device;
+    size_t gran = 0;
+    if (drv().granularity(&gran, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED) ==
+            CUDA_SUCCESS &&
+        gran > 0) {
+      // chunk: >= 1/16 of the largest buffer (few map calls per growth),
+      // 2 MiB for small caches, at most 64 MiB.
+      size_t chunk = gran;
+      while (chunk < max_bytes_per_tensor / 16 && chunk < (64u << 20)) chunk *= 2;
+      a->chunk = chunk;
+      a->slot_bytes = round_up(std::max<size_t>(max_bytes_per_tensor, 1), chunk);
+      if (drv().reserve(&a->base, 4 * a->slot_bytes, chunk, 0, 0) == CUDA_SUCCESS) {
+        a->pool = pool_for(device, chunk);
+        a->vmm_ok = true;
+      }
+    }
+  }
+  g_arenas.insert(a);
+  return a;
+}
+
+static int map_slot(Arena* a, int tensor, int slot, size_t bytes) {
+  Slot& sl = a->slots[tensor][slot];
+  const size_t need = (bytes + a->chunk - 1) / a->chunk;
+  CUdeviceptr va = a->base + (CUdeviceptr)((tensor * 2 + slot) * a->slot_bytes);
+  const size_t have = sl.chunks.size();
+  if (need <= have) return 0;
+  CUmemAllocationProp prop = {};
+  prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  prop.location.id = a->device;
+  for (size_t i = have; i < need; ++i) {
+    CUmemGenericAllocationHandle h;
+    if (!a->pool->free_list.empty()) {
+      h = a->pool->free_list.back();
+      a->pool->free_list.pop_back();
+    } else {
+      CUresult r = drv().create(&h, a->chunk, &prop, 0);
+      if (r == CUDA_ERROR_OUT_OF_MEMORY) return BMC_ERR_OOM;
+      if (r != CUDA_SUCCESS) return BMC_ERR_CUDA;
+    }
+    if (drv().map(va + i * a->chunk, a->chunk, 0, h, 0) != CUDA_SUCCESS) {
+      a->pool->free_list.push_back(h);
+      return BMC_ERR_CUDA;
+    }
+    sl.chunks.push_back(h);
+  }
+  CUmemAccessDesc acc = {};
+  acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  acc.location.id = a->device;
+  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  return cu_ok(drv().set_access(va + have * a->chunk, (need - have) * a->chunk, &acc, 1));
+}
+
+int arena_alloc(Arena* a, int tensor, size_t bytes, int kind, const Buffer* keep,
+                cudaStream_t s, Buffer* out) {
+  // `keep` is the tensor's live buffer (its slot is not reused).
+  *out = Buffer();
+  if (bytes == 0) bytes = 16;
+  if (kind == 0 && a->vmm_ok) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    reclaim_locked();
+    int slot = (keep && keep->ptr && keep->kind == 0) ? 1 - keep->slot : 0;
+    Slot& sl = a->slots[tensor][slot];
+    if (sl.pending) {  // the GPU may still read it: wait for the release event
+      cudaEventSynchronize(sl.pending);
+      unmap_slot(a, sl, tensor, slot);
+    }
+    int rc = map_slot(a, tensor, slot, bytes);
+    if (rc) return rc;
+    out->ptr = (void*)(a->base + (CUdeviceptr)((tensor * 2 + slot) * a->slot_bytes));
+    out->bytes = bytes;
+    out->slot = slot;
+    out->kind = 0;
+    a->live[tensor] = slot;
+    return 0;
+  }
+  cudaMemPool_t mp;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    mp = mempool_for(a->device);
+  }
+  if (!mp) return BMC_ERR_CUDA;
+  void* p = nullptr;
+  cudaError_t e = cudaMallocFromPoolAsync(&p, bytes, mp, s);
+  if (e == cudaErrorMemoryAllocation) return BMC_ERR_OOM;
+  if (e != cudaSuccess) return BMC_ERR_CUDA;
+  out->ptr = p;
+  out->bytes = bytes;
+  out->slot = -1;
+  out->kind = 1;
+  return 0;
+}
+
+int arena_release(Arena* a, Buffer* b, cudaStream_t s) {
+  if (!b->ptr) return 0;
+  int rc = 0;
+  if (b->kind == 1) {
+    rc = cudaFreeAsync(b->ptr, s) == cudaSuccess ? 0 : BMC_ERR_CUDA;
+  } else {
+    std::lock_guard<std::mutex> lk(g_mu);
+    const int tensor = (int)(((CUdeviceptr)b->ptr - a->base) / a->slot_bytes) / 2;
+    Slot& sl = a->slots[tensor][b->slot];
+    cudaEvent_t ev = nullptr;
+    if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventRecord(ev, s) != cudaSuccess) {
+      rc = BMC_ERR_CUDA;
+    } else {
+      if (sl.pending) cudaEventDestroy(sl.pending);
+      sl.pending = ev;
+    }
+  }
+  *b = Buffer();
+  return rc;
+}
+
+void arena_destroy(Arena* a) {
+  if (!a) return;
+  std::lock_guard<std::mutex> lk(g_mu);
+  for (int t = 0; t < 2; ++t)
+    for (int s = 0; s < 2; ++s) {
+      Slot& sl = a->slots[t][s];
+      if (sl.pending) cudaEventSynchronize(sl.pending);
+      if (a->vmm_ok) unmap_slot(a, sl, t, s);
+    }
+  if (a->base) drv().addr_free(a->base, 4 * a->slot_bytes);
+  g_arenas.erase(a);
+  delete a;
+}
+
+}  // namespace bmc

@@ -1,0 +1,567 @@
+// attn_decode.cu -- fused masked decode / small-M verify attention over the
+// padded BMC cache, CUDA cores, sm_100a.
+//
+// What it computes (mask P:L846-853, GQA P:L834-844,
+// SD query block P:L444-448): for every (batch b, kv head g) unit and each of
+// its M = G*t query rows (query head h = g*G + m/t, chain position tau = m%t)
+//     o = softmax(q K^T / sqrt(D) + bias) V,  bias_j = 0 if j < valid_b + tau
+//                                             else masked,
+// over ALL cap rows of the unit's slab.  Padded rows are read from HBM (the
+// method's contract: they cost bandwidth) but get probability exactly 0.
+//
+// Design:
+//  * The whole launch is one stream of 16 KiB tiles: tile i covers rows
+//    [j*TR, j*TR+TR) of unit u, i = u*TPU + j.  Each CTA (one per SM,
+//    persistent) takes a contiguous, equal share of that stream (split-K
+//    across the sequence AND across units), so every SM streams the same
+//    number of bytes regardless of B*H_kv or cap.
+//  * Thread 0 also acts as the producer: it moves K and V tiles into a
+//    4-stage shared-memory ring with cp.async.bulk (TMA bulk copies; each
+//    tile is a contiguous slab range) completing on mbarriers, refilling a
+//    stage as soon as all 8 warps released it.  No warp touches HBM for K/V
+//    through registers.
+//  * 8 consumer warps each own TR/8 rows of every tile and keep their own
+//    online-softmax state (running max, per-lane partial sums and outputs) in
+//    fp32 registers; q is held pre-scaled by log2(e)/sqrt(D) and scores use
+//    exp2.  Dot products use packed FFMA2; the per-row reduction uses warp
+//    shuffles over the lanes that split the row.
+//  * At a unit boundary the warps merge in shared memory.  A unit covered by
+//    one CTA writes O directly; otherwise each CTA writes a partial
+//    (max, sum, o) record and the last CTA to finish the unit (atomic
+//    arrival counter) merges the records and writes O (split-K combine).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "bmc_internal.h"
+
+namespace bmc {
+namespace attn {
+
+constexpr int kStageBytes = 16384;  // per operand (K or V) per stage
+constexpr int kStages = 4;
+constexpr int kConsumerWarps = 8;
+constexpr int kThreads = kConsumerWarps * 32;  // 2 warps per SMSP -> 255-register budget
+constexpr float kLog2e = 1.4426950408889634f;
+
+// ------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ void consumer_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
+}
+
+// 16-byte chunk -> float pairs (exact widening)
+template <typename T>
+struct Chunk;
+template <>
+struct Chunk<__nv_bfloat16> {
+  static constexpr int EPC = 8;  // elements per 16-byte chunk
+  __device__ static __forceinline__ void load(const uint4 c, float2* f) {
+    const uint32_t w[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      f[i] = make_float2(__uint_as_float(w[i] << 16), __uint_as_float(w[i] & 0xffff0000u));
+  }
+};
+template <>
+struct Chunk<float> {
+  static constexpr int EPC = 4;
+  __device__ static __forceinline__ void load(const uint4 c, float2* f) {
+    f[0] = make_float2(__uint_as_float(c.x), __uint_as_float(c.y));
+    f[1] = make_float2(__uint_as_float(c.z), __uint_as_float(c.w));
+  }
+};
+
+struct Params {
+  const uint8_t* K;
+  const uint8_t* V;
+  const uint8_t* Q;
+  float* O;
+  float* ws;
+  int* counters;
+  long long cap;
+  long long total_tiles;  // U * TPU
+  int tpu;                // tiles per unit
+  int H_kv, H_q, G, t;
+  int M;                  // query rows handled by this launch (<= MAXM)
+  int m0;                 // first query row of the unit handled by this launch
+  int Mu;                 // query rows per unit (G * t)
+  int ctas;
+  float qscale;           // log2(e) / sqrt(D)
+  int valid[BMC_MAX_B];
+};
+
+template <typename T, int D, int MAXM, int CPL>
+struct Cfg {
+  static constexpr int ROWB = D * (int)sizeof(T);
+  static constexpr int CH = ROWB / 16;          // chunks per row
+  static constexpr int LPR = CH / CPL;          // lanes per row
+  static constexpr int RPP = 32 / LPR;          // rows per warp pass
+  static constexpr int TR = kStageBytes / ROWB; // rows per tile
+  static constexpr int RPW = TR / kConsumerWarps;
+  static constexpr int PASSES = RPW / RPP;
+  static constexpr int EPC = Chunk<T>::EPC;
+  static constexpr int EL2 = CPL * EPC / 2;     // float2 per lane per row
+  static_assert(LPR >= 1 && LPR <= 32 && RPW % RPP == 0 && PASSES >= 1, "bad tiling");
+  static_assert(CPL == 1 || CPL == 2, "CPL");
+  static constexpr size_t kRing = (size_t)kStages * 2 * kStageBytes;
+  static constexpr size_t kMerge = (size_t)kConsumerWarps * MAXM * D * 4;
+  static constexpr size_t kSmall = (size_t)kConsumerWarps * MAXM * 2 * 4 + 64;
+  static constexpr size_t kBars = 2 * kStages * 8;
+  static constexpr size_t kSmem = kRing + kMerge + kSmall + kBars + 128;
+};
+
+// CTA owning global tile x in the equal partition t0(c) = floor(c*NT/C).
+__device__ __forceinline__ int cta_of_tile(long long x, long long NT, int C) {
+  return (int)(((x + 1) * C + NT - 1) / NT) - 1;
+}
+__device__ __forceinline__ long long tile_begin(int c, long long NT, int C) {
+  return (long long)c * NT / C;
+}
+
+template <typename T, int D, int MAXM, int CPL>
+__global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(const Params p) {
+  using C = Cfg<T, D, MAXM, CPL>;
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t* ring = smem;                                             // [stage][K|V][16 KiB]
+  float* sm_o = reinterpret_cast<float*>(smem + C::kRing);          // [warp][MAXM][D]
+  float* sm_m = sm_o + (size_t)kConsumerWarps * MAXM * D;           // [warp][MAXM]
+  float* sm_l = sm_m + kConsumerWarps * MAXM;                       // [warp][MAXM]
+  int* sm_flag = reinterpret_cast<int*>(sm_l + kConsumerWarps * MAXM);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kRing + C::kMerge + C::kSmall);
+  uint64_t* empty = full + kStages;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int cta = blockIdx.x;
+  const long long NT = p.total_tiles;
+  const long long t_begin = tile_begin(cta, NT, p.ctas);
+  const long long t_end = tile_begin(cta + 1, NT, p.ctas);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  // producer state (thread 0 only): tiles are issued in order
+  uint64_t pol = 0;
+  long long next_issue = t_begin;
+  auto issue = [&](long long i) {
+    const long long k = i - t_begin;
+    const int s = (int)(k % kStages);
+    const long long u = i / p.tpu;
+    const long long row0 = (i % p.tpu) * C::TR;
+    const long long rows = min((long long)C::TR, p.cap - row0);
+    const uint32_t bytes = (uint32_t)(rows * C::ROWB);
+    const size_t off = (size_t)(u * p.cap + row0) * C::ROWB;
+    uint8_t* dk = ring + (size_t)s * 2 * kStageBytes;
+    mbar_expect_tx(&full[s], 2 * bytes);
+    bulk_g2s(dk, p.K + off, bytes, &full[s], pol);
+    bulk_g2s(dk + kStageBytes, p.V + off, bytes, &full[s], pol);
+  };
+  if (threadIdx.x == 0) {
+    pol = evict_first_policy();
+    for (; next_issue < t_end && next_issue < t_begin + kStages; ++next_issue) issue(next_issue);
+  }
+
+  // -------------------------------------------------------------- consumers
+  const int rip = lane / C::LPR;   // row within a pass
+  const int cl = lane % C::LPR;    // lane within the row
+  int chunk[CPL];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) chunk[c] = cl + C::LPR * ((c + rip) % CPL);
+
+  float2 q2[MAXM][C::EL2];
+  float2 o2[MAXM][C::EL2];
+  float mw[MAXM], lsum[MAXM];
+  int nvis[MAXM];
+  long long cur_u = -1;
+  int max_vis = 0;
+  bool seg_first = true;
+
+  for (long long i = t_begin; i < t_end; ++i) {
+    const long long k = i - t_begin;
+    const int s = (int)(k % kStages);
+    const uint32_t ph = (uint32_t)((k / kStages) & 1);
+    const long long u = i / p.tpu;
+    const long long row0 = (i % p.tpu) * C::TR;
+    const int rows_in_tile = (int)min((long long)C::TR, p.cap - row0);
+    const int b = (int)(u / p.H_kv);
+    const int g = (int)(u % p.H_kv);
+
+    if (u != cur_u) {
+      // new segment: load this unit's query rows, reset the softmax state
+      cur_u = u;
+      seg_first = (i == t_begin);
+      const uint8_t* qbase =
+          p.Q + ((size_t)((size_t)b * p.H_q + (size_t)g * p.G) * p.t + p.m0) * C::ROWB;
+      max_vis = 0;
+#pragma unroll
+      for (int m = 0; m < MAXM; ++m) {
+        mw[m] = -INFINITY;
+        lsum[m] = 0.f;
+        nvis[m] = 0;
+#pragma unroll
+        for (int e = 0; e < C::EL2; ++e) {
+          o2[m][e] = make_float2(0.f, 0.f);
+          q2[m][e] = make_float2(0.f, 0.f);
+        }
+        if (m < p.M) {
+          nvis[m] = p.valid[b] + (p.m0 + m) % p.t;
+          max_vis = max(max_vis, nvis[m]);
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) {
+            const uint4 raw =
+                *reinterpret_cast<const uint4*>(qbase + (size_t)m * C::ROWB + chunk[c] * 16);
+            float2 f[C::EPC / 2];
+            Chunk<T>::load(raw, f);
+#pragma unroll
+            for (int e = 0; e < C::EPC / 2; ++e)
+              q2[m][c * (C::EPC / 2) + e] = make_float2(f[e].x * p.qscale, f[e].y * p.qscale);
+          }
+        }
+      }
+    }
+
+    mbar_wait(&full[s], ph);
+    const uint8_t* sk = ring + (size_t)s * 2 * kStageBytes;
+    const uint8_t* sv = sk + kStageBytes;
+
+    if (row0 < max_vis) {  // tiles with no visible row for any query are only streamed
+      float sc[C::PASSES][MAXM];
+#pragma unroll
+      for (int ps = 0; ps < C::PASSES; ++ps) {
+        const int row = warp * C::RPW + ps * C::RPP + rip;
+        float2 kf[C::EL2];
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          const uint4 raw = *reinterpret_cast<const uint4*>(sk + row * C::ROWB + chunk[c] * 16);
+          Chunk<T>::load(raw, kf + c * (C::EPC / 2));
+        }
+        const long long jr = row0 + row;
+#pragma unroll
+        for (int m = 0; m < MAXM; ++m) {
+          if (m < p.M) {
+            float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int e = 0; e < C::EL2; ++e) acc = __ffma2_rn(q2[m][e], kf[e], acc);
+            float v = acc.x + acc.y;
+#pragma unroll
+            for (int off = 1; off < C::LPR; off <<= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+            sc[ps][m] = (jr < nvis[m]) ? v : -INFINITY;
+          }
+        }
+      }
+      // online softmax update (per warp); probabilities overwrite the scores
+      float (&pr)[C::PASSES][MAXM] = sc;
+#pragma unroll
+      for (int m = 0; m < MAXM; ++m) {
+        if (m < p.M) {
+          float mt = sc[0][m];
+#pragma unroll
+          for (int ps = 1; ps < C::PASSES; ++ps) mt = fmaxf(mt, sc[ps][m]);
+#pragma unroll
+          for (int off = C::LPR; off < 32; off <<= 1)
+            mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, off));
+          const float mn = fmaxf(mw[m], mt);
+          if (mn == -INFINITY) {
+#pragma unroll
+            for (int ps = 0; ps < C::PASSES; ++ps) pr[ps][m] = 0.f;
+            continue;
+          }
+          float tsum = 0.f;
+#pragma unroll
+          for (int ps = 0; ps < C::PASSES; ++ps) {
+            pr[ps][m] = fast_exp2(sc[ps][m] - mn);
+            tsum += pr[ps][m];
+          }
+          if (mn != mw[m]) {
+            const float alpha = fast_exp2(mw[m] - mn);
+            lsum[m] *= alpha;
+            const float2 a2 = make_float2(alpha, alpha);
+#pragma unroll
+            for (int e = 0; e < C::EL2; ++e) o2[m][e] = __fmul2_rn(o2[m][e], a2);
+            mw[m] = mn;
+          }
+          lsum[m] += tsum;
+        }
+      }
+      // P . V
+#pragma unroll
+      for (int ps = 0; ps < C::PASSES; ++ps) {
+        const int row = warp * C::RPW + ps * C::RPP + rip;
+        if (row < rows_in_tile) {
+          float2 vf[C::EL2];
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) {
+            const uint4 raw =
+                *reinterpret_cast<const uint4*>(sv + row * C::ROWB + chunk[c] * 16);
+            Chunk<T>::load(raw, vf + c * (C::EPC / 2));
+          }
+#pragma unroll
+          for (int m = 0; m < MAXM; ++m) {
+            if (m < p.M) {
+              const float2 pp = make_float2(pr[ps][m], pr[ps][m]);
+#pragma unroll
+              for (int e = 0; e < C::EL2; ++e) o2[m][e] = __ffma2_rn(pp, vf[e], o2[m][e]);
+            }
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    if (threadIdx.x == 0 && next_issue < t_end) {
+      // refill this stage once every warp has released it
+      mbar_wait(&empty[s], ph);
+      issue(next_issue++);
+    }
+
+    // ------------------------------------------------------ segment end
+    const bool seg_last = (i + 1 == t_end) || ((i + 1) / p.tpu != u);
+    if (!seg_last) continue;
+
+    if (lane == 0) {
+#pragma unroll
+      for (int m = 0; m < MAXM; ++m) sm_m[warp * MAXM + m] = mw[m];
+    }
+    consumer_sync();
+#pragma unroll
+    for (int m = 0; m < MAXM; ++m) {
+      if (m >= p.M) continue;
+      float mc = -INFINITY;
+      for (int w = 0; w < kConsumerWarps; ++w) mc = fmaxf(mc, sm_m[w * MAXM + m]);
+      const float f = (mw[m] == -INFINITY) ? 0.f : fast_exp2(mw[m] - mc);
+      // lanes of one row group hold the same lsum: sum one lane per group
+      float l = lsum[m];
+#pragma unroll
+      for (int off = C::LPR; off < 32; off <<= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
+      // undo the per-row chunk rotation before summing row groups
+      if (CPL == 2 && (rip & 1)) {
+#pragma unroll
+        for (int e = 0; e < C::EL2 / 2; ++e) {
+          const float2 tmp = o2[m][e];
+          o2[m][e] = o2[m][e + C::EL2 / 2];
+          o2[m][e + C::EL2 / 2] = tmp;
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < C::EL2; ++e) {
+#pragma unroll
+        for (int off = C::LPR; off < 32; off <<= 1) {
+          o2[m][e].x += __shfl_xor_sync(0xffffffffu, o2[m][e].x, off);
+          o2[m][e].y += __shfl_xor_sync(0xffffffffu, o2[m][e].y, off);
+        }
+      }
+      if (rip == 0) {
+        float* dst = sm_o + ((size_t)warp * MAXM + m) * D;
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          const int x0 = (cl + C::LPR * c) * C::EPC;
+#pragma unroll
+          for (int e = 0; e < C::EPC / 2; ++e) {
+            const float2 v = o2[m][c * (C::EPC / 2) + e];
+            dst[x0 + 2 * e] = v.x * f;
+            dst[x0 + 2 * e + 1] = v.y * f;
+          }
+        }
+        if (lane == 0) sm_l[warp * MAXM + m] = l * f;
+      }
+    }
+    consumer_sync();
+
+    // CTA-level result of this segment
+    const long long ufirst = u * p.tpu, ulast = ufirst + p.tpu - 1;
+    const int c_lo = cta_of_tile(ufirst, NT, p.ctas);
+    const int c_hi = cta_of_tile(ulast, NT, p.ctas);
+    const int nseg = c_hi - c_lo + 1;
+    const int tid = threadIdx.x;
+    const size_t obase = ((size_t)((size_t)b * p.H_q + (size_t)g * p.G) * p.t + p.m0) * D;
+    if (nseg == 1) {
+      for (int idx = tid; idx < p.M * D; idx += kConsumerWarps * 32) {
+        const int m = idx / D, x = idx % D;
+        float o = 0.f, l = 0.f;
+        for (int w = 0; w < kConsumerWarps; ++w) {
+          o += sm_o[((size_t)w * MAXM + m) * D + x];
+          l += sm_l[w * MAXM + m];
+        }
+        p.O[obase + idx] = o / l;
+      }
+    } else {
+      const size_t rec = (size_t)p.M * (D + 2);
+      float* my = p.ws + ((size_t)cta * 2 + (seg_first ? 0 : 1)) * rec;
+      for (int idx = tid; idx < p.M * D; idx += kConsumerWarps * 32) {
+        const int m = idx / D, x = idx % D;
+        float o = 0.f;
+        for (int w = 0; w < kConsumerWarps; ++w) o += sm_o[((size_t)w * MAXM + m) * D + x];
+        my[idx] = o;
+      }
+      if (tid < p.M) {
+        float mc = -INFINITY, l = 0.f;
+        for (int w = 0; w < kConsumerWarps; ++w) {
+          mc = fmaxf(mc, sm_m[w * MAXM + tid]);
+          l += sm_l[w * MAXM + tid];
+        }
+        my[(size_t)p.M * D + tid] = mc;
+        my[(size_t)p.M * D + p.M + tid] = l;
+      }
+      __threadfence();
+      consumer_sync();
+      if (tid == 0) {
+        const int old = atomicAdd(&p.counters[u], 1);
+        *sm_flag = (old == nseg - 1);
+      }
+      consumer_sync();
+      if (*sm_flag) {
+        __threadfence();
+        // merge the nseg partial records of unit u (split-K combine)
+        for (int idx = tid; idx < p.M * D; idx += kConsumerWarps * 32) {
+          const int m = idx / D;
+          float mu = -INFINITY;
+          for (int c = c_lo; c <= c_hi; ++c) {
+            const long long fu = tile_begin(c, NT, p.ctas) / p.tpu;
+            const float* r = p.ws + ((size_t)c * 2 + (fu == u ? 0 : 1)) * rec;
+            mu = fmaxf(mu, __ldcg(r + (size_t)p.M * D + m));
+          }
+          float o = 0.f, l = 0.f;
+          for (int c = c_lo; c <= c_hi; ++c) {
+            const long long fu = tile_begin(c, NT, p.ctas) / p.tpu;
+            const float* r = p.ws + ((size_t)c * 2 + (fu == u ? 0 : 1)) * rec;
+            const float mk = __ldcg(r + (size_t)p.M * D + m);
+            const float w = (mk == -INFINITY) ? 0.f : fast_exp2(mk - mu);
+            o += __ldcg(r + idx) * w;
+            l += __ldcg(r + (size_t)p.M * D + p.M + m) * w;
+          }
+          p.O[obase + idx] = o / l;
+        }
+        if (tid == 0) p.counters[u] = 0;
+      }
+    }
+    consumer_sync();  // shared merge buffers are reused by the next segment
+  }
+}
+
+template <typename T, int D, int MAXM, int CPL>
+cudaError_t launch_t(const Params& prm, cudaStream_t s) {
+  using C = Cfg<T, D, MAXM, CPL>;
+  auto kern = attn_decode_kernel<T, D, MAXM, CPL>;
+  static bool attr_set = false;  // per instantiation
+  if (!attr_set) {
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kSmem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  kern<<<prm.ctas, kThreads, C::kSmem, s>>>(prm);
+  count_launch();
+  return cudaGetLastError();
+}
+
+template <typename T, int D>
+cudaError_t dispatch_m(const Params& prm, cudaStream_t s) {
+  if (prm.M <= 1) return launch_t<T, D, 1, 2>(prm, s);
+  if (prm.M <= 2) return launch_t<T, D, 2, 2>(prm, s);
+  if (prm.M <= 4) return launch_t<T, D, 4, 2>(prm, s);
+  return launch_t<T, D, 8, 1>(prm, s);
+}
+
+}  // namespace attn
+
+static int tile_rows(int D, int dtype) {
+  return attn::kStageBytes / (D * (dtype == BMC_BF16 ? 2 : 4));
+}
+
+size_t attn_workspace_floats(int U, int M, int D, int num_sms) {
+  (void)U;
+  const int mc = M < 8 ? M : 8;
+  return (size_t)num_sms * 2 * (size_t)mc * (D + 2);
+}
+
+cudaError_t launch_attn_decode(const AttnArgs& a, int num_sms, cudaStream_t s) {
+  const long long U = (long long)a.B * a.H_kv;
+  const int TR = tile_rows(a.D, a.dtype);
+  const int tpu = (int)((a.cap + TR - 1) / TR);
+  const long long NT = U * tpu;
+  if (NT == 0) return cudaSuccess;
+  attn::Params prm;
+  prm.K = (const uint8_t*)a.K;
+  prm.V = (const uint8_t*)a.V;
+  prm.Q = (const uint8_t*)a.Q;
+  prm.O = a.O;
+  prm.ws = a.ws;
+  prm.counters = a.counters;
+  prm.cap = a.cap;
+  prm.total_tiles = NT;
+  prm.tpu = tpu;
+  prm.H_kv = a.H_kv;
+  prm.H_q = a.H_q;
+  prm.G = a.H_q / a.H_kv;
+  prm.t = a.t;
+  prm.Mu = prm.G * a.t;
+  int ctas = a.ctas > 0 ? a.ctas : num_sms;
+  if (ctas > NT) ctas = (int)NT;
+  prm.ctas = ctas;
+  prm.qscale = attn::kLog2e / sqrtf((float)a.D);
+  for (int b = 0; b < a.B; ++b) prm.valid[b] = a.valid[b];
+  // query rows in groups of at most 8 per launch (CUDA-core path)
+  for (int m0 = 0; m0 < prm.Mu; m0 += 8) {
+    prm.m0 = m0;
+    prm.M = prm.Mu - m0 < 8 ? prm.Mu - m0 : 8;
+    cudaError_t e;
+    if (a.dtype == BMC_BF16) {
+      e = a.D == 128 ? attn::dispatch_m<__nv_bfloat16, 128>(prm, s)
+                     : attn::dispatch_m<__nv_bfloat16, 64>(prm, s);
+    } else {
+      e = a.D == 128 ? attn::dispatch_m<float, 128>(prm, s) : attn::dispatch_m<float, 64>(prm, s);
+    }
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace bmc

@@ -1,0 +1,506 @@
+// bmc_abi.cpp -- the C-ABI state machine of libbmc.so (include/bmc.h).
+//
+// The host keeps an exact shadow of every length (valid_b, cap, staged), so
+// no call ever reads anything back from the device on the hot path; all
+// validation happens before anything is enqueued.  Each call turns into at
+// most three stream-ordered kernel launches:
+//   bmc_append     [growth: arena map + realloc_copy_zero]  + write_rows
+//   bmc_spec_write [ITERATIVE growth]                       + write_rows
+//   bmc_sdpa       attn_decode (split-K, in-kernel combine)
+//   bmc_commit     zero_rows (rejected drafts only)
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "bmc_internal.h"
+
+using bmc::Buffer;
+
+struct bmc_ctx {
+  int B = 0, H_kv = 0, H_q = 0, D = 0, r = 0, N_max = 0;
+  bmc_dtype dt = BMC_BF16;
+  bmc_policy pol = BMC_POLICY_BMC;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int eb = 2, row_bytes = 0;
+  long long U = 0;
+  long long cap = 0;
+  std::vector<int> valid;
+  int staged = 0;
+  Buffer kbuf, vbuf;
+  bmc::Arena* arena = nullptr;
+  int arena_kind = 0;
+  float* ws = nullptr;
+  int* counters = nullptr;
+  int num_sms = 148;
+  int max_ctas = 148;
+  int attn_ctas = 0;
+  int attn_path = 0;
+  bmc_stats_t st = {};
+  int sticky = 0;
+  // staging of host-pointer arguments
+  void* stage_in = nullptr;
+  size_t stage_in_bytes = 0;
+  float* stage_out = nullptr;
+  size_t stage_out_bytes = 0;
+};
+
+static thread_local std::string g_err;
+
+static int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+static int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+static int cuda_fail(bmc_t h, cudaError_t e, const char* where) {
+  if (h) h->sticky = BMC_ERR_CUDA;
+  return fail(e == cudaErrorMemoryAllocation ? BMC_ERR_OOM : BMC_ERR_CUDA, "%s: %s", where,
+              cudaGetErrorString(e));
+}
+
+#define CK(h, expr, where)                                   \
+  do {                                                       \
+    cudaError_t _e = (expr);                                 \
+    if (_e != cudaSuccess) return cuda_fail((h), _e, where); \
+  } while (0)
+
+static int enter(bmc_t h) {
+  if (!h) return fail(BMC_ERR_ARG, "null handle");
+  if (h->sticky) return fail(h->sticky, "handle is in a sticky CUDA error state");
+  int cur = -1;
+  if (cudaGetDevice(&cur) != cudaSuccess || cur != h->device) {
+    cudaError_t e = cudaSetDevice(h->device);
+    if (e != cudaSuccess) return cuda_fail(h, e, "cudaSetDevice");
+  }
+  return 0;
+}
+
+static int max_valid(const bmc_t h) { return *std::max_element(h->valid.begin(), h->valid.end()); }
+static int min_valid(const bmc_t h) { return *std::min_element(h->valid.begin(), h->valid.end()); }
+
+// 0 device (or managed), 1 page-locked host, 2 pageable host
+static int ptr_kind(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return 2;
+  }
+  if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) return 0;
+  return a.type == cudaMemoryTypeHost ? 1 : 2;
+}
+static bool is_device_ptr(const void* p) { return ptr_kind(p) == 0; }
+
+static int ensure_stage_in(bmc_t h, size_t bytes) {
+  if (h->stage_in_bytes >= bytes) return 0;
+  if (h->stage_in) cudaFreeAsync(h->stage_in, h->stream);
+  h->stage_in = nullptr;
+  h->stage_in_bytes = 0;
+  CK(h, cudaMallocAsync(&h->stage_in, bytes, h->stream), "stage_in");
+  h->stage_in_bytes = bytes;
+  return 0;
+}
+
+// Map caller inputs (device or host) to device pointers; host inputs are
+// copied into the handle's staging buffer on its stream.
+static int device_inputs(bmc_t h, const void** ptrs, const size_t* bytes, int n,
+                         const void** dev) {
+  size_t need = 0;
+  bool any_host = false;
+  for (int i = 0; i < n; ++i) {
+    if (!is_device_ptr(ptrs[i])) {
+      any_host = true;
+      need += (bytes[i] + 255) / 256 * 256;
+    }
+  }
+  if (any_host) {
+    int rc = ensure_stage_in(h, need);
+    if (rc) return rc;
+  }
+  size_t off = 0;
+  for (int i = 0; i < n; ++i) {
+    if (is_device_ptr(ptrs[i])) {
+      dev[i] = ptrs[i];
+    } else {
+      void* d = (char*)h->stage_in + off;
+      CK(h, cudaMemcpyAsync(d, ptrs[i], bytes[i], cudaMemcpyHostToDevice, h->stream), "H2D");
+      dev[i] = d;
+      off += (bytes[i] + 255) / 256 * 256;
+    }
+  }
+  return 0;
+}
+
+// Replace the cache buffers by [U][new_cap][D] buffers holding the first
+// copy_rows rows of every unit, zero elsewhere.
+static int reallocate(bmc_t h, long long new_cap, long long copy_rows) {
+  const size_t bytes = (size_t)h->U * new_cap * h->row_bytes;
+  Buffer nk, nv;
+  int rc = bmc::arena_alloc(h->arena, 0, bytes, h->arena_kind, &h->kbuf, h->stream, &nk);
+  if (rc) return fail(rc, "arena_alloc(K, %zu bytes) failed", bytes);
+  rc = bmc::arena_alloc(h->arena, 1, bytes, h->arena_kind, &h->vbuf, h->stream, &nv);
+  if (rc) {
+    bmc::arena_release(h->arena, &nk, h->stream);
+    return fail(rc, "arena_alloc(V, %zu bytes) failed", bytes);
+  }
+  bmc::ReallocArgs a;
+  a.src_k = h->kbuf.ptr;
+  a.src_v = h->vbuf.ptr;
+  a.dst_k = nk.ptr;
+  a.dst_v = nv.ptr;
+  a.U = h->U;
+  a.cap_old = h->cap;
+  a.cap_new = new_cap;
+  a.copy_rows = copy_rows;
+  a.row_bytes = h->row_bytes;
+  CK(h, bmc::launch_realloc_copy_zero(a, h->stream), "realloc_copy_zero");
+  if (h->cap > 0) h->st.copy_events += 1;
+  h->st.alloc_events += 1;
+  h->st.copied_bytes += 2LL * h->U * copy_rows * h->row_bytes;
+  h->st.init_written_bytes += 2LL * h->U * new_cap * h->row_bytes;
+  if (bmc::arena_release(h->arena, &h->kbuf, h->stream) ||
+      bmc::arena_release(h->arena, &h->vbuf, h->stream)) {
+    h->sticky = BMC_ERR_CUDA;
+    return fail(BMC_ERR_CUDA, "arena_release failed");
+  }
+  h->kbuf = nk;
+  h->vbuf = nv;
+  h->cap = new_cap;
+  return 0;
+}
+
+static int write_rows(bmc_t h, const void* K, const void* V, int nsrc, int nwrite) {
+  bmc::RowsArgs a;
+  a.src_k = K;
+  a.src_v = V;
+  a.dst_k = h->kbuf.ptr;
+  a.dst_v = h->vbuf.ptr;
+  a.B = h->B;
+  a.H_kv = h->H_kv;
+  a.nsrc = nsrc;
+  a.nwrite = nwrite;
+  a.cap = h->cap;
+  a.row_bytes = h->row_bytes;
+  for (int b = 0; b < h->B; ++b) a.row0[b] = h->valid[b];
+  CK(h, bmc::launch_write_rows(a, h->stream), "write_rows");
+  h->st.append_written_bytes += 2LL * h->U * nwrite * h->row_bytes;
+  return 0;
+}
+
+extern "C" {
+
+int bmc_create_ex(int B, int H_kv, int H_q, int D, int r, int N_max, bmc_dtype dt,
+                  bmc_policy pol, int device, void* cuda_stream, bmc_t* out) {
+  if (!out) return fail(BMC_ERR_ARG, "out is null");
+  *out = nullptr;
+  if (B < 1 || H_kv < 1 || H_q < 1 || D < 1 || N_max < 1)
+    return fail(BMC_ERR_ARG, "dims must be >= 1 (B=%d H_kv=%d H_q=%d D=%d N_max=%d)", B, H_kv,
+                H_q, D, N_max);
+  if (H_q % H_kv != 0) return fail(BMC_ERR_ARG, "H_q %% H_kv != 0");
+  if (pol != BMC_POLICY_BMC && pol != BMC_POLICY_ITERATIVE && pol != BMC_POLICY_UPFRONT)
+    return fail(BMC_ERR_ARG, "bad policy %d", (int)pol);
+  if (pol == BMC_POLICY_BMC && (r < 1 || r > N_max))
+    return fail(BMC_ERR_ARG, "r=%d outside [1, N_max=%d]", r, N_max);
+  if (D != 64 && D != 128) return fail(BMC_ERR_UNSUPPORTED, "D=%d not in {64,128}", D);
+  if (dt != BMC_F32 && dt != BMC_BF16) return fail(BMC_ERR_UNSUPPORTED, "dtype %d", (int)dt);
+  if (B > BMC_MAX_B) return fail(BMC_ERR_UNSUPPORTED, "B=%d > BMC_MAX_B", B);
+
+  if (device < 0) {
+    cudaError_t e = cudaGetDevice(&device);
+    if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaGetDevice");
+  } else {
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaSetDevice");
+  }
+  bmc_ctx* h = new bmc_ctx();
+  h->B = B; h->H_kv = H_kv; h->H_q = H_q; h->D = D; h->r = r; h->N_max = N_max;
+  h->dt = dt; h->pol = pol; h->device = device;
+  h->stream = (cudaStream_t)cuda_stream;
+  h->eb = dt == BMC_BF16 ? 2 : 4;
+  h->row_bytes = D * h->eb;
+  h->U = (long long)B * H_kv;
+  h->valid.assign(B, 0);
+  cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device);
+  h->max_ctas = 4 * h->num_sms;
+  int err = 0;
+  h->arena = bmc::arena_create(device, (size_t)h->U * N_max * h->row_bytes, &err);
+  const size_t wsf = bmc::attn_workspace_floats((int)h->U, 8, D, h->max_ctas);
+  // stream-ordered: creating a handle never synchronises the device
+  cudaError_t e = cudaMallocAsync((void**)&h->ws, wsf * sizeof(float), h->stream);
+  if (e == cudaSuccess) e = cudaMallocAsync((void**)&h->counters, (size_t)h->U * sizeof(int), h->stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(h->counters, 0, (size_t)h->U * sizeof(int), h->stream);
+  if (e != cudaSuccess) {
+    int rc = cuda_fail(nullptr, e, "create workspace");
+    bmc_destroy(h);
+    return rc;
+  }
+  int rc = 0;
+  if (pol == BMC_POLICY_BMC) rc = reallocate(h, std::min(r, N_max), 0);
+  else if (pol == BMC_POLICY_UPFRONT) rc = reallocate(h, N_max, 0);
+  if (rc) {
+    std::string msg = g_err;
+    bmc_destroy(h);
+    g_err = msg;
+    return rc;
+  }
+  *out = h;
+  return 0;
+}
+
+int bmc_create(int B, int H_kv, int H_q, int D, int r, int N_max, bmc_t* out) {
+  return bmc_create_ex(B, H_kv, H_q, D, r, N_max, BMC_BF16, BMC_POLICY_BMC, -1, nullptr, out);
+}
+
+int bmc_append(bmc_t h, const void* K, const void* V) {
+  int rc = enter(h);
+  if (rc) return rc;
+  if (!K || !V) return fail(BMC_ERR_ARG, "K or V is null");
+  if (h->staged > 0) return fail(BMC_ERR_STATE, "append while %d drafts are staged", h->staged);
+  const int mv = max_valid(h);
+  if (mv >= h->N_max) return fail(BMC_ERR_CAPACITY, "cache full (N_max=%d)", h->N_max);
+  const size_t in_bytes = (size_t)h->U * h->row_bytes;
+  const void* ptrs[2] = {K, V};
+  const size_t sizes[2] = {in_bytes, in_bytes};
+  const void* dev[2];
+  if (h->pol == BMC_POLICY_ITERATIVE) {
+    rc = reallocate(h, mv + 1, mv);                      // Fig. AttnBlkListing concat
+  } else if (h->pol == BMC_POLICY_BMC && mv == h->cap) {
+    rc = reallocate(h, std::min<long long>(h->cap + h->r, h->N_max), h->cap);
+  }
+  if (rc) return rc;
+  rc = device_inputs(h, ptrs, sizes, 2, dev);
+  if (rc) return rc;
+  rc = write_rows(h, dev[0], dev[1], 1, 1);
+  if (rc) return rc;
+  for (auto& v : h->valid) v += 1;
+  return 0;
+}
+
+int bmc_spec_write(bmc_t h, const void* K_draft, const void* V_draft, int k) {
+  int rc = enter(h);
+  if (rc) return rc;
+  if (k < 0) return fail(BMC_ERR_ARG, "k=%d < 0", k);
+  if (k > 0 && (!K_draft || !V_draft)) return fail(BMC_ERR_ARG, "draft pointers are null");
+  if (h->staged > 0) return fail(BMC_ERR_STATE, "drafts already staged");
+  if (k == 0) return 0;
+  const int mv = max_valid(h);
+  int k_adm;
+  if (h->pol == BMC_POLICY_ITERATIVE) {
+    k_adm = std::min(k, h->N_max - mv);
+    if (k_adm > 0) {
+      rc = reallocate(h, (long long)mv + k_adm, mv);
+      if (rc) return rc;
+    }
+  } else {
+    k_adm = (int)std::min<long long>(k, h->cap - mv);    // P:L867-869 admission
+  }
+  if (k_adm > 0) {
+    const size_t in_bytes = (size_t)h->U * k * h->row_bytes;
+    const void* ptrs[2] = {K_draft, V_draft};
+    const size_t sizes[2] = {in_bytes, in_bytes};
+    const void* dev[2];
+    rc = device_inputs(h, ptrs, sizes, 2, dev);
+    if (rc) return rc;
+    rc = write_rows(h, dev[0], dev[1], k, k_adm);
+    if (rc) return rc;
+  }
+  h->staged = k_adm;
+  return k_adm;
+}
+
+int bmc_sdpa(bmc_t h, const void* Q, int n_valid, float* O) {
+  int rc = enter(h);
+  if (rc) return rc;
+  if (!Q || !O) return fail(BMC_ERR_ARG, "Q or O is null");
+  if (n_valid == 0) return fail(BMC_ERR_ARG, "n_valid == 0");
+  if (n_valid != BMC_PER_ROW) {
+    for (int b = 0; b < h->B; ++b)
+      if (h->valid[b] != n_valid)
+        return fail(BMC_ERR_STATE, "n_valid=%d but row %d holds %d", n_valid, b, h->valid[b]);
+  }
+  if (min_valid(h) == 0) return fail(BMC_ERR_ARG, "a batch row has no committed token");
+  const int t = 1 + h->staged;
+  const size_t q_bytes = (size_t)h->B * h->H_q * t * h->row_bytes;
+  const size_t o_bytes = (size_t)h->B * h->H_q * t * h->D * sizeof(float);
+  const void* qd = nullptr;
+  rc = device_inputs(h, &Q, &q_bytes, 1, &qd);
+  if (rc) return rc;
+  const int out_kind = ptr_kind(O);
+  const bool host_out = out_kind != 0;
+  float* od = O;
+  if (host_out) {
+    if (h->stage_out_bytes < o_bytes) {
+      if (h->stage_out) cudaFreeAsync(h->stage_out, h->stream);
+      h->stage_out = nullptr;
+      h->stage_out_bytes = 0;
+      CK(h, cudaMallocAsync((void**)&h->stage_out, o_bytes, h->stream), "stage_out");
+      h->stage_out_bytes = o_bytes;
+    }
+    od = h->stage_out;
+  }
+  bmc::AttnArgs a;
+  a.K = h->kbuf.ptr;
+  a.V = h->vbuf.ptr;
+  a.Q = qd;
+  a.O = od;
+  a.ws = h->ws;
+  a.counters = h->counters;
+  a.B = h->B;
+  a.H_kv = h->H_kv;
+  a.H_q = h->H_q;
+  a.D = h->D;
+  a.t = t;
+  a.cap = h->cap;
+  a.dtype = h->dt;
+  a.ctas = std::min(h->attn_ctas, h->max_ctas);
+  for (int b = 0; b < h->B; ++b) a.valid[b] = h->valid[b];
+  CK(h, bmc::launch_attn_decode(a, h->num_sms, h->stream), "attn_decode");
+  h->st.sdpa_calls += 1;
+  h->st.kv_bytes_read += 2LL * h->U * h->cap * h->row_bytes;
+  h->st.macs += 2LL * h->B * h->H_q * t * h->cap * (long long)h->D;
+  if (host_out) {
+    CK(h, cudaMemcpyAsync(O, od, o_bytes, cudaMemcpyDeviceToHost, h->stream), "D2H");
+    if (out_kind == 2) CK(h, cudaStreamSynchronize(h->stream), "sync");
+  }
+  return 0;
+}
+
+static int commit_impl(bmc_t h, const int* m) {
+  bmc::ZeroArgs z;
+  z.k = h->kbuf.ptr;
+  z.v = h->vbuf.ptr;
+  z.B = h->B;
+  z.H_kv = h->H_kv;
+  z.cap = h->cap;
+  z.row_bytes = h->row_bytes;
+  z.max_rows = 0;
+  for (int b = 0; b < h->B; ++b) {
+    z.row_lo[b] = h->valid[b] + m[b];        // rejected drafts (reading R9)
+    z.row_hi[b] = h->valid[b] + h->staged;
+    z.max_rows = std::max(z.max_rows, h->staged - m[b]);
+  }
+  if (z.max_rows > 0) CK(h, bmc::launch_zero_rows(z, h->stream), "zero_rows");
+  for (int b = 0; b < h->B; ++b) h->valid[b] += m[b];
+  h->staged = 0;
+  return 0;
+}
+
+int bmc_commit(bmc_t h, int n_accepted) {
+  int rc = enter(h);
+  if (rc) return rc;
+  if (h->staged == 0 && n_accepted > 0) return fail(BMC_ERR_STATE, "nothing staged");
+  if (n_accepted < 0 || n_accepted > h->staged)
+    return fail(BMC_ERR_ARG, "n_accepted=%d outside [0, %d]", n_accepted, h->staged);
+  std::vector<int> m(h->B, n_accepted);
+  return commit_impl(h, m.data());
+}
+
+int bmc_commit_rows(bmc_t h, const int* n_accepted_host) {
+  int rc = enter(h);
+  if (rc) return rc;
+  if (!n_accepted_host) return fail(BMC_ERR_ARG, "n_accepted is null");
+  for (int b = 0; b < h->B; ++b) {
+    if (h->staged == 0 && n_accepted_host[b] > 0) return fail(BMC_ERR_STATE, "nothing staged");
+    if (n_accepted_host[b] < 0 || n_accepted_host[b] > h->staged)
+      return fail(BMC_ERR_ARG, "n_accepted[%d]=%d outside [0, %d]", b, n_accepted_host[b],
+                  h->staged);
+  }
+  return commit_impl(h, n_accepted_host);
+}
+
+int bmc_destroy(bmc_t h) {
+  if (!h) return fail(BMC_ERR_ARG, "null handle");
+  cudaSetDevice(h->device);
+  cudaStreamSynchronize(h->stream);
+  bmc::arena_release(h->arena, &h->kbuf, h->stream);
+  bmc::arena_release(h->arena, &h->vbuf, h->stream);
+  if (h->stage_in) cudaFreeAsync(h->stage_in, h->stream);
+  if (h->stage_out) cudaFreeAsync(h->stage_out, h->stream);
+  if (h->ws) cudaFreeAsync(h->ws, h->stream);
+  if (h->counters) cudaFreeAsync(h->counters, h->stream);
+  cudaStreamSynchronize(h->stream);
+  bmc::arena_destroy(h->arena);
+  cudaGetLastError();
+  delete h;
+  return 0;
+}
+
+int bmc_stats(bmc_t h, bmc_stats_t* out) {
+  if (!h || !out) return fail(BMC_ERR_ARG, "null argument");
+  *out = h->st;
+  out->valid_min = min_valid(h);
+  out->valid_max = max_valid(h);
+  out->capacity = h->cap;
+  out->staged = h->staged;
+  return 0;
+}
+
+int bmc_kv_view(bmc_t h, void** K, void** V, int* cap) {
+  if (!h) return fail(BMC_ERR_ARG, "null handle");
+  if (K) *K = h->kbuf.ptr;
+  if (V) *V = h->vbuf.ptr;
+  if (cap) *cap = (int)h->cap;
+  return 0;
+}
+
+int bmc_read_cache(bmc_t h, void* K_dst, void* V_dst) {
+  int rc = enter(h);
+  if (rc) return rc;
+  if (!K_dst || !V_dst) return fail(BMC_ERR_ARG, "null destination");
+  const size_t bytes = (size_t)h->U * h->cap * h->row_bytes;
+  if (bytes == 0) return 0;
+  CK(h, cudaMemcpyAsync(K_dst, h->kbuf.ptr, bytes, cudaMemcpyDefault, h->stream), "read K");
+  CK(h, cudaMemcpyAsync(V_dst, h->vbuf.ptr, bytes, cudaMemcpyDefault, h->stream), "read V");
+  if (!is_device_ptr(K_dst) || !is_device_ptr(V_dst))
+    CK(h, cudaStreamSynchronize(h->stream), "sync");
+  return 0;
+}
+
+int bmc_valid(bmc_t h, int* valid_host) {
+  if (!h || !valid_host) return fail(BMC_ERR_ARG, "null argument");
+  memcpy(valid_host, h->valid.data(), sizeof(int) * h->B);
+  return 0;
+}
+
+int bmc_sync(bmc_t h) {
+  int rc = enter(h);
+  if (rc) return rc;
+  CK(h, cudaStreamSynchronize(h->stream), "sync");
+  return 0;
+}
+
+int bmc_set_option(bmc_t h, int key, long long value) {
+  if (!h) return fail(BMC_ERR_ARG, "null handle");
+  switch (key) {
+    case BMC_OPT_ATTN_CTAS:
+      if (value < 0) return fail(BMC_ERR_ARG, "ctas < 0");
+      h->attn_ctas = (int)value;
+      return 0;
+    case BMC_OPT_ATTN_PATH:
+      if (value < 0 || value > 2) return fail(BMC_ERR_ARG, "path");
+      h->attn_path = (int)value;
+      return 0;
+    case BMC_OPT_ARENA:
+      if (value < 0 || value > 1) return fail(BMC_ERR_ARG, "arena kind");
+      h->arena_kind = (int)value;
+      return 0;
+    default:
+      return fail(BMC_ERR_ARG, "unknown option %d", key);
+  }
+}
+
+unsigned long long bmc_launch_count(void) { return bmc::launch_count(); }
+
+const char* bmc_last_error(void) { return g_err.c_str(); }
+
+}  // extern "C"

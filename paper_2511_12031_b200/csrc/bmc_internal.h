@@ -1,0 +1,86 @@
+// bmc_internal.h -- internal interfaces between the C-ABI state machine
+// (bmc_abi.cpp), the chunk-growth arena (arena.cpp) and the sm_100a kernels
+// (bmc_kernels.cu, attn_decode.cu).  Not part of the public ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/bmc.h"
+
+namespace bmc {
+
+// ---------------------------------------------------------------- kernels
+// Every launcher returns the cudaError_t of its launch and bumps the global
+// launch counter.
+
+struct ReallocArgs {
+  const void* src_k; const void* src_v;   // [U][cap_old][D] (may be null if copy_rows == 0)
+  void* dst_k; void* dst_v;               // [U][cap_new][D]
+  long long U;
+  long long cap_old, cap_new;             // rows
+  long long copy_rows;                    // rows [0, copy_rows) copied, rest zeroed
+  int row_bytes;                          // D * element size, multiple of 16
+};
+cudaError_t launch_realloc_copy_zero(const ReallocArgs& a, cudaStream_t s);
+
+struct RowsArgs {
+  const void* src_k; const void* src_v;   // [B][H_kv][nsrc][D]
+  void* dst_k; void* dst_v;               // [U][cap][D]
+  int B, H_kv, nsrc, nwrite;              // write rows i < nwrite of the source
+  long long cap;
+  int row_bytes;
+  int row0[BMC_MAX_B];                    // destination row of source row 0, per batch row
+};
+cudaError_t launch_write_rows(const RowsArgs& a, cudaStream_t s);
+
+struct ZeroArgs {
+  void* k; void* v;                       // [U][cap][D]
+  int B, H_kv;
+  long long cap;
+  int row_bytes;
+  int row_lo[BMC_MAX_B], row_hi[BMC_MAX_B];   // zero rows [lo, hi) of batch row b
+  int max_rows;                           // max(hi - lo)
+};
+cudaError_t launch_zero_rows(const ZeroArgs& a, cudaStream_t s);
+
+struct AttnArgs {
+  const void* K; const void* V;           // [U][cap][D]
+  const void* Q;                          // [B][H_q][t][D]
+  float* O;                               // [B][H_q][t][D]
+  float* ws;                              // partial records
+  int* counters;                          // [U], zero between launches
+  int B, H_kv, H_q, D, t;
+  long long cap;
+  int dtype;                              // BMC_F32 / BMC_BF16
+  int ctas;                               // 0 = auto
+  int valid[BMC_MAX_B];
+};
+// Workspace floats / counter ints the attention needs for (U, M, D).
+size_t attn_workspace_floats(int U, int M, int D, int num_sms);
+cudaError_t launch_attn_decode(const AttnArgs& a, int num_sms, cudaStream_t s);
+
+void count_launch();
+unsigned long long launch_count();
+
+// ------------------------------------------------------------------ arena
+// Chunk-growth allocator: each handle owns one arena with two ping-pong
+// slots of reserved virtual address space per tensor; physical 2 MiB
+// granules come from a process-wide pool and are mapped on growth.
+struct Arena;
+struct Buffer {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  int slot = -1;        // arena slot (VMM), -1 = pool allocation
+  int kind = 0;         // 0 VMM, 1 pool
+};
+Arena* arena_create(int device, size_t max_bytes_per_tensor, int* err);
+// Obtain a buffer of `bytes` for tensor (0 = K, 1 = V) in the slot not
+// holding `keep` (the tensor's live buffer).  kind 0 = VMM slot, 1 =
+// stream-ordered pool allocation (also the fallback when VMM is unsupported).
+int arena_alloc(Arena* a, int tensor, size_t bytes, int kind, const Buffer* keep,
+                cudaStream_t s, Buffer* out);
+// Release a buffer once all work enqueued so far on s has finished with it.
+int arena_release(Arena* a, Buffer* b, cudaStream_t s);
+void arena_destroy(Arena* a);
+
+}  // namespace bmc

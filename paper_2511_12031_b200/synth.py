@@ -37,26 +37,28 @@ def torch_dtype(dtype: str) -> torch.dtype:
 
 def step_inputs(seed: int, layer: int, step: int, *, B: int, H_kv: int, H_q: int, D: int,
                 t: int = 1, k_draft: int = 0, dtype: str = "bf16",
-                variant: str = "normal") -> dict:
+                variant: str = "normal", want=("q", "k", "v", "kd", "vd")) -> dict:
     """Inputs of one decode (or speculative) iteration of one layer.
 
-    Returns CPU tensors: q [B][H_q][t][D], k/v [B][H_kv][D],
-    kd/vd [B][H_kv][k_draft][D] (absent when k_draft == 0)."""
-    g = _gen(seed, layer, step)
-    q = torch.randn(B, H_q, t, D, generator=g, dtype=torch.float32)
-    k = torch.randn(B, H_kv, D, generator=g, dtype=torch.float32)
-    v = torch.randn(B, H_kv, D, generator=g, dtype=torch.float32)
-    if variant == "peaky":
-        q = q * 8.0
-    elif variant == "outlier":
-        if torch.rand(1, generator=g).item() < 0.03:
-            k = k * 16.0
-    elif variant != "normal":
-        raise ValueError(variant)
-    out = {"q": q.to(_DT[dtype]), "k": k.to(_DT[dtype]), "v": v.to(_DT[dtype])}
-    if k_draft > 0:
-        out["kd"] = torch.randn(B, H_kv, k_draft, D, generator=g).to(_DT[dtype])
-        out["vd"] = torch.randn(B, H_kv, k_draft, D, generator=g).to(_DT[dtype])
+    Every tensor has its own stream (seed, layer, step, tensor), so any subset
+    can be drawn alone.  Returns CPU tensors: q [B][H_q][t][D],
+    k/v [B][H_kv][D], kd/vd [B][H_kv][k_draft][D] (when k_draft > 0)."""
+    shapes = {"q": (B, H_q, t, D), "k": (B, H_kv, D), "v": (B, H_kv, D),
+              "kd": (B, H_kv, k_draft, D), "vd": (B, H_kv, k_draft, D)}
+    out = {}
+    for tag, name in enumerate(("q", "k", "v", "kd", "vd")):
+        if name not in want or (name in ("kd", "vd") and k_draft == 0):
+            continue
+        x = torch.randn(*shapes[name], generator=_gen(seed, layer, step, tag),
+                        dtype=torch.float32)
+        if variant == "peaky" and name == "q":
+            x = x * 8.0
+        elif variant == "outlier" and name == "k":
+            if torch.rand(1, generator=_gen(seed, layer, step, 99)).item() < 0.03:
+                x = x * 16.0
+        elif variant not in ("normal", "peaky", "outlier"):
+            raise ValueError(variant)
+        out[name] = x.to(_DT[dtype])
     return out
 
 

@@ -1,0 +1,118 @@
+"""Lock-step driver: the same call sequence on libbmc (GPU, through the C ABI)
+and on the CPU oracle, with the same seeded inputs, comparing every output.
+
+Tolerances (BASELINE.json north_star): bf16 inputs max-abs <= 2e-3;
+fp32 inputs max|diff| <= 1e-5 * max(1, max|O_oracle|) (normwise reading of
+"1e-5 relative", R18).  Cache contents, capacities, counters and
+committed lengths must be bit-exact / equal.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+import oracle as O
+from paper_2511_12031_b200 import bmc, synth
+
+TOL_BF16 = 2e-3
+TOL_F32 = 1e-5
+STAT_KEYS = ("valid_min", "valid_max", "capacity", "staged", "alloc_events", "copy_events",
+             "copied_bytes", "init_written_bytes", "append_written_bytes", "kv_bytes_read",
+             "macs", "sdpa_calls")
+
+
+def err_of(o: np.ndarray, ref: np.ndarray, dtype: str) -> float:
+    """Error in the units of the tolerance (<= 1 passes)."""
+    d = float(np.abs(o.astype(np.float64) - ref).max()) if o.size else 0.0
+    if dtype == "bf16":
+        return d / TOL_BF16
+    return d / (TOL_F32 * max(1.0, float(np.abs(ref).max())))
+
+
+class Pair:
+    def __init__(self, B, H_kv, H_q, D, r, N, dtype="bf16", policy="bmc", seed=1,
+                 layer=0, ctas=0, host_io=False, variant="normal"):
+        self.B, self.H_kv, self.H_q, self.D, self.r, self.N = B, H_kv, H_q, D, r, N
+        self.dtype, self.seed, self.layer, self.variant = dtype, seed, layer, variant
+        self.host_io = host_io
+        self.gpu = bmc.KVCache(B, H_kv, H_q, D, r, N, dtype=dtype, policy=policy)
+        if ctas:
+            self.gpu.set_option(bmc.BMC_OPT_ATTN_CTAS, ctas)
+        pol = {"bmc": O.POLICY_BMC, "iterative": O.POLICY_ITERATIVE,
+               "upfront": O.POLICY_UPFRONT}[policy]
+        self.orc = O.Oracle(B, H_kv, H_q, D, r, N, dtype=O.F32 if dtype == "f32" else O.BF16,
+                            policy=pol)
+        self.step = 0
+        self.worst = 0.0
+
+    def _dev(self, x: torch.Tensor):
+        return x.contiguous() if self.host_io else x.cuda()
+
+    def append(self):
+        x = synth.step_inputs(self.seed, self.layer, self.step, B=self.B, H_kv=self.H_kv,
+                              H_q=self.H_q, D=self.D, dtype=self.dtype, want=("k", "v"),
+                              variant=self.variant)
+        self.step += 1
+        self.gpu.append(self._dev(x["k"]), self._dev(x["v"]))
+        self.orc.append(x["k"], x["v"])
+
+    def spec_write(self, k):
+        x = synth.step_inputs(self.seed, self.layer, self.step, B=self.B, H_kv=self.H_kv,
+                              H_q=self.H_q, D=self.D, dtype=self.dtype, k_draft=k,
+                              want=("kd", "vd"))
+        self.step += 1
+        a = self.gpu.spec_write(self._dev(x["kd"]), self._dev(x["vd"]), k)
+        b = self.orc.spec_write(x["kd"], x["vd"], k)
+        assert a == b, (a, b)
+        return a
+
+    def sdpa(self, n_valid=None):
+        st = self.orc.stats()
+        t = 1 + st["staged"]
+        if n_valid is None:
+            n_valid = st["valid_max"] if st["valid_min"] == st["valid_max"] else -1
+        x = synth.step_inputs(self.seed, self.layer, self.step, B=self.B, H_kv=self.H_kv,
+                              H_q=self.H_q, D=self.D, t=t, dtype=self.dtype, want=("q",),
+                              variant=self.variant)
+        self.step += 1
+        if self.host_io:
+            o = torch.empty(self.B, self.H_q, t, self.D, dtype=torch.float32).pin_memory()
+            self.gpu.sdpa(x["q"], n_valid, o)
+            self.gpu.sync()              # pinned host output is written asynchronously
+            og = o.numpy()
+        else:
+            og = self.gpu.sdpa(x["q"].cuda(), n_valid).cpu().numpy()
+        ref = self.orc.sdpa(x["q"], n_valid)
+        e = err_of(og, ref, self.dtype)
+        self.worst = max(self.worst, e)
+        assert e <= 1.0, f"sdpa mismatch at step {self.step}: {e:.3f} x tolerance"
+        return og, ref
+
+    def commit(self, m):
+        self.gpu.commit(m)
+        self.orc.commit(m)
+
+    def commit_rows(self, m):
+        self.gpu.commit_rows(m)
+        self.orc.commit_rows(m)
+
+    def check_state(self):
+        sg, so = self.gpu.stats(), self.orc.stats()
+        for key in STAT_KEYS:
+            assert sg[key] == so[key], (key, sg[key], so[key])
+        assert self.gpu.valid() == list(self.orc.valid())
+        Kg, Vg = self.gpu.kv()
+        Ko, Vo = self.orc.read_cache()
+        if self.dtype == "bf16":
+            kg = Kg.cpu().view(torch.int16).numpy().view(np.uint16)
+            vg = Vg.cpu().view(torch.int16).numpy().view(np.uint16)
+        else:
+            kg, vg = Kg.cpu().numpy().view(np.uint32), Vg.cpu().numpy().view(np.uint32)
+            Ko, Vo = Ko.view(np.uint32), Vo.view(np.uint32)
+        assert kg.shape == Ko.shape, (kg.shape, Ko.shape)
+        assert np.array_equal(kg, Ko), "K cache differs"
+        assert np.array_equal(vg, Vo), "V cache differs"
+
+    def close(self):
+        self.gpu.close()
+        self.orc.close()

@@ -1,0 +1,177 @@
+"""GPU parity: libbmc (sm_100a kernels, called through the C ABI) against the
+CPU oracle, element by element, on the same seeded inputs.
+
+Sizes span several 16 KiB tiles, ragged tails (r not dividing N, caps not a
+multiple of the tile rows), multi-CTA split-K segments and every policy.
+"""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from harness import Pair  # noqa: E402
+from paper_2511_12031_b200 import bmc, synth  # noqa: E402
+
+
+@pytest.fixture(autouse=True, scope="module")
+def _built():
+    import __graft_entry__
+    __graft_entry__.build()
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+
+
+def _decode(p: Pair, steps: int, check_every: int = 1, state_every: int = 0):
+    for i in range(steps):
+        p.append()
+        if (i + 1) % check_every == 0 or i + 1 == steps:
+            p.sdpa()
+        if state_every and (i + 1) % state_every == 0:
+            p.check_state()
+    p.check_state()
+
+
+def test_toy_config_full_run():
+    """BASELINE configs[0]: B=1, 2 heads, head_dim 64, N_max=128, r=16, fp32,
+    128 decode steps, every SDPA output and the final state checked."""
+    p = Pair(1, 2, 2, 64, 16, 128, dtype="f32")
+    _decode(p, 128, check_every=1, state_every=16)
+    s = p.gpu.stats()
+    assert s["alloc_events"] == 8 and s["copy_events"] == 7
+    p.close()
+
+
+@pytest.mark.parametrize("policy,r", [("bmc", 1), ("bmc", 7), ("bmc", 32), ("bmc", 300),
+                                      ("iterative", 1), ("upfront", 300)])
+def test_policies_bf16_d128(policy, r):
+    """Every policy, bf16 head_dim 128, ragged N=300 (r does not divide N)."""
+    p = Pair(3, 4, 4, 128, r, 300, dtype="bf16", policy=policy, seed=3)
+    _decode(p, 300, check_every=13, state_every=97)
+    p.close()
+
+
+@pytest.mark.parametrize("dtype,D", [("bf16", 64), ("f32", 128), ("f32", 64)])
+def test_dtypes_and_head_dims(dtype, D):
+    p = Pair(2, 3, 3, D, 24, 200, dtype=dtype, seed=5)
+    _decode(p, 200, check_every=9, state_every=50)
+    p.close()
+
+
+@pytest.mark.parametrize("H_kv,H_q", [(2, 8), (8, 32), (1, 4)])
+def test_gqa(H_kv, H_q):
+    """GQA: G = H_q/H_kv query heads share one KV head."""
+    p = Pair(2, H_kv, H_q, 128, 64, 256, dtype="bf16", seed=7)
+    _decode(p, 256, check_every=17)
+    p.close()
+
+
+@pytest.mark.parametrize("variant", ["peaky", "outlier"])
+def test_structured_inputs(variant):
+    """Near one-hot softmax (Q x 8) and +large-score outliers (max subtraction)."""
+    p = Pair(2, 4, 4, 128, 32, 160, dtype="bf16", seed=9, variant=variant)
+    _decode(p, 160, check_every=5)
+    p.close()
+
+
+@pytest.mark.parametrize("ctas", [1, 2, 3, 7, 64, 500])
+def test_split_k_segments(ctas):
+    """Force the number of persistent CTAs so units split across many / few
+    CTAs (split-K combine) and CTAs span many units."""
+    p = Pair(2, 4, 8, 128, 50, 700, dtype="bf16", seed=11, ctas=ctas)
+    _decode(p, 700, check_every=37)
+    p.close()
+
+
+@pytest.mark.parametrize("B,H_kv,H_q,k", [(1, 1, 1, 4), (4, 2, 2, 4), (3, 2, 4, 3),
+                                          (2, 2, 16, 8)])
+def test_speculative_chain(B, H_kv, H_q, k):
+    """SD in the padded rows: append x_last, place k chain drafts
+    (admission-limited), verify with t = 1 + k_adm query rows, per-row commit
+    with rollback of rejected rows.  (2,2,16,8) gives M = 8*9 = 72
+    query rows per KV head (the 70B-shaped verify)."""
+    p = Pair(B, H_kv, H_q, 128, 16, 400, dtype="bf16", seed=13)
+    for _ in range(5):
+        p.append()
+    p.sdpa()
+    it = 0
+    while p.orc.stats()["valid_max"] < 380:
+        p.append()
+        k_adm = p.spec_write(k)
+        p.sdpa(n_valid=-1)
+        m = synth.acceptance(13, it, B, k_adm)
+        p.commit_rows(m)
+        it += 1
+        if it % 10 == 0:
+            p.check_state()
+    p.check_state()
+    p.close()
+
+
+def test_sd_admission_and_allocs():
+    """Admission never grows the cache; the allocation count is the plain-BMC
+    one."""
+    p = Pair(2, 2, 2, 128, 8, 64, dtype="bf16", seed=15)
+    p.append()
+    allocs = p.gpu.stats()["alloc_events"]
+    assert p.spec_write(20) == 7
+    p.sdpa()
+    p.commit(3)
+    assert p.gpu.stats()["alloc_events"] == allocs
+    p.check_state()
+    p.close()
+
+
+def test_host_pointer_io():
+    """The end-to-end path: host inputs staged inside the call, host output."""
+    p = Pair(2, 2, 4, 128, 16, 100, dtype="bf16", seed=17, host_io=True)
+    _decode(p, 100, check_every=7)
+    p.append()
+    p.spec_write(3)
+    p.sdpa()
+    p.commit(1)
+    p.check_state()
+    p.close()
+
+
+def test_single_row_and_tiny():
+    """n_valid = 1 (single visible row -> O = v exactly up to rounding), B*H = 1."""
+    p = Pair(1, 1, 1, 128, 4, 9, dtype="f32", seed=19)
+    p.append()
+    og, ref = p.sdpa()
+    _decode(p, 8, check_every=1)
+    p.close()
+
+
+def test_error_codes_gpu():
+    g = bmc.KVCache(1, 1, 1, 64, 2, 2, dtype="f32")
+    z = torch.zeros(1, 1, 64, device="cuda")
+    g.append(z, z)
+    g.append(z, z)
+    with pytest.raises(bmc.BMCError) as e:
+        g.append(z, z)
+    assert e.value.code == bmc.BMC_ERR_CAPACITY
+    with pytest.raises(bmc.BMCError) as e:
+        g.commit(1)
+    assert e.value.code == bmc.BMC_ERR_STATE
+    q = torch.zeros(1, 1, 1, 64, device="cuda")
+    with pytest.raises(bmc.BMCError) as e:
+        g.sdpa(q, 1)
+    assert e.value.code == bmc.BMC_ERR_STATE
+    g.close()
+
+
+def test_arena_kinds_agree():
+    """VMM arena and stream-ordered pool give identical results."""
+    for kind in (0, 1):
+        p = Pair(2, 2, 2, 128, 8, 120, dtype="bf16", seed=21)
+        p.gpu.set_option(bmc.BMC_OPT_ARENA, kind)
+        _decode(p, 120, check_every=11, state_every=40)
+        p.close()
+
+
+def test_launch_count_increments():
+    n0 = bmc.bmc_launch_count()
+    p = Pair(1, 2, 2, 128, 4, 16, dtype="bf16")
+    _decode(p, 16, check_every=4)
+    assert bmc.bmc_launch_count() - n0 >= 16 + 4
+    p.close()
