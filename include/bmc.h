@@ -116,6 +116,14 @@ int bmc_commit(bmc_t h, int n_accepted);
 /* bmc_commit_rows: per-row acceptance, n_accepted_host[B] (host array). */
 int bmc_commit_rows(bmc_t h, const int* n_accepted_host);
 
+/* bmc_decode_step: one plain decode step of a whole model, i.e. for every
+   layer l = 0..L-1: bmc_append(hs[l], K[l], V[l]) then
+   bmc_sdpa(hs[l], Q[l], n_valid, O[l]) (n_valid = the committed length AFTER
+   the append, or BMC_PER_ROW).  Arrays of L pointers.  Every layer is
+   validated before anything is enqueued.  One call instead of 2L. */
+int bmc_decode_step(const bmc_t* hs, int L, const void* const* K, const void* const* V,
+                    const void* const* Q, float* const* O, int n_valid);
+
 /* bmc_destroy: synchronises the handle's stream, frees the cache memory. */
 int bmc_destroy(bmc_t h);
 
@@ -150,7 +158,8 @@ int bmc_sync(bmc_t h);
 /* Tuning / test options (key, value).  Keys:
      1 BMC_OPT_ATTN_CTAS      CTAs of the attention kernel (0 = auto)
      2 BMC_OPT_ATTN_PATH      0 auto, 1 CUDA-core split-K, 2 tcgen05 verify
-     3 BMC_OPT_ARENA          0 VMM arena (default), 1 stream-ordered pool  */
+     3 BMC_OPT_ARENA          0 VMM ping-pong slots, 1 stream-ordered pool
+                              (default; takes effect at the next growth)  */
 #define BMC_OPT_ATTN_CTAS 1
 #define BMC_OPT_ATTN_PATH 2
 #define BMC_OPT_ARENA 3

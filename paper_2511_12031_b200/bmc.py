@@ -34,7 +34,7 @@ _NAMES = {0: "OK", -1: "ARG", -2: "STATE", -3: "CAPACITY", -4: "OOM", -5: "CUDA"
           -6: "UNSUPPORTED"}
 
 EXPORTS = ["bmc_create", "bmc_create_ex", "bmc_append", "bmc_spec_write", "bmc_sdpa",
-           "bmc_commit", "bmc_commit_rows", "bmc_destroy", "bmc_stats", "bmc_kv_view",
+           "bmc_commit", "bmc_commit_rows", "bmc_decode_step", "bmc_destroy", "bmc_stats", "bmc_kv_view",
            "bmc_valid", "bmc_read_cache", "bmc_sync", "bmc_set_option", "bmc_launch_count", "bmc_last_error"]
 
 
@@ -74,6 +74,7 @@ def load(path: str = SO_PATH):
     L.bmc_commit.argtypes = [vp, i]
     L.bmc_commit_rows.argtypes = [vp, ctypes.POINTER(ctypes.c_int)]
     L.bmc_destroy.argtypes = [vp]
+    L.bmc_decode_step.argtypes = [vp, i, vp, vp, vp, vp, i]
     L.bmc_stats.argtypes = [vp, ctypes.POINTER(Stats)]
     L.bmc_kv_view.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(i)]
     L.bmc_valid.argtypes = [vp, ctypes.POINTER(ctypes.c_int)]
@@ -142,6 +143,23 @@ def bmc_commit(h, n_accepted: int) -> int:
 def bmc_commit_rows(h, n_accepted) -> int:
     arr = (ctypes.c_int * len(n_accepted))(*[int(x) for x in n_accepted])
     return _check(load().bmc_commit_rows(h, arr), "bmc_commit_rows")
+
+
+class StepPlan:
+    """Pointer arrays for bmc_decode_step over L handles (build once, reuse)."""
+
+    def __init__(self, caches):
+        self.L = len(caches)
+        self.hs = (ctypes.c_void_p * self.L)(*[c.h.value for c in caches])
+
+    def ptrs(self, tensors):
+        return (ctypes.c_void_p * self.L)(*[t.data_ptr() for t in tensors])
+
+
+def bmc_decode_step(plan: StepPlan, K, V, Q, O, n_valid: int) -> int:
+    """K, V, Q, O: ctypes pointer arrays from plan.ptrs(...)."""
+    return _check(load().bmc_decode_step(plan.hs, plan.L, K, V, Q, O, n_valid),
+                  "bmc_decode_step")
 
 
 def bmc_destroy(h) -> int:

@@ -52,6 +52,7 @@ struct Driver {
   PFN_cuMemSetAccess set_access = nullptr;
   PFN_cuDeviceGet device_get = nullptr;
   PFN_cuDeviceGetAttribute device_attr = nullptr;
+  PFN_cuMemGetAddressRange range = nullptr;
   bool ok = false;
   bool tried = false;
 };
@@ -78,7 +79,8 @@ const Driver& drv() {
                resolve("cuMemUnmap", &g_drv.unmap) &&
                resolve("cuMemSetAccess", &g_drv.set_access) &&
                resolve("cuDeviceGet", &g_drv.device_get) &&
-               resolve("cuDeviceGetAttribute", &g_drv.device_attr);
+               resolve("cuDeviceGetAttribute", &g_drv.device_attr) &&
+               resolve("cuMemGetAddressRange", &g_drv.range);
   }
   return g_drv;
 }
@@ -299,6 +301,56 @@ void arena_destroy(Arena* a) {
   if (a->base) drv().addr_free(a->base, 4 * a->slot_bytes);
   g_arenas.erase(a);
   delete a;
+}
+
+// ------------------------------------------------------ pointer classes
+// cudaPointerGetAttributes costs microseconds; the hot path calls it for every
+// tensor argument.  Device allocations are remembered by address range (a
+// device range never turns into host memory under UVA), so repeat calls with
+// pointers into known device allocations cost a short scan.
+namespace {
+struct Range { uintptr_t base, end; };
+std::mutex g_rmu;
+std::vector<Range> g_ranges;
+}  // namespace
+
+int pointer_kind(const void* ptr) {
+  const uintptr_t p = (uintptr_t)ptr;
+  {
+    std::lock_guard<std::mutex> lk(g_rmu);
+    for (size_t i = 0; i < g_ranges.size(); ++i) {
+      if (p >= g_ranges[i].base && p < g_ranges[i].end) {
+        if (i > 0) std::swap(g_ranges[i], g_ranges[i - 1]);  // keep hot ranges in front
+        return 0;
+      }
+    }
+  }
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return 2;
+  }
+  if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) {
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (drv().ok && drv().range(&base, &size, (CUdeviceptr)p) == CUDA_SUCCESS && size > 0) {
+      std::lock_guard<std::mutex> lk(g_rmu);
+      if (g_ranges.size() >= 256) g_ranges.pop_back();
+      g_ranges.insert(g_ranges.begin(), Range{(uintptr_t)base, (uintptr_t)base + size});
+    }
+    return 0;
+  }
+  return a.type == cudaMemoryTypeHost ? 1 : 2;
+}
+
+void forget_range(const void* ptr) {
+  std::lock_guard<std::mutex> lk(g_rmu);
+  const uintptr_t p = (uintptr_t)ptr;
+  for (size_t i = 0; i < g_ranges.size(); ++i)
+    if (p >= g_ranges[i].base && p < g_ranges[i].end) {
+      g_ranges.erase(g_ranges.begin() + i);
+      return;
+    }
 }
 
 }  // namespace bmc

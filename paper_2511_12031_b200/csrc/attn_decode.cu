@@ -40,7 +40,6 @@ namespace bmc {
 namespace attn {
 
 constexpr int kStageBytes = 16384;  // per operand (K or V) per stage
-constexpr int kStages = 4;
 constexpr int kConsumerWarps = 8;
 constexpr int kThreads = kConsumerWarps * 32;  // 2 warps per SMSP -> 255-register budget
 constexpr float kLog2e = 1.4426950408889634f;
@@ -132,7 +131,7 @@ struct Params {
   int valid[BMC_MAX_B];
 };
 
-template <typename T, int D, int MAXM, int CPL>
+template <typename T, int D, int MAXM, int CPL, int CTAS>
 struct Cfg {
   static constexpr int ROWB = D * (int)sizeof(T);
   static constexpr int CH = ROWB / 16;          // chunks per row
@@ -143,12 +142,13 @@ struct Cfg {
   static constexpr int PASSES = RPW / RPP;
   static constexpr int EPC = Chunk<T>::EPC;
   static constexpr int EL2 = CPL * EPC / 2;     // float2 per lane per row
+  static constexpr int STAGES = CTAS == 2 ? 3 : 4;
   static_assert(LPR >= 1 && LPR <= 32 && RPW % RPP == 0 && PASSES >= 1, "bad tiling");
   static_assert(CPL == 1 || CPL == 2, "CPL");
-  static constexpr size_t kRing = (size_t)kStages * 2 * kStageBytes;
-  static constexpr size_t kMerge = (size_t)kConsumerWarps * MAXM * D * 4;
+  static constexpr size_t kRing = (size_t)STAGES * 2 * kStageBytes;
+  static constexpr size_t kMerge = (size_t)kConsumerWarps * D * 4;          // one query at a time
   static constexpr size_t kSmall = (size_t)kConsumerWarps * MAXM * 2 * 4 + 64;
-  static constexpr size_t kBars = 2 * kStages * 8;
+  static constexpr size_t kBars = 2 * STAGES * 8;
   static constexpr size_t kSmem = kRing + kMerge + kSmall + kBars + 128;
 };
 
@@ -160,27 +160,30 @@ __device__ __forceinline__ long long tile_begin(int c, long long NT, int C) {
   return (long long)c * NT / C;
 }
 
-template <typename T, int D, int MAXM, int CPL>
-__global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(const Params p) {
-  using C = Cfg<T, D, MAXM, CPL>;
+template <typename T, int D, int MAXM, int CPL, int CTAS>
+__global__ void __launch_bounds__(kThreads, CTAS) attn_decode_kernel(const Params p) {
+  using C = Cfg<T, D, MAXM, CPL, CTAS>;
+  constexpr int S = C::STAGES;
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* ring = smem;                                             // [stage][K|V][16 KiB]
-  float* sm_o = reinterpret_cast<float*>(smem + C::kRing);          // [warp][MAXM][D]
-  float* sm_m = sm_o + (size_t)kConsumerWarps * MAXM * D;           // [warp][MAXM]
+  float* sm_o = reinterpret_cast<float*>(smem + C::kRing);          // [warp][D]
+  float* sm_m = sm_o + (size_t)kConsumerWarps * D;                  // [warp][MAXM]
   float* sm_l = sm_m + kConsumerWarps * MAXM;                       // [warp][MAXM]
   int* sm_flag = reinterpret_cast<int*>(sm_l + kConsumerWarps * MAXM);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kRing + C::kMerge + C::kSmall);
-  uint64_t* empty = full + kStages;
+  uint64_t* empty = full + S;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const int tid = threadIdx.x;
   const int cta = blockIdx.x;
   const long long NT = p.total_tiles;
   const long long t_begin = tile_begin(cta, NT, p.ctas);
   const long long t_end = tile_begin(cta + 1, NT, p.ctas);
+  const int tpu = p.tpu;
 
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kConsumerWarps);
     }
@@ -188,28 +191,31 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(const Params p
   }
   __syncthreads();
 
-  // producer state (thread 0 only): tiles are issued in order
+  // ---- producer state (thread 0 only): tiles are issued in order
   uint64_t pol = 0;
-  long long next_issue = t_begin;
-  auto issue = [&](long long i) {
-    const long long k = i - t_begin;
-    const int s = (int)(k % kStages);
-    const long long u = i / p.tpu;
-    const long long row0 = (i % p.tpu) * C::TR;
+  long long pi = t_begin;                // next tile to issue
+  long long pu = t_begin / tpu;          // its unit
+  int pj = (int)(t_begin % tpu);         // its tile within the unit
+  int ps_stage = 0;
+  auto issue = [&]() {
+    const long long row0 = (long long)pj * C::TR;
     const long long rows = min((long long)C::TR, p.cap - row0);
     const uint32_t bytes = (uint32_t)(rows * C::ROWB);
-    const size_t off = (size_t)(u * p.cap + row0) * C::ROWB;
-    uint8_t* dk = ring + (size_t)s * 2 * kStageBytes;
-    mbar_expect_tx(&full[s], 2 * bytes);
-    bulk_g2s(dk, p.K + off, bytes, &full[s], pol);
-    bulk_g2s(dk + kStageBytes, p.V + off, bytes, &full[s], pol);
+    const size_t off = (size_t)(pu * p.cap + row0) * C::ROWB;
+    uint8_t* dk = ring + (size_t)ps_stage * 2 * kStageBytes;
+    mbar_expect_tx(&full[ps_stage], 2 * bytes);
+    bulk_g2s(dk, p.K + off, bytes, &full[ps_stage], pol);
+    bulk_g2s(dk + kStageBytes, p.V + off, bytes, &full[ps_stage], pol);
+    ++pi;
+    if (++pj == tpu) { pj = 0; ++pu; }
+    if (++ps_stage == S) ps_stage = 0;
   };
-  if (threadIdx.x == 0) {
+  if (tid == 0) {
     pol = evict_first_policy();
-    for (; next_issue < t_end && next_issue < t_begin + kStages; ++next_issue) issue(next_issue);
+    while (pi < t_end && pi < t_begin + S) issue();
   }
 
-  // -------------------------------------------------------------- consumers
+  // ---- consumers (all 8 warps)
   const int rip = lane / C::LPR;   // row within a pass
   const int cl = lane % C::LPR;    // lane within the row
   int chunk[CPL];
@@ -220,24 +226,24 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(const Params p
   float2 o2[MAXM][C::EL2];
   float mw[MAXM], lsum[MAXM];
   int nvis[MAXM];
-  long long cur_u = -1;
   int max_vis = 0;
   bool seg_first = true;
+  bool seg_start = true;
+
+  long long u = t_begin / tpu;
+  int j = (int)(t_begin % tpu);
+  int stage = 0;
+  uint32_t phase = 0;
+  int b = (int)(u / p.H_kv);
+  int g = (int)(u - (long long)b * p.H_kv);
 
   for (long long i = t_begin; i < t_end; ++i) {
-    const long long k = i - t_begin;
-    const int s = (int)(k % kStages);
-    const uint32_t ph = (uint32_t)((k / kStages) & 1);
-    const long long u = i / p.tpu;
-    const long long row0 = (i % p.tpu) * C::TR;
+    const long long row0 = (long long)j * C::TR;
     const int rows_in_tile = (int)min((long long)C::TR, p.cap - row0);
-    const int b = (int)(u / p.H_kv);
-    const int g = (int)(u % p.H_kv);
 
-    if (u != cur_u) {
+    if (seg_start) {
       // new segment: load this unit's query rows, reset the softmax state
-      cur_u = u;
-      seg_first = (i == t_begin);
+      seg_start = false;
       const uint8_t* qbase =
           p.Q + ((size_t)((size_t)b * p.H_q + (size_t)g * p.G) * p.t + p.m0) * C::ROWB;
       max_vis = 0;
@@ -268,57 +274,74 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(const Params p
       }
     }
 
-    mbar_wait(&full[s], ph);
-    const uint8_t* sk = ring + (size_t)s * 2 * kStageBytes;
+    mbar_wait(&full[stage], phase);
+    const uint8_t* sk = ring + (size_t)stage * 2 * kStageBytes;
     const uint8_t* sv = sk + kStageBytes;
 
     if (row0 < max_vis) {  // tiles with no visible row for any query are only streamed
-      float sc[C::PASSES][MAXM];
+      // K rows of all passes first (independent loads, then independent FMA chains)
+      float2 kf[C::PASSES][C::EL2];
 #pragma unroll
       for (int ps = 0; ps < C::PASSES; ++ps) {
         const int row = warp * C::RPW + ps * C::RPP + rip;
-        float2 kf[C::EL2];
 #pragma unroll
         for (int c = 0; c < CPL; ++c) {
           const uint4 raw = *reinterpret_cast<const uint4*>(sk + row * C::ROWB + chunk[c] * 16);
-          Chunk<T>::load(raw, kf + c * (C::EPC / 2));
+          Chunk<T>::load(raw, kf[ps] + c * (C::EPC / 2));
         }
-        const long long jr = row0 + row;
+      }
+      float sc[C::PASSES][MAXM];
+#pragma unroll
+      for (int m = 0; m < MAXM; ++m) {
+        if (m < p.M) {
+#pragma unroll
+          for (int ps = 0; ps < C::PASSES; ++ps) {
+            float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int e = 0; e < C::EL2; e += 2) {
+              a0 = __ffma2_rn(q2[m][e], kf[ps][e], a0);
+              if (e + 1 < C::EL2) a1 = __ffma2_rn(q2[m][e + 1], kf[ps][e + 1], a1);
+            }
+            sc[ps][m] = (a0.x + a1.x) + (a0.y + a1.y);
+          }
+        }
+      }
+#pragma unroll
+      for (int off = 1; off < C::LPR; off <<= 1) {
 #pragma unroll
         for (int m = 0; m < MAXM; ++m) {
           if (m < p.M) {
-            float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
-            for (int e = 0; e < C::EL2; ++e) acc = __ffma2_rn(q2[m][e], kf[e], acc);
-            float v = acc.x + acc.y;
-#pragma unroll
-            for (int off = 1; off < C::LPR; off <<= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-            sc[ps][m] = (jr < nvis[m]) ? v : -INFINITY;
+            for (int ps = 0; ps < C::PASSES; ++ps)
+              sc[ps][m] += __shfl_xor_sync(0xffffffffu, sc[ps][m], off);
           }
         }
       }
       // online softmax update (per warp); probabilities overwrite the scores
-      float (&pr)[C::PASSES][MAXM] = sc;
 #pragma unroll
       for (int m = 0; m < MAXM; ++m) {
         if (m < p.M) {
-          float mt = sc[0][m];
+          float mt = -INFINITY;
 #pragma unroll
-          for (int ps = 1; ps < C::PASSES; ++ps) mt = fmaxf(mt, sc[ps][m]);
+          for (int ps = 0; ps < C::PASSES; ++ps) {
+            const long long jr = row0 + warp * C::RPW + ps * C::RPP + rip;
+            if (jr >= nvis[m]) sc[ps][m] = -INFINITY;
+            mt = fmaxf(mt, sc[ps][m]);
+          }
 #pragma unroll
           for (int off = C::LPR; off < 32; off <<= 1)
             mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, off));
           const float mn = fmaxf(mw[m], mt);
           if (mn == -INFINITY) {
 #pragma unroll
-            for (int ps = 0; ps < C::PASSES; ++ps) pr[ps][m] = 0.f;
+            for (int ps = 0; ps < C::PASSES; ++ps) sc[ps][m] = 0.f;
             continue;
           }
           float tsum = 0.f;
 #pragma unroll
           for (int ps = 0; ps < C::PASSES; ++ps) {
-            pr[ps][m] = fast_exp2(sc[ps][m] - mn);
-            tsum += pr[ps][m];
+            sc[ps][m] = fast_exp2(sc[ps][m] - mn);
+            tsum += sc[ps][m];
           }
           if (mn != mw[m]) {
             const float alpha = fast_exp2(mw[m] - mn);
@@ -331,46 +354,65 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(const Params p
           lsum[m] += tsum;
         }
       }
-      // P . V
+      // P . V (rows past the end of a ragged last tile were never loaded)
+      float2 vf[C::PASSES][C::EL2];
+#pragma unroll
+      for (int ps = 0; ps < C::PASSES; ++ps) {
+        const int row = warp * C::RPW + ps * C::RPP + rip;
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          const uint4 raw = *reinterpret_cast<const uint4*>(sv + row * C::ROWB + chunk[c] * 16);
+          Chunk<T>::load(raw, vf[ps] + c * (C::EPC / 2));
+        }
+      }
 #pragma unroll
       for (int ps = 0; ps < C::PASSES; ++ps) {
         const int row = warp * C::RPW + ps * C::RPP + rip;
         if (row < rows_in_tile) {
-          float2 vf[C::EL2];
-#pragma unroll
-          for (int c = 0; c < CPL; ++c) {
-            const uint4 raw =
-                *reinterpret_cast<const uint4*>(sv + row * C::ROWB + chunk[c] * 16);
-            Chunk<T>::load(raw, vf + c * (C::EPC / 2));
-          }
 #pragma unroll
           for (int m = 0; m < MAXM; ++m) {
             if (m < p.M) {
-              const float2 pp = make_float2(pr[ps][m], pr[ps][m]);
+              const float2 pp = make_float2(sc[ps][m], sc[ps][m]);
 #pragma unroll
-              for (int e = 0; e < C::EL2; ++e) o2[m][e] = __ffma2_rn(pp, vf[e], o2[m][e]);
+              for (int e = 0; e < C::EL2; ++e) o2[m][e] = __ffma2_rn(pp, vf[ps][e], o2[m][e]);
             }
           }
         }
       }
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
-    if (threadIdx.x == 0 && next_issue < t_end) {
+    if (lane == 0) mbar_arrive(&empty[stage]);
+    if (tid == 0 && pi < t_end) {
       // refill this stage once every warp has released it
-      mbar_wait(&empty[s], ph);
-      issue(next_issue++);
+      mbar_wait(&empty[stage], phase);
+      issue();
     }
+    if (++stage == S) { stage = 0; phase ^= 1; }
 
     // ------------------------------------------------------ segment end
-    const bool seg_last = (i + 1 == t_end) || ((i + 1) / p.tpu != u);
+    const bool seg_last = (i + 1 == t_end) || (j + 1 == tpu);
+    const long long cu = u;
+    const int cb = b, cg = g;
+    if (++j == tpu) {
+      j = 0;
+      ++u;
+      if (++g == p.H_kv) { g = 0; ++b; }
+    }
     if (!seg_last) continue;
+    seg_start = true;
 
     if (lane == 0) {
 #pragma unroll
       for (int m = 0; m < MAXM; ++m) sm_m[warp * MAXM + m] = mw[m];
     }
     consumer_sync();
+    const long long ufirst = cu * tpu, ulast = ufirst + tpu - 1;
+    const int c_lo = cta_of_tile(ufirst, NT, p.ctas);
+    const int c_hi = cta_of_tile(ulast, NT, p.ctas);
+    const int nseg = c_hi - c_lo + 1;
+    const size_t obase = ((size_t)((size_t)cb * p.H_q + (size_t)cg * p.G) * p.t + p.m0) * D;
+    const size_t rec = (size_t)p.M * (D + 2);
+    float* my = p.ws + ((size_t)cta * 2 + (seg_first ? 0 : 1)) * rec;
 #pragma unroll
     for (int m = 0; m < MAXM; ++m) {
       if (m >= p.M) continue;
@@ -399,7 +441,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(const Params p
         }
       }
       if (rip == 0) {
-        float* dst = sm_o + ((size_t)warp * MAXM + m) * D;
+        float* dst = sm_o + (size_t)warp * D;
 #pragma unroll
         for (int c = 0; c < CPL; ++c) {
           const int x0 = (cl + C::LPR * c) * C::EPC;
@@ -412,66 +454,50 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(const Params p
         }
         if (lane == 0) sm_l[warp * MAXM + m] = l * f;
       }
+      consumer_sync();
+      if (tid < D) {
+        float o = 0.f, lt = 0.f;
+#pragma unroll
+        for (int w = 0; w < kConsumerWarps; ++w) {
+          o += sm_o[(size_t)w * D + tid];
+          lt += sm_l[w * MAXM + m];
+        }
+        if (nseg == 1) {
+          p.O[obase + (size_t)m * D + tid] = o / lt;
+        } else {
+          my[(size_t)m * D + tid] = o;
+          if (tid == 0) {
+            my[(size_t)p.M * D + m] = mc;
+            my[(size_t)p.M * D + p.M + m] = lt;
+          }
+        }
+      }
+      consumer_sync();
     }
-    consumer_sync();
-
-    // CTA-level result of this segment
-    const long long ufirst = u * p.tpu, ulast = ufirst + p.tpu - 1;
-    const int c_lo = cta_of_tile(ufirst, NT, p.ctas);
-    const int c_hi = cta_of_tile(ulast, NT, p.ctas);
-    const int nseg = c_hi - c_lo + 1;
-    const int tid = threadIdx.x;
-    const size_t obase = ((size_t)((size_t)b * p.H_q + (size_t)g * p.G) * p.t + p.m0) * D;
-    if (nseg == 1) {
-      for (int idx = tid; idx < p.M * D; idx += kConsumerWarps * 32) {
-        const int m = idx / D, x = idx % D;
-        float o = 0.f, l = 0.f;
-        for (int w = 0; w < kConsumerWarps; ++w) {
-          o += sm_o[((size_t)w * MAXM + m) * D + x];
-          l += sm_l[w * MAXM + m];
-        }
-        p.O[obase + idx] = o / l;
-      }
-    } else {
-      const size_t rec = (size_t)p.M * (D + 2);
-      float* my = p.ws + ((size_t)cta * 2 + (seg_first ? 0 : 1)) * rec;
-      for (int idx = tid; idx < p.M * D; idx += kConsumerWarps * 32) {
-        const int m = idx / D, x = idx % D;
-        float o = 0.f;
-        for (int w = 0; w < kConsumerWarps; ++w) o += sm_o[((size_t)w * MAXM + m) * D + x];
-        my[idx] = o;
-      }
-      if (tid < p.M) {
-        float mc = -INFINITY, l = 0.f;
-        for (int w = 0; w < kConsumerWarps; ++w) {
-          mc = fmaxf(mc, sm_m[w * MAXM + tid]);
-          l += sm_l[w * MAXM + tid];
-        }
-        my[(size_t)p.M * D + tid] = mc;
-        my[(size_t)p.M * D + p.M + tid] = l;
-      }
+    seg_first = false;
+    if (nseg > 1) {
       __threadfence();
       consumer_sync();
       if (tid == 0) {
-        const int old = atomicAdd(&p.counters[u], 1);
+        const int old = atomicAdd(&p.counters[cu], 1);
         *sm_flag = (old == nseg - 1);
       }
       consumer_sync();
       if (*sm_flag) {
         __threadfence();
-        // merge the nseg partial records of unit u (split-K combine)
-        for (int idx = tid; idx < p.M * D; idx += kConsumerWarps * 32) {
+        // merge the nseg partial records of unit cu (split-K combine)
+        for (int idx = tid; idx < p.M * D; idx += kThreads) {
           const int m = idx / D;
           float mu = -INFINITY;
           for (int c = c_lo; c <= c_hi; ++c) {
-            const long long fu = tile_begin(c, NT, p.ctas) / p.tpu;
-            const float* r = p.ws + ((size_t)c * 2 + (fu == u ? 0 : 1)) * rec;
+            const long long fu = tile_begin(c, NT, p.ctas) / tpu;
+            const float* r = p.ws + ((size_t)c * 2 + (fu == cu ? 0 : 1)) * rec;
             mu = fmaxf(mu, __ldcg(r + (size_t)p.M * D + m));
           }
           float o = 0.f, l = 0.f;
           for (int c = c_lo; c <= c_hi; ++c) {
-            const long long fu = tile_begin(c, NT, p.ctas) / p.tpu;
-            const float* r = p.ws + ((size_t)c * 2 + (fu == u ? 0 : 1)) * rec;
+            const long long fu = tile_begin(c, NT, p.ctas) / tpu;
+            const float* r = p.ws + ((size_t)c * 2 + (fu == cu ? 0 : 1)) * rec;
             const float mk = __ldcg(r + (size_t)p.M * D + m);
             const float w = (mk == -INFINITY) ? 0.f : fast_exp2(mk - mu);
             o += __ldcg(r + idx) * w;
@@ -479,35 +505,41 @@ __global__ void __launch_bounds__(kThreads, 1) attn_decode_kernel(const Params p
           }
           p.O[obase + idx] = o / l;
         }
-        if (tid == 0) p.counters[u] = 0;
+        if (tid == 0) p.counters[cu] = 0;
       }
+      consumer_sync();  // the flag and merge buffers are reused by the next segment
     }
-    consumer_sync();  // shared merge buffers are reused by the next segment
   }
 }
 
-template <typename T, int D, int MAXM, int CPL>
-cudaError_t launch_t(const Params& prm, cudaStream_t s) {
-  using C = Cfg<T, D, MAXM, CPL>;
-  auto kern = attn_decode_kernel<T, D, MAXM, CPL>;
-  static bool attr_set = false;  // per instantiation
-  if (!attr_set) {
+template <typename T, int D, int MAXM, int CPL, int CTAS>
+cudaError_t launch_t(const Params& prm_in, int num_sms, cudaStream_t s) {
+  using C = Cfg<T, D, MAXM, CPL, CTAS>;
+  auto kern = attn_decode_kernel<T, D, MAXM, CPL, CTAS>;
+  static int attr_dev = -1;  // per instantiation
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev != dev) {
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kSmem);
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    attr_dev = dev;
   }
-  kern<<<prm.ctas, kThreads, C::kSmem, s>>>(prm);
+  Params prm = prm_in;
+  int ctas = prm.ctas > 0 ? prm.ctas : num_sms * CTAS;
+  if (ctas > prm.total_tiles) ctas = (int)prm.total_tiles;
+  prm.ctas = ctas;
+  kern<<<ctas, kThreads, C::kSmem, s>>>(prm);
   count_launch();
   return cudaGetLastError();
 }
 
 template <typename T, int D>
-cudaError_t dispatch_m(const Params& prm, cudaStream_t s) {
-  if (prm.M <= 1) return launch_t<T, D, 1, 2>(prm, s);
-  if (prm.M <= 2) return launch_t<T, D, 2, 2>(prm, s);
-  if (prm.M <= 4) return launch_t<T, D, 4, 2>(prm, s);
-  return launch_t<T, D, 8, 1>(prm, s);
+cudaError_t dispatch_m(const Params& prm, int num_sms, cudaStream_t s) {
+  if (prm.M <= 1) return launch_t<T, D, 1, 2, 2>(prm, num_sms, s);
+  if (prm.M <= 2) return launch_t<T, D, 2, 1, 2>(prm, num_sms, s);
+  if (prm.M <= 4) return launch_t<T, D, 4, 1, 1>(prm, num_sms, s);
+  return launch_t<T, D, 8, 1, 1>(prm, num_sms, s);
 }
 
 }  // namespace attn
@@ -543,9 +575,7 @@ cudaError_t launch_attn_decode(const AttnArgs& a, int num_sms, cudaStream_t s) {
   prm.G = a.H_q / a.H_kv;
   prm.t = a.t;
   prm.Mu = prm.G * a.t;
-  int ctas = a.ctas > 0 ? a.ctas : num_sms;
-  if (ctas > NT) ctas = (int)NT;
-  prm.ctas = ctas;
+  prm.ctas = a.ctas;   // 0 = num_sms x CTAs per SM of the chosen variant
   prm.qscale = attn::kLog2e / sqrtf((float)a.D);
   for (int b = 0; b < a.B; ++b) prm.valid[b] = a.valid[b];
   // query rows in groups of at most 8 per launch (CUDA-core path)
@@ -554,10 +584,11 @@ cudaError_t launch_attn_decode(const AttnArgs& a, int num_sms, cudaStream_t s) {
     prm.M = prm.Mu - m0 < 8 ? prm.Mu - m0 : 8;
     cudaError_t e;
     if (a.dtype == BMC_BF16) {
-      e = a.D == 128 ? attn::dispatch_m<__nv_bfloat16, 128>(prm, s)
-                     : attn::dispatch_m<__nv_bfloat16, 64>(prm, s);
+      e = a.D == 128 ? attn::dispatch_m<__nv_bfloat16, 128>(prm, num_sms, s)
+                     : attn::dispatch_m<__nv_bfloat16, 64>(prm, num_sms, s);
     } else {
-      e = a.D == 128 ? attn::dispatch_m<float, 128>(prm, s) : attn::dispatch_m<float, 64>(prm, s);
+      e = a.D == 128 ? attn::dispatch_m<float, 128>(prm, num_sms, s)
+                     : attn::dispatch_m<float, 64>(prm, num_sms, s);
     }
     if (e != cudaSuccess) return e;
   }

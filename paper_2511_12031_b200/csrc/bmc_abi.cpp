@@ -34,7 +34,7 @@ struct bmc_ctx {
   int staged = 0;
   Buffer kbuf, vbuf;
   bmc::Arena* arena = nullptr;
-  int arena_kind = 0;
+  int arena_kind = 1;   // stream-ordered pool (measured fastest); 0 = VMM slots
   float* ws = nullptr;
   int* counters = nullptr;
   int num_sms = 148;
@@ -89,16 +89,7 @@ static int enter(bmc_t h) {
 static int max_valid(const bmc_t h) { return *std::max_element(h->valid.begin(), h->valid.end()); }
 static int min_valid(const bmc_t h) { return *std::min_element(h->valid.begin(), h->valid.end()); }
 
-// 0 device (or managed), 1 page-locked host, 2 pageable host
-static int ptr_kind(const void* p) {
-  cudaPointerAttributes a;
-  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-    cudaGetLastError();
-    return 2;
-  }
-  if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) return 0;
-  return a.type == cudaMemoryTypeHost ? 1 : 2;
-}
+static int ptr_kind(const void* p) { return bmc::pointer_kind(p); }
 static bool is_device_ptr(const void* p) { return ptr_kind(p) == 0; }
 
 static int ensure_stage_in(bmc_t h, size_t bytes) {
@@ -117,8 +108,10 @@ static int device_inputs(bmc_t h, const void** ptrs, const size_t* bytes, int n,
                          const void** dev) {
   size_t need = 0;
   bool any_host = false;
+  bool dev_ptr[8];
   for (int i = 0; i < n; ++i) {
-    if (!is_device_ptr(ptrs[i])) {
+    dev_ptr[i] = is_device_ptr(ptrs[i]);
+    if (!dev_ptr[i]) {
       any_host = true;
       need += (bytes[i] + 255) / 256 * 256;
     }
@@ -129,7 +122,7 @@ static int device_inputs(bmc_t h, const void** ptrs, const size_t* bytes, int n,
   }
   size_t off = 0;
   for (int i = 0; i < n; ++i) {
-    if (is_device_ptr(ptrs[i])) {
+    if (dev_ptr[i]) {
       dev[i] = ptrs[i];
     } else {
       void* d = (char*)h->stage_in + off;
@@ -371,6 +364,33 @@ int bmc_sdpa(bmc_t h, const void* Q, int n_valid, float* O) {
   if (host_out) {
     CK(h, cudaMemcpyAsync(O, od, o_bytes, cudaMemcpyDeviceToHost, h->stream), "D2H");
     if (out_kind == 2) CK(h, cudaStreamSynchronize(h->stream), "sync");
+  }
+  return 0;
+}
+
+int bmc_decode_step(const bmc_t* hs, int L, const void* const* K, const void* const* V,
+                    const void* const* Q, float* const* O, int n_valid) {
+  if (!hs || L < 1 || !K || !V || !Q || !O) return fail(BMC_ERR_ARG, "null argument");
+  // validate every layer before enqueueing anything
+  for (int l = 0; l < L; ++l) {
+    bmc_t h = hs[l];
+    int rc = enter(h);
+    if (rc) return rc;
+    if (!K[l] || !V[l] || !Q[l] || !O[l]) return fail(BMC_ERR_ARG, "layer %d: null tensor", l);
+    if (h->staged > 0) return fail(BMC_ERR_STATE, "layer %d: drafts are staged", l);
+    if (max_valid(h) >= h->N_max) return fail(BMC_ERR_CAPACITY, "layer %d: cache full", l);
+    if (n_valid == 0) return fail(BMC_ERR_ARG, "n_valid == 0");
+    if (n_valid != BMC_PER_ROW)
+      for (int b = 0; b < h->B; ++b)
+        if (h->valid[b] + 1 != n_valid)
+          return fail(BMC_ERR_STATE, "layer %d: n_valid=%d but row %d will hold %d", l, n_valid,
+                      b, h->valid[b] + 1);
+  }
+  for (int l = 0; l < L; ++l) {
+    int rc = bmc_append(hs[l], K[l], V[l]);
+    if (rc) return rc;
+    rc = bmc_sdpa(hs[l], Q[l], n_valid, O[l]);
+    if (rc) return rc;
   }
   return 0;
 }

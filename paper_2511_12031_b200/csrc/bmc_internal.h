@@ -83,4 +83,9 @@ int arena_alloc(Arena* a, int tensor, size_t bytes, int kind, const Buffer* keep
 int arena_release(Arena* a, Buffer* b, cudaStream_t s);
 void arena_destroy(Arena* a);
 
+// 0 device / managed, 1 page-locked host, 2 pageable host (cached by range).
+int pointer_kind(const void* p);
+// Drop a cached device range (its memory is being freed or unmapped).
+void forget_range(const void* p);
+
 }  // namespace bmc

@@ -123,7 +123,7 @@ def test_sd_admission_and_allocs():
 
 def test_host_pointer_io():
     """The end-to-end path: host inputs staged inside the call, host output."""
-    p = Pair(2, 2, 4, 128, 16, 100, dtype="bf16", seed=17, host_io=True)
+    p = Pair(2, 2, 4, 128, 16, 110, dtype="bf16", seed=17, host_io=True)
     _decode(p, 100, check_every=7)
     p.append()
     p.spec_write(3)
