@@ -112,23 +112,34 @@ struct Chunk<float> {
   }
 };
 
-struct Params {
-  const uint8_t* K;
+// One layer of a launch (host fills it; kernel parameter space).
+struct LayerDesc {
+  const uint8_t* K;      // cache [U][cap][D]
   const uint8_t* V;
-  const uint8_t* Q;
-  float* O;
-  float* ws;
-  int* counters;
+  const uint8_t* Q;      // [B][H_q][t][D]
+  float* O;              // [B][H_q][t][D]
+  const uint8_t* Knew;   // pending appended row per unit [B][H_kv][D] (n_app == 1)
+  const uint8_t* Vnew;
+  const uint8_t* Kd;     // pending drafts [B][H_kv][kd_stride][D] (n_draft rows)
+  const uint8_t* Vd;
+  float* ws;             // partial records of this layer's split units
+  int* counters;         // [U] arrival counters, zero between launches
   long long cap;
-  long long total_tiles;  // U * TPU
-  int tpu;                // tiles per unit
-  int H_kv, H_q, G, t;
-  int M;                  // query rows handled by this launch (<= MAXM)
+  long long tile0;       // first tile of this layer in the launch's tile stream
+  int tpu;               // tiles per unit
+  int n_app, n_draft, kd_stride;
+};
+
+template <int MAXL>
+struct Params {
+  long long total_tiles;
+  int L, U, H_kv, H_q, G, t;
+  int M;                  // query rows per unit handled by this launch (<= MAXM)
   int m0;                 // first query row of the unit handled by this launch
-  int Mu;                 // query rows per unit (G * t)
   int ctas;
   float qscale;           // log2(e) / sqrt(D)
-  int valid[BMC_MAX_B];
+  int valid[BMC_MAX_B];   // committed rows per batch row (incl. a pending append)
+  LayerDesc layer[MAXL];
 };
 
 template <typename T, int D, int MAXM, int CPL, int CTAS>
@@ -160,8 +171,39 @@ __device__ __forceinline__ long long tile_begin(int c, long long NT, int C) {
   return (long long)c * NT / C;
 }
 
-template <typename T, int D, int MAXM, int CPL, int CTAS>
-__global__ void __launch_bounds__(kThreads, CTAS) attn_decode_kernel(const Params p) {
+// Position in the tile stream: layer l, unit u (= b*H_kv + g), tile j of u.
+struct Cursor {
+  int l, b, g, j;
+  long long u;
+};
+
+template <int MAXL>
+__device__ __forceinline__ Cursor locate(const Params<MAXL>& p, long long tile) {
+  int l = 0;
+  while (l + 1 < p.L && p.layer[l + 1].tile0 <= tile) ++l;
+  const long long local = tile - p.layer[l].tile0;
+  const int tpu = p.layer[l].tpu;
+  Cursor c;
+  c.l = l;
+  c.u = local / tpu;
+  c.j = (int)(local - c.u * tpu);
+  c.b = (int)(c.u / p.H_kv);
+  c.g = (int)(c.u - (long long)c.b * p.H_kv);
+  return c;
+}
+
+template <int MAXL>
+__device__ __forceinline__ void advance(const Params<MAXL>& p, Cursor& c) {
+  if (++c.j == p.layer[c.l].tpu) {
+    c.j = 0;
+    ++c.u;
+    if (++c.g == p.H_kv) { c.g = 0; ++c.b; }
+    if (c.u == p.U) { c.u = 0; c.b = 0; c.g = 0; ++c.l; }
+  }
+}
+
+template <typename T, int D, int MAXM, int CPL, int CTAS, int MAXL>
+__global__ void __launch_bounds__(kThreads, CTAS) attn_step_kernel(const __grid_constant__ Params<MAXL> p) {
   using C = Cfg<T, D, MAXM, CPL, CTAS>;
   constexpr int S = C::STAGES;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -180,7 +222,6 @@ __global__ void __launch_bounds__(kThreads, CTAS) attn_decode_kernel(const Param
   const long long NT = p.total_tiles;
   const long long t_begin = tile_begin(cta, NT, p.ctas);
   const long long t_end = tile_begin(cta + 1, NT, p.ctas);
-  const int tpu = p.tpu;
 
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
@@ -193,21 +234,21 @@ __global__ void __launch_bounds__(kThreads, CTAS) attn_decode_kernel(const Param
 
   // ---- producer state (thread 0 only): tiles are issued in order
   uint64_t pol = 0;
-  long long pi = t_begin;                // next tile to issue
-  long long pu = t_begin / tpu;          // its unit
-  int pj = (int)(t_begin % tpu);         // its tile within the unit
+  long long pi = t_begin;
+  Cursor pc = locate(p, t_begin);
   int ps_stage = 0;
   auto issue = [&]() {
-    const long long row0 = (long long)pj * C::TR;
-    const long long rows = min((long long)C::TR, p.cap - row0);
+    const LayerDesc& ld = p.layer[pc.l];
+    const long long row0 = (long long)pc.j * C::TR;
+    const long long rows = min((long long)C::TR, ld.cap - row0);
     const uint32_t bytes = (uint32_t)(rows * C::ROWB);
-    const size_t off = (size_t)(pu * p.cap + row0) * C::ROWB;
+    const size_t off = (size_t)(pc.u * ld.cap + row0) * C::ROWB;
     uint8_t* dk = ring + (size_t)ps_stage * 2 * kStageBytes;
     mbar_expect_tx(&full[ps_stage], 2 * bytes);
-    bulk_g2s(dk, p.K + off, bytes, &full[ps_stage], pol);
-    bulk_g2s(dk + kStageBytes, p.V + off, bytes, &full[ps_stage], pol);
+    bulk_g2s(dk, ld.K + off, bytes, &full[ps_stage], pol);
+    bulk_g2s(dk + kStageBytes, ld.V + off, bytes, &full[ps_stage], pol);
     ++pi;
-    if (++pj == tpu) { pj = 0; ++pu; }
+    advance(p, pc);
     if (++ps_stage == S) ps_stage = 0;
   };
   if (tid == 0) {
@@ -229,23 +270,24 @@ __global__ void __launch_bounds__(kThreads, CTAS) attn_decode_kernel(const Param
   int max_vis = 0;
   bool seg_first = true;
   bool seg_start = true;
+  long long seg_tile0 = t_begin;   // first global tile of the current unit
 
-  long long u = t_begin / tpu;
-  int j = (int)(t_begin % tpu);
+  Cursor cc = locate(p, t_begin);
   int stage = 0;
   uint32_t phase = 0;
-  int b = (int)(u / p.H_kv);
-  int g = (int)(u - (long long)b * p.H_kv);
 
   for (long long i = t_begin; i < t_end; ++i) {
-    const long long row0 = (long long)j * C::TR;
-    const int rows_in_tile = (int)min((long long)C::TR, p.cap - row0);
+    const LayerDesc& ld = p.layer[cc.l];
+    const long long row0 = (long long)cc.j * C::TR;
+    const int rows_in_tile = (int)min((long long)C::TR, ld.cap - row0);
+    const int vb = p.valid[cc.b];
 
     if (seg_start) {
       // new segment: load this unit's query rows, reset the softmax state
       seg_start = false;
+      seg_tile0 = i - cc.j;
       const uint8_t* qbase =
-          p.Q + ((size_t)((size_t)b * p.H_q + (size_t)g * p.G) * p.t + p.m0) * C::ROWB;
+          ld.Q + ((size_t)((size_t)cc.b * p.H_q + (size_t)cc.g * p.G) * p.t + p.m0) * C::ROWB;
       max_vis = 0;
 #pragma unroll
       for (int m = 0; m < MAXM; ++m) {
@@ -258,7 +300,7 @@ __global__ void __launch_bounds__(kThreads, CTAS) attn_decode_kernel(const Param
           q2[m][e] = make_float2(0.f, 0.f);
         }
         if (m < p.M) {
-          nvis[m] = p.valid[b] + (p.m0 + m) % p.t;
+          nvis[m] = vb + (p.m0 + m) % p.t;
           max_vis = max(max_vis, nvis[m]);
 #pragma unroll
           for (int c = 0; c < CPL; ++c) {
@@ -275,8 +317,47 @@ __global__ void __launch_bounds__(kThreads, CTAS) attn_decode_kernel(const Param
     }
 
     mbar_wait(&full[stage], phase);
-    const uint8_t* sk = ring + (size_t)stage * 2 * kStageBytes;
-    const uint8_t* sv = sk + kStageBytes;
+    uint8_t* sk = ring + (size_t)stage * 2 * kStageBytes;
+    uint8_t* sv = sk + kStageBytes;
+
+    // ---- fused KV-cache update: rows appended / drafted since the last
+    // launch are written into the cache here (P:L609 in-place update) and
+    // patched into the staged tile, so no separate write kernel runs.
+    {
+      const int a_row = ld.n_app ? vb - 1 : -1;              // appended row
+      const int d_lo = vb, d_hi = vb + ld.n_draft;           // drafts
+      const long long t_lo = row0, t_hi = row0 + rows_in_tile;
+      const bool has_app = ld.n_app && a_row >= t_lo && a_row < t_hi;
+      const int pd_lo = (int)max((long long)d_lo, t_lo), pd_hi = (int)min((long long)d_hi, t_hi);
+      const int npd = ld.n_draft ? max(0, pd_hi - pd_lo) : 0;
+      if (has_app || npd > 0) {
+        consumer_sync();                       // every warp has seen the TMA bytes land
+        const int nrows = (has_app ? 1 : 0) + npd;
+        constexpr int CHR = C::ROWB / 16;      // 16-byte chunks per row
+        for (int x = tid; x < nrows * 2 * CHR; x += kThreads) {
+          const int ck = x % CHR;
+          const int tensor = (x / CHR) & 1;
+          const int ri = x / (2 * CHR);
+          int row;
+          const uint8_t* src;
+          if (has_app && ri == 0) {
+            row = a_row;
+            src = (tensor ? ld.Vnew : ld.Knew) + (size_t)cc.u * C::ROWB;
+          } else {
+            const int di = pd_lo - d_lo + ri - (has_app ? 1 : 0);
+            row = d_lo + di;
+            src = (tensor ? ld.Vd : ld.Kd) + ((size_t)cc.u * ld.kd_stride + di) * C::ROWB;
+          }
+          const uint4 v = *reinterpret_cast<const uint4*>(src + ck * 16);
+          *reinterpret_cast<uint4*>((tensor ? sv : sk) + (size_t)(row - row0) * C::ROWB + ck * 16) = v;
+          uint8_t* dst = const_cast<uint8_t*>(tensor ? ld.V : ld.K) +
+                         ((size_t)cc.u * ld.cap + row) * C::ROWB + ck * 16;
+          *reinterpret_cast<uint4*>(dst) = v;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        consumer_sync();
+      }
+    }
 
     if (row0 < max_vis) {  // tiles with no visible row for any query are only streamed
       // K rows of all passes first (independent loads, then independent FMA chains)
@@ -390,29 +471,25 @@ __global__ void __launch_bounds__(kThreads, CTAS) attn_decode_kernel(const Param
     if (++stage == S) { stage = 0; phase ^= 1; }
 
     // ------------------------------------------------------ segment end
-    const bool seg_last = (i + 1 == t_end) || (j + 1 == tpu);
-    const long long cu = u;
-    const int cb = b, cg = g;
-    if (++j == tpu) {
-      j = 0;
-      ++u;
-      if (++g == p.H_kv) { g = 0; ++b; }
-    }
+    const Cursor cs = cc;     // the unit this tile belongs to
+    const bool seg_last = (i + 1 == t_end) || (cc.j + 1 == ld.tpu);
+    advance(p, cc);
     if (!seg_last) continue;
     seg_start = true;
+    const LayerDesc& sl = p.layer[cs.l];
 
     if (lane == 0) {
 #pragma unroll
       for (int m = 0; m < MAXM; ++m) sm_m[warp * MAXM + m] = mw[m];
     }
     consumer_sync();
-    const long long ufirst = cu * tpu, ulast = ufirst + tpu - 1;
+    const long long ufirst = seg_tile0, ulast = seg_tile0 + sl.tpu - 1;
     const int c_lo = cta_of_tile(ufirst, NT, p.ctas);
     const int c_hi = cta_of_tile(ulast, NT, p.ctas);
     const int nseg = c_hi - c_lo + 1;
-    const size_t obase = ((size_t)((size_t)cb * p.H_q + (size_t)cg * p.G) * p.t + p.m0) * D;
+    const size_t obase = ((size_t)((size_t)cs.b * p.H_q + (size_t)cs.g * p.G) * p.t + p.m0) * D;
     const size_t rec = (size_t)p.M * (D + 2);
-    float* my = p.ws + ((size_t)cta * 2 + (seg_first ? 0 : 1)) * rec;
+    float* my = sl.ws + ((size_t)cta * 2 + (seg_first ? 0 : 1)) * rec;
 #pragma unroll
     for (int m = 0; m < MAXM; ++m) {
       if (m >= p.M) continue;
@@ -463,7 +540,7 @@ __global__ void __launch_bounds__(kThreads, CTAS) attn_decode_kernel(const Param
           lt += sm_l[w * MAXM + m];
         }
         if (nseg == 1) {
-          p.O[obase + (size_t)m * D + tid] = o / lt;
+          sl.O[obase + (size_t)m * D + tid] = o / lt;
         } else {
           my[(size_t)m * D + tid] = o;
           if (tid == 0) {
@@ -479,43 +556,41 @@ __global__ void __launch_bounds__(kThreads, CTAS) attn_decode_kernel(const Param
       __threadfence();
       consumer_sync();
       if (tid == 0) {
-        const int old = atomicAdd(&p.counters[cu], 1);
+        const int old = atomicAdd(&sl.counters[cs.u], 1);
         *sm_flag = (old == nseg - 1);
       }
       consumer_sync();
       if (*sm_flag) {
         __threadfence();
-        // merge the nseg partial records of unit cu (split-K combine)
+        // merge the nseg partial records of this unit (split-K combine)
         for (int idx = tid; idx < p.M * D; idx += kThreads) {
           const int m = idx / D;
           float mu = -INFINITY;
           for (int c = c_lo; c <= c_hi; ++c) {
-            const long long fu = tile_begin(c, NT, p.ctas) / tpu;
-            const float* r = p.ws + ((size_t)c * 2 + (fu == cu ? 0 : 1)) * rec;
+            const float* r = sl.ws + ((size_t)c * 2 + (tile_begin(c, NT, p.ctas) >= ufirst ? 0 : 1)) * rec;
             mu = fmaxf(mu, __ldcg(r + (size_t)p.M * D + m));
           }
           float o = 0.f, l = 0.f;
           for (int c = c_lo; c <= c_hi; ++c) {
-            const long long fu = tile_begin(c, NT, p.ctas) / tpu;
-            const float* r = p.ws + ((size_t)c * 2 + (fu == cu ? 0 : 1)) * rec;
+            const float* r = sl.ws + ((size_t)c * 2 + (tile_begin(c, NT, p.ctas) >= ufirst ? 0 : 1)) * rec;
             const float mk = __ldcg(r + (size_t)p.M * D + m);
             const float w = (mk == -INFINITY) ? 0.f : fast_exp2(mk - mu);
             o += __ldcg(r + idx) * w;
             l += __ldcg(r + (size_t)p.M * D + p.M + m) * w;
           }
-          p.O[obase + idx] = o / l;
+          sl.O[obase + idx] = o / l;
         }
-        if (tid == 0) p.counters[cu] = 0;
+        if (tid == 0) sl.counters[cs.u] = 0;
       }
       consumer_sync();  // the flag and merge buffers are reused by the next segment
     }
   }
 }
 
-template <typename T, int D, int MAXM, int CPL, int CTAS>
-cudaError_t launch_t(const Params& prm_in, int num_sms, cudaStream_t s) {
+template <typename T, int D, int MAXM, int CPL, int CTAS, int MAXL>
+cudaError_t launch_t(const Params<MAXL>& prm_in, int num_sms, cudaStream_t s) {
   using C = Cfg<T, D, MAXM, CPL, CTAS>;
-  auto kern = attn_decode_kernel<T, D, MAXM, CPL, CTAS>;
+  auto kern = attn_step_kernel<T, D, MAXM, CPL, CTAS, MAXL>;
   static int attr_dev = -1;  // per instantiation
   int dev = 0;
   cudaGetDevice(&dev);
@@ -525,7 +600,7 @@ cudaError_t launch_t(const Params& prm_in, int num_sms, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     attr_dev = dev;
   }
-  Params prm = prm_in;
+  Params<MAXL> prm = prm_in;
   int ctas = prm.ctas > 0 ? prm.ctas : num_sms * CTAS;
   if (ctas > prm.total_tiles) ctas = (int)prm.total_tiles;
   prm.ctas = ctas;
@@ -534,62 +609,81 @@ cudaError_t launch_t(const Params& prm_in, int num_sms, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-template <typename T, int D>
-cudaError_t dispatch_m(const Params& prm, int num_sms, cudaStream_t s) {
-  if (prm.M <= 1) return launch_t<T, D, 1, 2, 2>(prm, num_sms, s);
-  if (prm.M <= 2) return launch_t<T, D, 2, 1, 2>(prm, num_sms, s);
-  if (prm.M <= 4) return launch_t<T, D, 4, 1, 1>(prm, num_sms, s);
-  return launch_t<T, D, 8, 1, 1>(prm, num_sms, s);
+template <typename T, int D, int MAXL>
+cudaError_t dispatch_m(const Params<MAXL>& prm, int num_sms, cudaStream_t s) {
+  if (prm.M <= 1) return launch_t<T, D, 1, 2, 2, MAXL>(prm, num_sms, s);
+  if (prm.M <= 2) return launch_t<T, D, 2, 1, 2, MAXL>(prm, num_sms, s);
+  if (prm.M <= 4) return launch_t<T, D, 4, 1, 1, MAXL>(prm, num_sms, s);
+  return launch_t<T, D, 8, 1, 1, MAXL>(prm, num_sms, s);
 }
 
-}  // namespace attn
-
-static int tile_rows(int D, int dtype) {
-  return attn::kStageBytes / (D * (dtype == BMC_BF16 ? 2 : 4));
-}
-
-size_t attn_workspace_floats(int U, int M, int D, int num_sms) {
-  (void)U;
-  const int mc = M < 8 ? M : 8;
-  return (size_t)num_sms * 2 * (size_t)mc * (D + 2);
-}
-
-cudaError_t launch_attn_decode(const AttnArgs& a, int num_sms, cudaStream_t s) {
-  const long long U = (long long)a.B * a.H_kv;
-  const int TR = tile_rows(a.D, a.dtype);
-  const int tpu = (int)((a.cap + TR - 1) / TR);
-  const long long NT = U * tpu;
-  if (NT == 0) return cudaSuccess;
-  attn::Params prm;
-  prm.K = (const uint8_t*)a.K;
-  prm.V = (const uint8_t*)a.V;
-  prm.Q = (const uint8_t*)a.Q;
-  prm.O = a.O;
-  prm.ws = a.ws;
-  prm.counters = a.counters;
-  prm.cap = a.cap;
-  prm.total_tiles = NT;
-  prm.tpu = tpu;
+template <int MAXL>
+cudaError_t launch_chunk(const AttnStepArgs& a, int l0, int nl, int num_sms, cudaStream_t s) {
+  Params<MAXL> prm;
+  const int TR = kStageBytes / (a.D * (a.dtype == BMC_BF16 ? 2 : 4));
+  prm.L = nl;
+  prm.U = a.B * a.H_kv;
   prm.H_kv = a.H_kv;
   prm.H_q = a.H_q;
   prm.G = a.H_q / a.H_kv;
   prm.t = a.t;
-  prm.Mu = prm.G * a.t;
-  prm.ctas = a.ctas;   // 0 = num_sms x CTAs per SM of the chosen variant
-  prm.qscale = attn::kLog2e / sqrtf((float)a.D);
+  prm.ctas = a.ctas;
+  prm.qscale = kLog2e / sqrtf((float)a.D);
   for (int b = 0; b < a.B; ++b) prm.valid[b] = a.valid[b];
+  long long tiles = 0;
+  for (int i = 0; i < nl; ++i) {
+    const AttnLayer& h = a.layers[l0 + i];
+    LayerDesc& d = prm.layer[i];
+    d.K = (const uint8_t*)h.K;
+    d.V = (const uint8_t*)h.V;
+    d.Q = (const uint8_t*)h.Q;
+    d.O = h.O;
+    d.Knew = (const uint8_t*)h.Knew;
+    d.Vnew = (const uint8_t*)h.Vnew;
+    d.Kd = (const uint8_t*)h.Kd;
+    d.Vd = (const uint8_t*)h.Vd;
+    d.ws = h.ws;
+    d.counters = h.counters;
+    d.cap = h.cap;
+    d.tpu = (int)((h.cap + TR - 1) / TR);
+    d.tile0 = tiles;
+    d.n_app = h.n_app;
+    d.n_draft = h.n_draft;
+    d.kd_stride = h.kd_stride;
+    tiles += (long long)prm.U * d.tpu;
+  }
+  prm.total_tiles = tiles;
+  if (tiles == 0) return cudaSuccess;
+  const int Mu = prm.G * a.t;
   // query rows in groups of at most 8 per launch (CUDA-core path)
-  for (int m0 = 0; m0 < prm.Mu; m0 += 8) {
+  for (int m0 = 0; m0 < Mu; m0 += 8) {
     prm.m0 = m0;
-    prm.M = prm.Mu - m0 < 8 ? prm.Mu - m0 : 8;
+    prm.M = Mu - m0 < 8 ? Mu - m0 : 8;
     cudaError_t e;
     if (a.dtype == BMC_BF16) {
-      e = a.D == 128 ? attn::dispatch_m<__nv_bfloat16, 128>(prm, num_sms, s)
-                     : attn::dispatch_m<__nv_bfloat16, 64>(prm, num_sms, s);
+      e = a.D == 128 ? dispatch_m<__nv_bfloat16, 128, MAXL>(prm, num_sms, s)
+                     : dispatch_m<__nv_bfloat16, 64, MAXL>(prm, num_sms, s);
     } else {
-      e = a.D == 128 ? attn::dispatch_m<float, 128>(prm, num_sms, s)
-                     : attn::dispatch_m<float, 64>(prm, num_sms, s);
+      e = a.D == 128 ? dispatch_m<float, 128, MAXL>(prm, num_sms, s)
+                     : dispatch_m<float, 64, MAXL>(prm, num_sms, s);
     }
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace attn
+
+size_t attn_workspace_floats(int M, int D, int max_ctas) {
+  const int mc = M < 8 ? M : 8;
+  return (size_t)max_ctas * 2 * (size_t)mc * (D + 2);
+}
+
+cudaError_t launch_attn_step(const AttnStepArgs& a, int num_sms, cudaStream_t s) {
+  if (a.L == 1) return attn::launch_chunk<1>(a, 0, 1, num_sms, s);
+  for (int l0 = 0; l0 < a.L; l0 += kMaxLayersPerLaunch) {
+    const int nl = a.L - l0 < kMaxLayersPerLaunch ? a.L - l0 : kMaxLayersPerLaunch;
+    cudaError_t e = attn::launch_chunk<kMaxLayersPerLaunch>(a, l0, nl, num_sms, s);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;

@@ -2,12 +2,19 @@
 //
 // The host keeps an exact shadow of every length (valid_b, cap, staged), so
 // no call ever reads anything back from the device on the hot path; all
-// validation happens before anything is enqueued.  Each call turns into at
-// most three stream-ordered kernel launches:
-//   bmc_append     [growth: arena map + realloc_copy_zero]  + write_rows
-//   bmc_spec_write [ITERATIVE growth]                       + write_rows
-//   bmc_sdpa       attn_decode (split-K, in-kernel combine)
-//   bmc_commit     zero_rows (rejected drafts only)
+// validation happens before anything is enqueued.
+//
+// Row writes are deferred: bmc_append / bmc_spec_write only record the
+// caller's row pointers ("pending rows"); the next bmc_sdpa writes them into
+// the cache inside the attention kernel (the kernel that owns the tile holding
+// the row patches its staged copy and stores the row), so a decode step is one
+// launch per layer (one per <=32 layers through bmc_decode_step).  Any other
+// operation that needs the rows in memory first flushes them with the
+// standalone write_rows kernel.  Launches per call:
+//   bmc_append      [growth: arena + realloc_copy_zero]
+//   bmc_spec_write  [ITERATIVE growth]
+//   bmc_sdpa        attn_step (split-K, in-kernel combine, fused row writes)
+//   bmc_commit      zero_rows (rejected drafts only)
 #include <cuda_runtime.h>
 #include <stdarg.h>
 #include <stdio.h>
@@ -43,11 +50,17 @@ struct bmc_ctx {
   int attn_path = 0;
   bmc_stats_t st = {};
   int sticky = 0;
-  // staging of host-pointer arguments
-  void* stage_in = nullptr;
-  size_t stage_in_bytes = 0;
+  // staging of host-pointer arguments: 0 appended rows, 1 drafts, 2 Q
+  void* stage_in[3] = {nullptr, nullptr, nullptr};
+  size_t stage_in_bytes[3] = {0, 0, 0};
   float* stage_out = nullptr;
   size_t stage_out_bytes = 0;
+  // rows recorded by append / spec_write, not yet written to the cache
+  const void* knew = nullptr;
+  const void* vnew = nullptr;
+  const void* kd = nullptr;
+  const void* vd = nullptr;
+  int n_app = 0, n_draft = 0, kd_stride = 0;
 };
 
 static thread_local std::string g_err;
@@ -92,19 +105,19 @@ static int min_valid(const bmc_t h) { return *std::min_element(h->valid.begin(),
 static int ptr_kind(const void* p) { return bmc::pointer_kind(p); }
 static bool is_device_ptr(const void* p) { return ptr_kind(p) == 0; }
 
-static int ensure_stage_in(bmc_t h, size_t bytes) {
-  if (h->stage_in_bytes >= bytes) return 0;
-  if (h->stage_in) cudaFreeAsync(h->stage_in, h->stream);
-  h->stage_in = nullptr;
-  h->stage_in_bytes = 0;
-  CK(h, cudaMallocAsync(&h->stage_in, bytes, h->stream), "stage_in");
-  h->stage_in_bytes = bytes;
+static int ensure_stage_in(bmc_t h, int slot, size_t bytes) {
+  if (h->stage_in_bytes[slot] >= bytes) return 0;
+  if (h->stage_in[slot]) cudaFreeAsync(h->stage_in[slot], h->stream);
+  h->stage_in[slot] = nullptr;
+  h->stage_in_bytes[slot] = 0;
+  CK(h, cudaMallocAsync(&h->stage_in[slot], bytes, h->stream), "stage_in");
+  h->stage_in_bytes[slot] = bytes;
   return 0;
 }
 
 // Map caller inputs (device or host) to device pointers; host inputs are
-// copied into the handle's staging buffer on its stream.
-static int device_inputs(bmc_t h, const void** ptrs, const size_t* bytes, int n,
+// copied into the handle's staging buffer `slot` on its stream.
+static int device_inputs(bmc_t h, int slot, const void** ptrs, const size_t* bytes, int n,
                          const void** dev) {
   size_t need = 0;
   bool any_host = false;
@@ -117,7 +130,7 @@ static int device_inputs(bmc_t h, const void** ptrs, const size_t* bytes, int n,
     }
   }
   if (any_host) {
-    int rc = ensure_stage_in(h, need);
+    int rc = ensure_stage_in(h, slot, need);
     if (rc) return rc;
   }
   size_t off = 0;
@@ -125,7 +138,7 @@ static int device_inputs(bmc_t h, const void** ptrs, const size_t* bytes, int n,
     if (dev_ptr[i]) {
       dev[i] = ptrs[i];
     } else {
-      void* d = (char*)h->stage_in + off;
+      void* d = (char*)h->stage_in[slot] + off;
       CK(h, cudaMemcpyAsync(d, ptrs[i], bytes[i], cudaMemcpyHostToDevice, h->stream), "H2D");
       dev[i] = d;
       off += (bytes[i] + 255) / 256 * 256;
@@ -172,7 +185,7 @@ static int reallocate(bmc_t h, long long new_cap, long long copy_rows) {
   return 0;
 }
 
-static int write_rows(bmc_t h, const void* K, const void* V, int nsrc, int nwrite) {
+static int write_rows(bmc_t h, const void* K, const void* V, int nsrc, int nwrite, int row_shift) {
   bmc::RowsArgs a;
   a.src_k = K;
   a.src_v = V;
@@ -184,10 +197,52 @@ static int write_rows(bmc_t h, const void* K, const void* V, int nsrc, int nwrit
   a.nwrite = nwrite;
   a.cap = h->cap;
   a.row_bytes = h->row_bytes;
-  for (int b = 0; b < h->B; ++b) a.row0[b] = h->valid[b];
+  for (int b = 0; b < h->B; ++b) a.row0[b] = h->valid[b] + row_shift;
   CK(h, bmc::launch_write_rows(a, h->stream), "write_rows");
-  h->st.append_written_bytes += 2LL * h->U * nwrite * h->row_bytes;
   return 0;
+}
+
+// Write recorded rows that no attention launch has consumed yet.
+static int flush_pending(bmc_t h) {
+  int rc = 0;
+  if (h->n_app) rc = write_rows(h, h->knew, h->vnew, 1, 1, -1);   // row valid_b - 1
+  if (!rc && h->n_draft) rc = write_rows(h, h->kd, h->vd, h->kd_stride, h->n_draft, 0);
+  h->n_app = h->n_draft = 0;
+  return rc;
+}
+
+static void fill_layer(bmc_t h, const void* Q, float* O, bmc::AttnLayer* l) {
+  l->K = h->kbuf.ptr;
+  l->V = h->vbuf.ptr;
+  l->Q = Q;
+  l->O = O;
+  l->Knew = h->knew;
+  l->Vnew = h->vnew;
+  l->Kd = h->kd;
+  l->Vd = h->vd;
+  l->ws = h->ws;
+  l->counters = h->counters;
+  l->cap = h->cap;
+  l->n_app = h->n_app;
+  l->n_draft = h->n_draft;
+  l->kd_stride = h->kd_stride;
+}
+
+static void fill_args(bmc_t h, int t, bmc::AttnStepArgs* a) {
+  a->B = h->B;
+  a->H_kv = h->H_kv;
+  a->H_q = h->H_q;
+  a->D = h->D;
+  a->t = t;
+  a->dtype = h->dt;
+  a->ctas = std::min(h->attn_ctas, h->max_ctas);
+  for (int b = 0; b < h->B; ++b) a->valid[b] = h->valid[b];
+}
+
+static void account_sdpa(bmc_t h, int t) {
+  h->st.sdpa_calls += 1;
+  h->st.kv_bytes_read += 2LL * h->U * h->cap * h->row_bytes;
+  h->st.macs += 2LL * h->B * h->H_q * t * h->cap * (long long)h->D;
 }
 
 extern "C" {
@@ -227,7 +282,7 @@ int bmc_create_ex(int B, int H_kv, int H_q, int D, int r, int N_max, bmc_dtype d
   h->max_ctas = 4 * h->num_sms;
   int err = 0;
   h->arena = bmc::arena_create(device, (size_t)h->U * N_max * h->row_bytes, &err);
-  const size_t wsf = bmc::attn_workspace_floats((int)h->U, 8, D, h->max_ctas);
+  const size_t wsf = bmc::attn_workspace_floats(8, D, h->max_ctas);
   // stream-ordered: creating a handle never synchronises the device
   cudaError_t e = cudaMallocAsync((void**)&h->ws, wsf * sizeof(float), h->stream);
   if (e == cudaSuccess) e = cudaMallocAsync((void**)&h->counters, (size_t)h->U * sizeof(int), h->stream);
@@ -254,29 +309,39 @@ int bmc_create(int B, int H_kv, int H_q, int D, int r, int N_max, bmc_t* out) {
   return bmc_create_ex(B, H_kv, H_q, D, r, N_max, BMC_BF16, BMC_POLICY_BMC, -1, nullptr, out);
 }
 
-int bmc_append(bmc_t h, const void* K, const void* V) {
-  int rc = enter(h);
+// Append = growth if needed + record the row (written by the next SDPA).
+static int append_impl(bmc_t h, const void* K, const void* V) {
+  int rc = 0;
+  if (h->n_app || h->n_draft) rc = flush_pending(h);
   if (rc) return rc;
-  if (!K || !V) return fail(BMC_ERR_ARG, "K or V is null");
-  if (h->staged > 0) return fail(BMC_ERR_STATE, "append while %d drafts are staged", h->staged);
   const int mv = max_valid(h);
-  if (mv >= h->N_max) return fail(BMC_ERR_CAPACITY, "cache full (N_max=%d)", h->N_max);
-  const size_t in_bytes = (size_t)h->U * h->row_bytes;
-  const void* ptrs[2] = {K, V};
-  const size_t sizes[2] = {in_bytes, in_bytes};
-  const void* dev[2];
   if (h->pol == BMC_POLICY_ITERATIVE) {
     rc = reallocate(h, mv + 1, mv);                      // Fig. AttnBlkListing concat
   } else if (h->pol == BMC_POLICY_BMC && mv == h->cap) {
     rc = reallocate(h, std::min<long long>(h->cap + h->r, h->N_max), h->cap);
   }
   if (rc) return rc;
-  rc = device_inputs(h, ptrs, sizes, 2, dev);
+  const size_t in_bytes = (size_t)h->U * h->row_bytes;
+  const void* ptrs[2] = {K, V};
+  const size_t sizes[2] = {in_bytes, in_bytes};
+  const void* dev[2];
+  rc = device_inputs(h, 0, ptrs, sizes, 2, dev);
   if (rc) return rc;
-  rc = write_rows(h, dev[0], dev[1], 1, 1);
-  if (rc) return rc;
+  h->knew = dev[0];
+  h->vnew = dev[1];
+  h->n_app = 1;
+  h->st.append_written_bytes += 2LL * h->U * h->row_bytes;
   for (auto& v : h->valid) v += 1;
   return 0;
+}
+
+int bmc_append(bmc_t h, const void* K, const void* V) {
+  int rc = enter(h);
+  if (rc) return rc;
+  if (!K || !V) return fail(BMC_ERR_ARG, "K or V is null");
+  if (h->staged > 0) return fail(BMC_ERR_STATE, "append while %d drafts are staged", h->staged);
+  if (max_valid(h) >= h->N_max) return fail(BMC_ERR_CAPACITY, "cache full (N_max=%d)", h->N_max);
+  return append_impl(h, K, V);
 }
 
 int bmc_spec_write(bmc_t h, const void* K_draft, const void* V_draft, int k) {
@@ -291,7 +356,8 @@ int bmc_spec_write(bmc_t h, const void* K_draft, const void* V_draft, int k) {
   if (h->pol == BMC_POLICY_ITERATIVE) {
     k_adm = std::min(k, h->N_max - mv);
     if (k_adm > 0) {
-      rc = reallocate(h, (long long)mv + k_adm, mv);
+      if (h->n_app) rc = flush_pending(h);                // the copy must see every row
+      if (!rc) rc = reallocate(h, (long long)mv + k_adm, mv);
       if (rc) return rc;
     }
   } else {
@@ -302,10 +368,13 @@ int bmc_spec_write(bmc_t h, const void* K_draft, const void* V_draft, int k) {
     const void* ptrs[2] = {K_draft, V_draft};
     const size_t sizes[2] = {in_bytes, in_bytes};
     const void* dev[2];
-    rc = device_inputs(h, ptrs, sizes, 2, dev);
+    rc = device_inputs(h, 1, ptrs, sizes, 2, dev);
     if (rc) return rc;
-    rc = write_rows(h, dev[0], dev[1], k, k_adm);
-    if (rc) return rc;
+    h->kd = dev[0];
+    h->vd = dev[1];
+    h->n_draft = k_adm;
+    h->kd_stride = k;
+    h->st.append_written_bytes += 2LL * h->U * k_adm * h->row_bytes;
   }
   h->staged = k_adm;
   return k_adm;
@@ -326,7 +395,7 @@ int bmc_sdpa(bmc_t h, const void* Q, int n_valid, float* O) {
   const size_t q_bytes = (size_t)h->B * h->H_q * t * h->row_bytes;
   const size_t o_bytes = (size_t)h->B * h->H_q * t * h->D * sizeof(float);
   const void* qd = nullptr;
-  rc = device_inputs(h, &Q, &q_bytes, 1, &qd);
+  rc = device_inputs(h, 2, &Q, &q_bytes, 1, &qd);
   if (rc) return rc;
   const int out_kind = ptr_kind(O);
   const bool host_out = out_kind != 0;
@@ -341,26 +410,15 @@ int bmc_sdpa(bmc_t h, const void* Q, int n_valid, float* O) {
     }
     od = h->stage_out;
   }
-  bmc::AttnArgs a;
-  a.K = h->kbuf.ptr;
-  a.V = h->vbuf.ptr;
-  a.Q = qd;
-  a.O = od;
-  a.ws = h->ws;
-  a.counters = h->counters;
-  a.B = h->B;
-  a.H_kv = h->H_kv;
-  a.H_q = h->H_q;
-  a.D = h->D;
-  a.t = t;
-  a.cap = h->cap;
-  a.dtype = h->dt;
-  a.ctas = std::min(h->attn_ctas, h->max_ctas);
-  for (int b = 0; b < h->B; ++b) a.valid[b] = h->valid[b];
-  CK(h, bmc::launch_attn_decode(a, h->num_sms, h->stream), "attn_decode");
-  h->st.sdpa_calls += 1;
-  h->st.kv_bytes_read += 2LL * h->U * h->cap * h->row_bytes;
-  h->st.macs += 2LL * h->B * h->H_q * t * h->cap * (long long)h->D;
+  bmc::AttnLayer layer;
+  fill_layer(h, qd, od, &layer);
+  bmc::AttnStepArgs a;
+  fill_args(h, t, &a);
+  a.L = 1;
+  a.layers = &layer;
+  CK(h, bmc::launch_attn_step(a, h->num_sms, h->stream), "attn_step");
+  h->n_app = h->n_draft = 0;
+  account_sdpa(h, t);
   if (host_out) {
     CK(h, cudaMemcpyAsync(O, od, o_bytes, cudaMemcpyDeviceToHost, h->stream), "D2H");
     if (out_kind == 2) CK(h, cudaStreamSynchronize(h->stream), "sync");
@@ -386,16 +444,48 @@ int bmc_decode_step(const bmc_t* hs, int L, const void* const* K, const void* co
           return fail(BMC_ERR_STATE, "layer %d: n_valid=%d but row %d will hold %d", l, n_valid,
                       b, h->valid[b] + 1);
   }
+  // one launch for all layers when they share shape, dtype, stream and lengths
+  bool fused = true;
+  for (int l = 1; l < L; ++l) {
+    const bmc_t a = hs[0], b = hs[l];
+    if (a->B != b->B || a->H_kv != b->H_kv || a->H_q != b->H_q || a->D != b->D ||
+        a->dt != b->dt || a->stream != b->stream || a->device != b->device || a->valid != b->valid)
+      fused = false;
+  }
+  for (int l = 0; l < L; ++l)
+    if (ptr_kind(Q[l]) != 0 || ptr_kind(O[l]) != 0) fused = false;
+  if (!fused) {
+    for (int l = 0; l < L; ++l) {
+      int rc = bmc_append(hs[l], K[l], V[l]);
+      if (rc) return rc;
+      rc = bmc_sdpa(hs[l], Q[l], n_valid, O[l]);
+      if (rc) return rc;
+    }
+    return 0;
+  }
+  std::vector<bmc::AttnLayer> layers(L);
   for (int l = 0; l < L; ++l) {
-    int rc = bmc_append(hs[l], K[l], V[l]);
+    int rc = append_impl(hs[l], K[l], V[l]);
     if (rc) return rc;
-    rc = bmc_sdpa(hs[l], Q[l], n_valid, O[l]);
-    if (rc) return rc;
+    fill_layer(hs[l], Q[l], O[l], &layers[l]);
+  }
+  bmc::AttnStepArgs a;
+  fill_args(hs[0], 1, &a);
+  a.L = L;
+  a.layers = layers.data();
+  CK(hs[0], bmc::launch_attn_step(a, hs[0]->num_sms, hs[0]->stream), "attn_step");
+  for (int l = 0; l < L; ++l) {
+    hs[l]->n_app = hs[l]->n_draft = 0;
+    account_sdpa(hs[l], 1);
   }
   return 0;
 }
 
 static int commit_impl(bmc_t h, const int* m) {
+  if (h->n_app || h->n_draft) {
+    int rc = flush_pending(h);
+    if (rc) return rc;
+  }
   bmc::ZeroArgs z;
   z.k = h->kbuf.ptr;
   z.v = h->vbuf.ptr;
@@ -441,10 +531,12 @@ int bmc_commit_rows(bmc_t h, const int* n_accepted_host) {
 int bmc_destroy(bmc_t h) {
   if (!h) return fail(BMC_ERR_ARG, "null handle");
   cudaSetDevice(h->device);
+  if (!h->sticky && (h->n_app || h->n_draft)) flush_pending(h);
   cudaStreamSynchronize(h->stream);
   bmc::arena_release(h->arena, &h->kbuf, h->stream);
   bmc::arena_release(h->arena, &h->vbuf, h->stream);
-  if (h->stage_in) cudaFreeAsync(h->stage_in, h->stream);
+  for (int i = 0; i < 3; ++i)
+    if (h->stage_in[i]) cudaFreeAsync(h->stage_in[i], h->stream);
   if (h->stage_out) cudaFreeAsync(h->stage_out, h->stream);
   if (h->ws) cudaFreeAsync(h->ws, h->stream);
   if (h->counters) cudaFreeAsync(h->counters, h->stream);
@@ -466,7 +558,12 @@ int bmc_stats(bmc_t h, bmc_stats_t* out) {
 }
 
 int bmc_kv_view(bmc_t h, void** K, void** V, int* cap) {
-  if (!h) return fail(BMC_ERR_ARG, "null handle");
+  int rc = enter(h);
+  if (rc) return rc;
+  if (h->n_app || h->n_draft) {
+    rc = flush_pending(h);
+    if (rc) return rc;
+  }
   if (K) *K = h->kbuf.ptr;
   if (V) *V = h->vbuf.ptr;
   if (cap) *cap = (int)h->cap;
@@ -477,6 +574,10 @@ int bmc_read_cache(bmc_t h, void* K_dst, void* V_dst) {
   int rc = enter(h);
   if (rc) return rc;
   if (!K_dst || !V_dst) return fail(BMC_ERR_ARG, "null destination");
+  if (h->n_app || h->n_draft) {
+    rc = flush_pending(h);
+    if (rc) return rc;
+  }
   const size_t bytes = (size_t)h->U * h->cap * h->row_bytes;
   if (bytes == 0) return 0;
   CK(h, cudaMemcpyAsync(K_dst, h->kbuf.ptr, bytes, cudaMemcpyDefault, h->stream), "read K");
@@ -495,6 +596,10 @@ int bmc_valid(bmc_t h, int* valid_host) {
 int bmc_sync(bmc_t h) {
   int rc = enter(h);
   if (rc) return rc;
+  if (h->n_app || h->n_draft) {
+    rc = flush_pending(h);
+    if (rc) return rc;
+  }
   CK(h, cudaStreamSynchronize(h->stream), "sync");
   return 0;
 }

@@ -43,21 +43,30 @@ struct ZeroArgs {
 };
 cudaError_t launch_zero_rows(const ZeroArgs& a, cudaStream_t s);
 
-struct AttnArgs {
-  const void* K; const void* V;           // [U][cap][D]
+// One layer of an attention launch.
+struct AttnLayer {
+  const void* K; const void* V;           // cache [U][cap][D]
   const void* Q;                          // [B][H_q][t][D]
   float* O;                               // [B][H_q][t][D]
+  const void* Knew; const void* Vnew;     // pending appended row [B][H_kv][D] (n_app = 1)
+  const void* Kd; const void* Vd;         // pending drafts [B][H_kv][kd_stride][D]
   float* ws;                              // partial records
   int* counters;                          // [U], zero between launches
-  int B, H_kv, H_q, D, t;
   long long cap;
-  int dtype;                              // BMC_F32 / BMC_BF16
-  int ctas;                               // 0 = auto
-  int valid[BMC_MAX_B];
+  int n_app, n_draft, kd_stride;
 };
-// Workspace floats / counter ints the attention needs for (U, M, D).
-size_t attn_workspace_floats(int U, int M, int D, int num_sms);
-cudaError_t launch_attn_decode(const AttnArgs& a, int num_sms, cudaStream_t s);
+constexpr int kMaxLayersPerLaunch = 32;
+struct AttnStepArgs {
+  int B, H_kv, H_q, D, t, dtype;
+  int ctas;                               // 0 = auto
+  int valid[BMC_MAX_B];                   // committed rows incl. the pending append
+  int L;
+  const AttnLayer* layers;
+};
+size_t attn_workspace_floats(int M, int D, int max_ctas);
+// Masked SDPA of L layers in one persistent launch (per 32 layers), with the
+// pending appended / drafted rows written into each cache on the way.
+cudaError_t launch_attn_step(const AttnStepArgs& a, int num_sms, cudaStream_t s);
 
 void count_launch();
 unsigned long long launch_count();
