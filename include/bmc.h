@@ -21,7 +21,11 @@
  *     never synchronise the device.  The host tracks every length itself
  *     (no device->host reads on the hot path).
  *   - The caller owns K, V, K_draft, V_draft, Q, O and must keep device
- *     buffers alive until the stream has passed the call.  The library owns
+ *     buffers alive until the stream has passed the call.  Rows given to
+ *     bmc_append / bmc_spec_write are written into the cache by the NEXT
+ *     call on the handle that touches it (normally bmc_sdpa, which fuses the
+ *     write into the attention kernel): their device buffers must stay alive
+ *     and unmodified until the stream has passed that call.  The library owns
  *     the cache memory (per-handle arena) and its workspace.
  *   - Single writer per handle.  Distinct handles are independent.
  *   - Inputs are stored bit-for-bit (no dtype conversion in append/spec);

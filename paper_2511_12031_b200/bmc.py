@@ -223,11 +223,20 @@ class KVCache:
                                self.device, self.stream.cuda_stream)
         self.torch_dtype = _TORCH_DT[self.dtype]
 
+    # Rows passed to append / spec_write are read by the next call that
+    # touches the cache (include/bmc.h): keep them referenced until then so the
+    # torch caching allocator cannot hand their memory to another tensor first.
+    _keep = ()
+
     def append(self, K, V):
-        return bmc_append(self.h, K, V)
+        rc = bmc_append(self.h, K, V)
+        self._keep = (K, V)
+        return rc
 
     def spec_write(self, Kd, Vd, k):
-        return bmc_spec_write(self.h, Kd, Vd, k)
+        rc = bmc_spec_write(self.h, Kd, Vd, k)
+        self._keep = self._keep + (Kd, Vd)
+        return rc
 
     def sdpa(self, Q, n_valid, O=None):
         if O is None:
@@ -235,13 +244,18 @@ class KVCache:
             O = torch.empty(self.B, self.H_q, t, self.D, dtype=torch.float32,
                             device=Q.device if isinstance(Q, torch.Tensor) else "cuda")
         bmc_sdpa(self.h, Q, n_valid, O)
+        self._keep = ()
         return O
 
     def commit(self, n):
-        return bmc_commit(self.h, n)
+        rc = bmc_commit(self.h, n)
+        self._keep = ()
+        return rc
 
     def commit_rows(self, n):
-        return bmc_commit_rows(self.h, n)
+        rc = bmc_commit_rows(self.h, n)
+        self._keep = ()
+        return rc
 
     def stats(self):
         return bmc_stats(self.h)
@@ -259,10 +273,13 @@ class KVCache:
                         device=f"cuda:{self.device}")
         V = torch.empty_like(K)
         bmc_read_cache(self.h, K, V)
+        self._keep = ()
         return K, V
 
     def sync(self):
-        return bmc_sync(self.h)
+        rc = bmc_sync(self.h)
+        self._keep = ()
+        return rc
 
     def close(self):
         if getattr(self, "h", None) is not None:
