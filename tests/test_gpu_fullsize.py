@@ -1,0 +1,201 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py
+times (bmc_decode_step: all layers of a step in one persistent launch).
+
+Inputs are seeded N(0,1) draws (torch generator on the device for speed,
+RNE-rounded to bf16); the oracle receives the same rounded bits of the
+sampled units.  Checked: SDPA outputs of sampled (batch, kv-head) units at
+sampled steps against per-unit oracles (element by element, max-abs 2e-3),
+the whole cache against the appended rows (bit-exact, zero padding), and the
+allocation / copy ledger against the paper's closed forms.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+import oracle as O  # noqa: E402
+from harness import TOL_BF16  # noqa: E402
+from paper_2511_12031_b200 import bmc, synth  # noqa: E402
+
+
+@pytest.fixture(autouse=True, scope="module")
+def _built():
+    import __graft_entry__
+    __graft_entry__.build()
+
+
+def _bits(x: torch.Tensor) -> torch.Tensor:
+    return x.view(torch.int16)
+
+
+def _run_decode_fullsize(B, H_kv, H_q, D, N, r, L, sample_steps, sample_units, seed):
+    dev = torch.device("cuda")
+    caches = [bmc.KVCache(B, H_kv, H_q, D, r, N, dtype="bf16") for _ in range(L)]
+    plan = bmc.StepPlan(caches)
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+    U = B * H_kv
+    G = H_q // H_kv
+    Kall = [torch.empty(N, B, H_kv, D, dtype=torch.bfloat16, device=dev) for _ in range(L)]
+    Vall = [torch.empty_like(Kall[0]) for _ in range(L)]
+    outs = [torch.empty(B, H_q, 1, D, device=dev) for _ in range(L)]
+    Optr = plan.ptrs(outs)
+    saved = {}
+    for n in range(1, N + 1):
+        ks, vs, qs = [], [], []
+        for l in range(L):
+            Kall[l][n - 1] = torch.randn(B, H_kv, D, generator=g, device=dev).to(torch.bfloat16)
+            Vall[l][n - 1] = torch.randn(B, H_kv, D, generator=g, device=dev).to(torch.bfloat16)
+            qs.append(torch.randn(B, H_q, 1, D, generator=g, device=dev).to(torch.bfloat16))
+            ks.append(Kall[l][n - 1])
+            vs.append(Vall[l][n - 1])
+        bmc.bmc_decode_step(plan, plan.ptrs(ks), plan.ptrs(vs), plan.ptrs(qs), Optr, n)
+        if n in sample_steps:
+            for l in range(L):
+                saved[(n, l)] = (qs[l].clone(), outs[l].clone())
+    torch.cuda.synchronize()
+    return caches, Kall, Vall, saved
+
+
+@pytest.mark.parametrize("cfg", [
+    # BASELINE configs[1]: Llama-2-7B shape, B=16, context 4096, r = 64 (bench default)
+    dict(B=16, H_kv=32, H_q=32, D=128, N=4096, r=64, L=2),
+    # BASELINE configs[3] per GPU: Llama-3-8B GQA (32 q / 8 kv heads), B=64, context 8192
+    dict(B=64, H_kv=8, H_q=32, D=128, N=8192, r=128, L=1),
+])
+def test_fullsize_decode(cfg):
+    B, H_kv, H_q, D, N, r, L = (cfg[k] for k in ("B", "H_kv", "H_q", "D", "N", "r", "L"))
+    steps = sorted({1, r - 1, r, r + 1, 1000, N // 2, N - 1, N})
+    units = [(0, 0), (B - 1, H_kv - 1), (B // 2, H_kv // 3), (3 % B, (5 * H_kv) // 7)]
+    caches, Kall, Vall, saved = _run_decode_fullsize(B, H_kv, H_q, D, N, r, L, set(steps),
+                                                     units, seed=2511)
+    G = H_q // H_kv
+    U = B * H_kv
+    # 1) cache contents: committed rows == appended rows (bit-exact), no padding at N
+    for l in range(L):
+        Kc, Vc = caches[l].kv()
+        assert Kc.shape == (U, N, D)
+        expK = Kall[l].permute(1, 2, 0, 3).reshape(U, N, D)
+        expV = Vall[l].permute(1, 2, 0, 3).reshape(U, N, D)
+        assert torch.equal(_bits(Kc), _bits(expK)) and torch.equal(_bits(Vc), _bits(expV))
+    # 2) ledger against the closed forms (P:L609-611 T = N/r, one copy per growth)
+    s = caches[0].stats()
+    T = math.ceil(N / r)
+    assert s["alloc_events"] == T and s["copy_events"] == T - 1
+    assert s["copied_bytes"] == 2 * U * D * 2 * r * (T - 1) * T // 2
+    assert s["macs"] == sum(2 * B * H_q * min(r * math.ceil(n / r), N) * D
+                            for n in range(1, N + 1))
+    # 3) SDPA outputs of sampled units vs per-unit oracles
+    worst = 0.0
+    for l in range(L):
+        Kl = Kall[l].cpu()
+        Vl = Vall[l].cpu()
+        for (b, g) in units:
+            orc = O.Oracle(1, 1, G, D, r, N, dtype=O.BF16, policy=O.POLICY_BMC)
+            for n in range(1, N + 1):
+                orc.append(Kl[n - 1, b, g].reshape(1, 1, D).contiguous(),
+                           Vl[n - 1, b, g].reshape(1, 1, D).contiguous())
+                if n in saved and (n, l) in saved:
+                    q, o = saved[(n, l)]
+                    qu = q[b, g * G:(g + 1) * G].cpu().reshape(1, G, 1, D).contiguous()
+                    ref = orc.sdpa(qu, n)
+                    got = o[b, g * G:(g + 1) * G].cpu().numpy().reshape(ref.shape)
+                    worst = max(worst, float(np.abs(got - ref).max()))
+            orc.close()
+    assert worst <= TOL_BF16, worst
+    for c in caches:
+        c.close()
+
+
+def test_fullsize_speculative_7b():
+    """BASELINE configs[2]: 7B shape, B=32, k=4 chain drafts in the padded
+    rows, per-row acceptance (Bernoulli 0.7 leading successes), one layer to
+    N=4096; sampled units checked against per-unit oracles replaying the same
+    row sequence."""
+    B, H, D, N, r, k = 32, 32, 128, 4096, 64, 4
+    dev = torch.device("cuda")
+    c = bmc.KVCache(B, H, H, D, r, N, dtype="bf16")
+    g = torch.Generator(device=dev)
+    g.manual_seed(7)
+    units = [(0, 0), (31, 31), (17, 5)]
+    hist = {u: [] for u in units}          # per unit: list of ("app"|"spec"|"sdpa"|"commit", data)
+    it = 0
+    worst = 0.0
+    checks = 0
+    while max(c.valid()) < N - 1:
+        kn = torch.randn(B, H, D, generator=g, device=dev).to(torch.bfloat16)
+        vn = torch.randn(B, H, D, generator=g, device=dev).to(torch.bfloat16)
+        c.append(kn, vn)
+        kk = min(k, N - max(c.valid()))
+        kd = torch.randn(B, H, k, D, generator=g, device=dev).to(torch.bfloat16)
+        vd = torch.randn(B, H, k, D, generator=g, device=dev).to(torch.bfloat16)
+        k_adm = c.spec_write(kd, vd, kk) if kk > 0 else 0
+        t = 1 + k_adm
+        q = torch.randn(B, H, t, D, generator=g, device=dev).to(torch.bfloat16)
+        o = c.sdpa(q, -1)
+        m = synth.acceptance(11, it, B, k_adm)
+        sample = it % 97 == 0 or max(c.valid()) > N - 12
+        for (b, h) in units:
+            hist[(b, h)].append((kn[b, h].cpu(), vn[b, h].cpu(), kd[b, h, :k_adm].cpu(),
+                                 vd[b, h, :k_adm].cpu(), q[b, h].cpu() if sample else None,
+                                 o[b, h].cpu().numpy() if sample else None, m[b]))
+        c.commit_rows(m)
+        it += 1
+    for (b, h), ops in hist.items():
+        orc = O.Oracle(1, 1, 1, D, r, N, dtype=O.BF16, policy=O.POLICY_BMC)
+        for (kn, vn, kd, vd, q, o, mb) in ops:
+            orc.append(kn.reshape(1, 1, D), vn.reshape(1, 1, D))
+            ka = kd.shape[0]
+            if ka:
+                assert orc.spec_write(kd.reshape(1, 1, ka, D).contiguous(),
+                                      vd.reshape(1, 1, ka, D).contiguous(), ka) == ka
+            if q is not None:
+                ref = orc.sdpa(q.reshape(1, 1, 1 + ka, D).contiguous(), -1)
+                worst = max(worst, float(np.abs(o.reshape(ref.shape) - ref).max()))
+                checks += 1
+            if ka:
+                orc.commit(min(mb, ka))
+        orc.close()
+    assert checks > 10 and worst <= TOL_BF16, (checks, worst)
+    s = c.stats()
+    assert s["alloc_events"] == math.ceil(s["valid_max"] / r) or s["capacity"] == N
+    c.close()
+
+
+def test_decode_step_matches_per_layer_calls():
+    """bmc_decode_step (fused multi-layer launch, >32 layers -> 2 launches)
+    matches per-layer append + sdpa calls: caches and ledgers bit-identical,
+    outputs equal up to the split-K summation order (the CTA partition of the
+    tile stream differs)."""
+    B, H_kv, H_q, D, N, r, L = 2, 2, 8, 128, 200, 24, 40
+    dev = torch.device("cuda")
+    a = [bmc.KVCache(B, H_kv, H_q, D, r, N, dtype="bf16") for _ in range(L)]
+    b = [bmc.KVCache(B, H_kv, H_q, D, r, N, dtype="bf16") for _ in range(L)]
+    plan = bmc.StepPlan(a)
+    g = torch.Generator(device=dev)
+    g.manual_seed(3)
+    oa = [torch.empty(B, H_q, 1, D, device=dev) for _ in range(L)]
+    ob = [torch.empty(B, H_q, 1, D, device=dev) for _ in range(L)]
+    for n in range(1, N + 1):
+        ks = [torch.randn(B, H_kv, D, generator=g, device=dev).to(torch.bfloat16) for _ in range(L)]
+        vs = [torch.randn(B, H_kv, D, generator=g, device=dev).to(torch.bfloat16) for _ in range(L)]
+        qs = [torch.randn(B, H_q, 1, D, generator=g, device=dev).to(torch.bfloat16)
+              for _ in range(L)]
+        bmc.bmc_decode_step(plan, plan.ptrs(ks), plan.ptrs(vs), plan.ptrs(qs), plan.ptrs(oa), n)
+        for l in range(L):
+            b[l].append(ks[l], vs[l])
+            b[l].sdpa(qs[l], n, ob[l])
+        torch.cuda.synchronize()   # keep ks/vs alive until consumed
+        if n % 37 == 0 or n == N:
+            for l in range(L):
+                torch.testing.assert_close(oa[l], ob[l], rtol=0, atol=2e-6)
+    for l in range(L):
+        ka, va = a[l].kv()
+        kb, vb = b[l].kv()
+        assert torch.equal(_bits(ka), _bits(kb)) and torch.equal(_bits(va), _bits(vb))
+        assert a[l].stats() == b[l].stats()
+    for x in a + b:
+        x.close()
