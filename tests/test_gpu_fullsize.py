@@ -145,7 +145,11 @@ def test_fullsize_speculative_7b():
         c.commit_rows(m)
         it += 1
     for (b, h), ops in hist.items():
-        orc = O.Oracle(1, 1, 1, D, r, N, dtype=O.BF16, policy=O.POLICY_BMC)
+        # One unit alone cannot reproduce the batch's shared growth schedule
+        # (admission uses max_b valid_b), so it is replayed with the GPU's
+        # admitted counts in an UPFRONT oracle: SDPA is independent of the
+        # padding (mask invariance, tests/test_oracle_pins.py).
+        orc = O.Oracle(1, 1, 1, D, r, N, dtype=O.BF16, policy=O.POLICY_UPFRONT)
         for (kn, vn, kd, vd, q, o, mb) in ops:
             orc.append(kn.reshape(1, 1, D), vn.reshape(1, 1, D))
             ka = kd.shape[0]
