@@ -35,6 +35,7 @@
 #include <stdint.h>
 
 #include "bmc_internal.h"
+#include "combine.cuh"
 
 namespace bmc {
 namespace attn {
@@ -488,7 +489,7 @@ __global__ void __launch_bounds__(kThreads, CTAS) attn_step_kernel(const __grid_
     const int c_hi = cta_of_tile(ulast, NT, p.ctas);
     const int nseg = c_hi - c_lo + 1;
     const size_t obase = ((size_t)((size_t)cs.b * p.H_q + (size_t)cs.g * p.G) * p.t + p.m0) * D;
-    const size_t rec = (size_t)p.M * (D + 2);
+    const size_t rec = rec_floats(p.M, D);
     float* my = sl.ws + ((size_t)cta * 2 + (seg_first ? 0 : 1)) * rec;
 #pragma unroll
     for (int m = 0; m < MAXM; ++m) {
@@ -563,23 +564,8 @@ __global__ void __launch_bounds__(kThreads, CTAS) attn_step_kernel(const __grid_
       if (*sm_flag) {
         __threadfence();
         // merge the nseg partial records of this unit (split-K combine)
-        for (int idx = tid; idx < p.M * D; idx += kThreads) {
-          const int m = idx / D;
-          float mu = -INFINITY;
-          for (int c = c_lo; c <= c_hi; ++c) {
-            const float* r = sl.ws + ((size_t)c * 2 + (tile_begin(c, NT, p.ctas) >= ufirst ? 0 : 1)) * rec;
-            mu = fmaxf(mu, __ldcg(r + (size_t)p.M * D + m));
-          }
-          float o = 0.f, l = 0.f;
-          for (int c = c_lo; c <= c_hi; ++c) {
-            const float* r = sl.ws + ((size_t)c * 2 + (tile_begin(c, NT, p.ctas) >= ufirst ? 0 : 1)) * rec;
-            const float mk = __ldcg(r + (size_t)p.M * D + m);
-            const float w = (mk == -INFINITY) ? 0.f : fast_exp2(mk - mu);
-            o += __ldcg(r + idx) * w;
-            l += __ldcg(r + (size_t)p.M * D + p.M + m) * w;
-          }
-          sl.O[obase + idx] = o / l;
-        }
+        combine_unit<2>(sl.ws, rec, c_lo, c_hi, ufirst, NT, p.ctas, p.M, D, sl.O + obase, sm_o,
+                     tid, kThreads, [] { consumer_sync(); });
         if (tid == 0) sl.counters[cs.u] = 0;
       }
       consumer_sync();  // the flag and merge buffers are reused by the next segment
@@ -675,8 +661,7 @@ cudaError_t launch_chunk(const AttnStepArgs& a, int l0, int nl, int num_sms, cud
 }  // namespace attn
 
 size_t attn_workspace_floats(int M, int D, int max_ctas) {
-  const int mc = M < 8 ? M : 8;
-  return (size_t)max_ctas * 2 * (size_t)mc * (D + 2);
+  return (size_t)max_ctas * 2 * rec_floats(M, D);
 }
 
 cudaError_t launch_attn_step(const AttnStepArgs& a, int num_sms, cudaStream_t s) {

@@ -1,0 +1,649 @@
+// attn_tc.cu -- speculative-verify attention on the 5th-generation tensor
+// cores (tcgen05 + TMEM + TMA), sm_100a, bf16 cache, head dim 128.
+//
+// Same computation as attn_decode.cu (mask P:L846-853, GQA
+// P:L834-844, SD query block P:L444-448, verify GEMM P:L905): for a
+// (batch b, kv head g) unit, its M = G*t query rows (M <= 128) attend the
+// unit's cap key rows; row tau = m % t sees keys [0, valid_b + tau).
+// Used when M is large enough to make a real tensor-core tile (the 70B
+// config's M = 8*(1+k_adm) <= 72); CUDA cores otherwise (north_star item 4).
+//
+// Per CTA (persistent, one per SM) the launch's (unit, 64-key tile) stream is
+// split into equal contiguous shares; a CTA processes the runs of its share
+// that fall into one unit ("items") one after the other:
+//   warps 0, 6: TMA producers -- 2D tensor-map loads (SWIZZLE_128B) of the K
+//             and the V tile (64 keys x 128 dims, 2 boxes each) into two
+//             4-stage rings; a K stage is released as soon as its Q.K^T
+//             MMAs complete, a V stage after its P.V MMAs;
+//   warp 1  : TMEM allocator + single-thread MMA issuer:
+//               S[b]  (TMEM, 128 lanes x 64 cols fp32) = Q . K^T
+//                     M=128 x N=64 x K=128, A = Q (K-major SW128, smem),
+//                     B = K tile (K-major SW128);
+//               O     (TMEM, 128 x 128 fp32)          += P . V
+//                     M=128 x N=128 x K=64, A = P (bf16, K-major SW128),
+//                     B = V tile (MN-major SW128), issued twice: P_hi, P_lo;
+//   warps 2-5: softmax / epilogue, one thread per query row (TMEM lane):
+//             tcgen05.ld of the S row, mask, online softmax with lazy
+//             rescaling of O (only when the running max grows by > 8 in
+//             log2 units; O is rescaled in TMEM with tcgen05.ld/st), and
+//             P = exp2(s - m) split into bf16 hi + lo (P = hi + lo to 2^-17),
+//             written to smem in the UMMA layout.
+// The bf16 rounding of P alone (2^-9 relative) could spend the whole 2e-3
+// budget on a near one-hot row; the hi/lo split makes P exact to ~2^-17 at the
+// price of a second P.V MMA, which the tensor pipe has ample room for (this
+// kernel is HBM-bound: 32 KiB of K+V per 3.1 M MACs).
+// Split units use the same partial-record + last-CTA combine as attn_decode.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "bmc_internal.h"
+#include "combine.cuh"
+
+namespace bmc {
+namespace tc {
+
+constexpr int D = 128;            // head dim (bf16)
+constexpr int KT = 64;            // keys per tile
+constexpr int MM = 128;           // MMA M (query rows, padded)
+constexpr int KS = 4;             // K ring stages (released right after Q.K^T)
+constexpr int VS = 4;             // V ring stages (released after P.V)
+constexpr int kThreads = 224;     // 7 warps
+constexpr uint32_t kTileBytes = KT * D * 2;            // 16 KiB per tensor per tile
+constexpr uint32_t kBox = 64 * KT * 2;                 // one 64-col box: 8 KiB
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kRescale = 8.0f;  // lazy-rescale threshold (log2 units)
+
+// shared memory map (bytes, 1024-aligned blocks)
+constexpr uint32_t OFF_Q = 0;                                  // [2 atoms][128 rows][128 B]
+constexpr uint32_t OFF_P = OFF_Q + MM * D * 2;                 // [2 buf][hi,lo][128 rows][128 B]
+constexpr uint32_t P_BYTES = MM * KT * 2;                      // 16 KiB
+constexpr uint32_t OFF_K = OFF_P + 4 * P_BYTES;                // [stage][2 boxes][64][128 B]
+constexpr uint32_t OFF_V = OFF_K + KS * kTileBytes;
+constexpr uint32_t OFF_BAR = OFF_V + VS * kTileBytes;
+constexpr uint32_t kSmem = OFF_BAR + 256 + 1024;               // + alignment slack
+static_assert(kSmem <= 232448, "shared memory");
+
+struct Params {
+  CUtensorMap tmK;   // [U*cap rows][128] bf16, box 64 x 64, SWIZZLE_128B
+  CUtensorMap tmV;
+  const __nv_bfloat16* Q;   // [B][H_q][t][D]
+  float* O;                 // [B][H_q][t][D]
+  float* ws;
+  int* counters;
+  long long cap;
+  long long total_tiles;
+  int tpu, U, H_kv, H_q, G, t, M, ctas;
+  float qscale;
+  int valid[BMC_MAX_B];
+};
+
+// ------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(n));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* tm, int c0, int c1,
+                                            uint32_t bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+      "l"(tm), "r"(c0), "r"(c1), "r"(bar), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   bar)
+               : "memory");
+}
+__device__ __forceinline__ void umma_f16(uint32_t dtmem, uint64_t adesc, uint64_t bdesc,
+                                         uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(dtmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ void softmax_sync() {  // warps 2..5
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+}
+
+// 64 consecutive fp32 TMEM columns of this thread's lane
+__device__ __forceinline__ void tmem_ld64(uint32_t taddr, float* v) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x64.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,"
+      "%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,"
+      "%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+        "=r"(r[31]), "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]),
+        "=r"(r[37]), "=r"(r[38]), "=r"(r[39]), "=r"(r[40]), "=r"(r[41]), "=r"(r[42]),
+        "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]), "=r"(r[48]),
+        "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]),
+        "=r"(r[55]), "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]),
+        "=r"(r[61]), "=r"(r[62]), "=r"(r[63])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_st64(uint32_t taddr, const float* v) {
+  const uint32_t* r = reinterpret_cast<const uint32_t*>(v);
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x64.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,"
+      "%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,%48,"
+      "%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63,%64};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+      "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]),
+      "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]),
+      "r"(r[29]), "r"(r[30]), "r"(r[31]), "r"(r[32]), "r"(r[33]), "r"(r[34]), "r"(r[35]),
+      "r"(r[36]), "r"(r[37]), "r"(r[38]), "r"(r[39]), "r"(r[40]), "r"(r[41]), "r"(r[42]),
+      "r"(r[43]), "r"(r[44]), "r"(r[45]), "r"(r[46]), "r"(r[47]), "r"(r[48]), "r"(r[49]),
+      "r"(r[50]), "r"(r[51]), "r"(r[52]), "r"(r[53]), "r"(r[54]), "r"(r[55]), "r"(r[56]),
+      "r"(r[57]), "r"(r[58]), "r"(r[59]), "r"(r[60]), "r"(r[61]), "r"(r[62]), "r"(r[63])
+      : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+// 32 consecutive fp32 TMEM columns of this thread's lane
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+        "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float* v) {
+  const uint32_t* r = reinterpret_cast<const uint32_t*>(v);
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+      "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]),
+      "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]),
+      "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+// UMMA shared-memory descriptor, SWIZZLE_128B (layout type 2), version 1.
+// lbo/sbo in bytes.
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;   // version (Blackwell)
+  d |= (uint64_t)2 << 61;   // SWIZZLE_128B
+  return d;
+}
+// Instruction descriptor kind::f16: fp32 accumulate, bf16 A and B.
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int b_mn_major) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)b_mn_major << 16) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+// byte offset of (row, 16-byte chunk) inside a [rows][128 B] SWIZZLE_128B atom column
+__device__ __forceinline__ uint32_t sw128(uint32_t row, uint32_t chunk) {
+  return row * 128u + ((chunk ^ (row & 7u)) << 4);
+}
+
+__device__ __forceinline__ int cta_of_tile(long long x, long long NT, int C) {
+  return (int)(((x + 1) * C + NT - 1) / NT) - 1;
+}
+__device__ __forceinline__ long long tile_begin(int c, long long NT, int C) {
+  return (long long)c * NT / C;
+}
+
+__global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_constant__ Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  // 1024-byte alignment for the swizzle atoms
+  uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const uint32_t sbase = su32(smem);
+  const uint32_t bar0 = sbase + OFF_BAR;
+  // mbarriers (8 bytes each)
+  auto FULLK = [&](int s) { return bar0 + 8u * s; };               // TMA -> MMA
+  auto EMPTYK = [&](int s) { return bar0 + 8u * (4 + s); };        // MMA -> TMA
+  auto FULLV = [&](int s) { return bar0 + 8u * (8 + s); };
+  auto EMPTYV = [&](int s) { return bar0 + 8u * (12 + s); };
+  auto SFULL = [&](int b) { return bar0 + 8u * (16 + b); };        // MMA -> softmax
+  auto SEMPTY = [&](int b) { return bar0 + 8u * (18 + b); };       // softmax -> MMA
+  auto PFULL = [&](int b) { return bar0 + 8u * (20 + b); };        // softmax -> MMA
+  auto PEMPTY = [&](int b) { return bar0 + 8u * (22 + b); };       // MMA -> softmax
+  const uint32_t QFULL = bar0 + 8u * 24;                           // softmax -> MMA
+  const uint32_t ODONE = bar0 + 8u * 25;                           // MMA -> softmax
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + OFF_BAR + 8 * 26);
+  int* sm_flag = reinterpret_cast<int*>(smem + OFF_BAR + 8 * 26 + 8);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const long long NT = p.total_tiles;
+  const long long t_begin = tile_begin(blockIdx.x, NT, p.ctas);
+  const long long t_end = tile_begin(blockIdx.x + 1, NT, p.ctas);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < KS; ++s) {
+      mbar_init(FULLK(s), 1);
+      mbar_init(EMPTYK(s), 1);
+    }
+    for (int s = 0; s < VS; ++s) {
+      mbar_init(FULLV(s), 1);
+      mbar_init(EMPTYV(s), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(SFULL(b), 1);
+      mbar_init(SEMPTY(b), 128);
+      mbar_init(PFULL(b), 128);
+      mbar_init(PEMPTY(b), 1);
+    }
+    mbar_init(QFULL, 128);
+    mbar_init(ODONE, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
+                     su32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  // zero the padded rows of Q and P once (rows >= M are never written again)
+  for (uint32_t i = threadIdx.x; i < (OFF_K - OFF_Q) / 16; i += kThreads)
+    reinterpret_cast<uint4*>(smem + OFF_Q)[i] = make_uint4(0, 0, 0, 0);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tO = tmem + 128;
+
+  if (warp == 0 || warp == 6) {
+    // ------------------------------------------------------ TMA producers
+    if (lane == 0) {
+      const bool isK = warp == 0;
+      const CUtensorMap* tm = isK ? &p.tmK : &p.tmV;
+      const int NS = isK ? KS : VS;
+      const uint32_t ring = sbase + (isK ? OFF_K : OFF_V);
+      const uint64_t pol = evict_first_policy();
+      int s = 0;
+      uint32_t ph = 0;
+      long long u = t_begin / p.tpu;
+      int j = (int)(t_begin % p.tpu);
+      for (long long i = t_begin; i < t_end; ++i) {
+        mbar_wait(isK ? EMPTYK(s) : EMPTYV(s), ph ^ 1);
+        const int row = (int)(u * p.cap + (long long)j * KT);
+        const uint32_t dst = ring + s * kTileBytes;
+        const uint32_t fb = isK ? FULLK(s) : FULLV(s);
+        mbar_expect_tx(fb, kTileBytes);
+        tma_load_2d(dst, tm, 0, row, fb, pol);
+        tma_load_2d(dst + kBox, tm, 64, row, fb, pol);
+        if (++j == p.tpu) { j = 0; ++u; }
+        if (++s == NS) { s = 0; ph ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t IQK = idesc_bf16(MM, KT, 0);   // S = Q K^T, B K-major
+      constexpr uint32_t IPV = idesc_bf16(MM, D, 1);    // O += P V, B MN-major
+      int ks = 0, vs = 0;
+      uint32_t kph = 0, vph = 0;
+      uint32_t sph = 0, pph = 0;      // phase bits per S / P buffer
+      uint32_t qph = 0;
+      long long i = t_begin;
+      int tcount = 0;                 // tiles of this CTA so far (S / P buffer index)
+      while (i < t_end) {
+        const long long u = i / p.tpu;
+        const long long iend = min(t_end, (u + 1) * p.tpu);
+        mbar_wait(QFULL, qph);        // Q of this unit is in smem
+        qph ^= 1;
+        fence_after();
+        const int n = (int)(iend - i);
+        // software pipeline: S(k+1) is computed while softmax works on S(k)
+        for (int k = 0; k <= n; ++k) {
+          if (k < n) {
+            const int b = (tcount + k) & 1;
+            mbar_wait(FULLK(ks), kph);
+            mbar_wait(SEMPTY(b), ((sph >> b) & 1) ^ 1);
+            sph ^= 1u << b;
+            fence_after();
+            const uint32_t kt = sbase + OFF_K + ks * kTileBytes;
+            const uint32_t tS = tmem + 64 * b;
+#pragma unroll
+            for (int kk = 0; kk < D / 16; ++kk) {
+              const uint32_t qa = sbase + OFF_Q + (kk >> 2) * (MM * 128) + (kk & 3) * 32;
+              const uint32_t ka = kt + (kk >> 2) * kBox + (kk & 3) * 32;
+              umma_f16(tS, sdesc(qa, 16, 1024), sdesc(ka, 16, 1024), IQK, kk > 0);
+            }
+            umma_commit(SFULL(b));
+            umma_commit(EMPTYK(ks));    // K stage reusable once Q.K^T completed
+            if (++ks == KS) { ks = 0; kph ^= 1; }
+          }
+          if (k > 0) {
+            const int kp = k - 1;
+            const int b = (tcount + kp) & 1;
+            mbar_wait(PFULL(b), (pph >> b) & 1);
+            pph ^= 1u << b;
+            mbar_wait(FULLV(vs), vph);
+            fence_after();
+            const uint32_t vt = sbase + OFF_V + vs * kTileBytes;
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+              const uint32_t pa0 = sbase + OFF_P + (2 * b + half) * P_BYTES;
+#pragma unroll
+              for (int kk = 0; kk < KT / 16; ++kk) {
+                const uint32_t pa = pa0 + kk * 32;
+                const uint32_t va = vt + kk * 2048;   // 16 keys = two 8-row groups
+                umma_f16(tO, sdesc(pa, 16, 1024), sdesc(va, kBox, 1024), IPV,
+                         (kp > 0 || half > 0 || kk > 0) ? 1u : 0u);
+              }
+            }
+            umma_commit(PEMPTY(b));     // P buffer b reusable, O updated
+            umma_commit(EMPTYV(vs));    // V stage reusable
+            if (++vs == VS) { vs = 0; vph ^= 1; }
+          }
+        }
+        umma_commit(ODONE);             // every MMA of this item is complete
+        tcount += n;
+        i = iend;
+      }
+    }
+  } else {
+    // ------------------------------------------------ softmax + epilogue
+    const int quarter = warp & 3;       // TMEM lanes 32*quarter .. +31
+    const int row = quarter * 32 + lane;
+    const bool active = row < p.M;
+    const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
+    const int stid = threadIdx.x - 64;  // 0..127
+    uint32_t sph = 0, oph = 0;
+    uint32_t puse0 = 0, puse1 = 0;      // tiles that have used P buffer 0 / 1
+    long long i = t_begin;
+    int tcount = 0;
+    bool first_item = true;
+    while (i < t_end) {
+      const long long u = i / p.tpu;
+      const long long iend = min(t_end, (u + 1) * p.tpu);
+      const int b_ = (int)(u / p.H_kv), g_ = (int)(u % p.H_kv);
+      const int j0 = (int)(i % p.tpu);
+      // load this unit's query rows into smem (K-major SW128; scaled in fp32 later)
+      const __nv_bfloat16* qsrc = p.Q + ((size_t)b_ * p.H_q + (size_t)g_ * p.G) * p.t * D;
+      for (int x = stid; x < p.M * (D / 8); x += 128) {
+        const int r = x / (D / 8), c = x % (D / 8);
+        const uint4 v = *reinterpret_cast<const uint4*>(qsrc + (size_t)r * D + c * 8);
+        *reinterpret_cast<uint4*>(smem + OFF_Q + (c >> 3) * (MM * 128) + sw128(r, c & 7)) = v;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(QFULL);
+      const int nvis = active ? p.valid[b_] + (row % p.t) : 0;
+      float m_use = -INFINITY, l = 0.f;
+      const int n = (int)(iend - i);
+      for (int k = 0; k < n; ++k) {
+        const int bb = (tcount + k) & 1;
+        const long long key0 = (long long)(j0 + k) * KT;
+        mbar_wait(SFULL(bb), (sph >> bb) & 1);
+        sph ^= 1u << bb;
+        fence_after();
+        float sv[KT];
+        tmem_ld64(tmem + 64 * bb + lane_addr, sv);
+        fence_before();
+        mbar_arrive(SEMPTY(bb));
+        // P buffer bb was last read by the PV of the tile two back: the c-th
+        // completion of PEMPTY(bb) belongs to the c-th tile using bb
+        const uint32_t pu = bb ? puse1 : puse0;
+        if (pu >= 1) mbar_wait(PEMPTY(bb), (pu - 1) & 1);
+        float mt = -INFINITY;
+        if (active) {
+#pragma unroll
+          for (int c = 0; c < KT; ++c) {
+            sv[c] = (key0 + c < nvis) ? sv[c] * p.qscale : -INFINITY;
+            mt = fmaxf(mt, sv[c]);
+          }
+        }
+        // lazy rescale: keep the old max unless the new one exceeds it by > 8
+        bool rescale = false;
+        float alpha = 1.f;
+        if (active && mt > m_use + kRescale) {
+          alpha = (m_use == -INFINITY) ? 0.f : fast_exp2(m_use - mt);
+          rescale = (m_use != -INFINITY) && k > 0;
+          m_use = mt;
+          l *= alpha;
+        }
+        // O must not be written by PV(k-1) while it is rescaled
+        if (__any_sync(0xffffffffu, rescale)) {
+          const uint32_t pp = bb ? puse0 : puse1;   // buffer of the previous tile
+          mbar_wait(PEMPTY(bb ^ 1), (pp - 1) & 1);  // its PV has completed
+          fence_after();
+#pragma unroll 1
+          for (int h = 0; h < 4; ++h) {
+            float ov[32];
+            tmem_ld32(tO + h * 32 + lane_addr, ov);
+            if (rescale) {
+#pragma unroll
+              for (int c = 0; c < 32; ++c) ov[c] *= alpha;
+            }
+            tmem_st32(tO + h * 32 + lane_addr, ov);
+          }
+          fence_before();
+        }
+        // P = exp2(s - m_use) split into bf16 hi + lo, written in UMMA layout
+        uint8_t* phi = smem + OFF_P + (2 * bb) * P_BYTES;
+        uint8_t* plo = phi + P_BYTES;
+        if (active) {
+          float ts = 0.f;
+          const bool none = (m_use == -INFINITY);
+#pragma unroll
+          for (int c8 = 0; c8 < KT / 8; ++c8) {
+            uint32_t hw[4], lw[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float p0 = none ? 0.f : fast_exp2(sv[c8 * 8 + 2 * e] - m_use);
+              const float p1 = none ? 0.f : fast_exp2(sv[c8 * 8 + 2 * e + 1] - m_use);
+              ts += p0 + p1;
+              const __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
+              const float2 hf = __bfloat1622float2(h2);
+              const __nv_bfloat162 l2 = __floats2bfloat162_rn(p0 - hf.x, p1 - hf.y);
+              hw[e] = *reinterpret_cast<const uint32_t*>(&h2);
+              lw[e] = *reinterpret_cast<const uint32_t*>(&l2);
+            }
+            *reinterpret_cast<uint4*>(phi + sw128(row, c8)) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+            *reinterpret_cast<uint4*>(plo + sw128(row, c8)) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+          }
+          l += ts;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(PFULL(bb));
+        if (bb) ++puse1; else ++puse0;
+      }
+      // ---- epilogue of this item: O (TMEM) -> output or partial record
+      mbar_wait(ODONE, oph);
+      oph ^= 1;
+      fence_after();
+      const long long ufirst = u * p.tpu, ulast = ufirst + p.tpu - 1;
+      const int c_lo = cta_of_tile(ufirst, NT, p.ctas);
+      const int c_hi = cta_of_tile(ulast, NT, p.ctas);
+      const int nseg = c_hi - c_lo + 1;
+      const size_t rec = rec_floats(p.M, D);
+      float* my = p.ws + ((size_t)blockIdx.x * 2 + (first_item ? 0 : 1)) * rec;
+      float* orow = p.O + (((size_t)b_ * p.H_q + (size_t)g_ * p.G) * p.t) * D + (size_t)row * D;
+      const float inv = 1.f / l;
+#pragma unroll 1
+      for (int h = 0; h < 4; ++h) {
+        float ov[32];
+        tmem_ld32(tO + h * 32 + lane_addr, ov);
+        if (active) {
+          float* dst = (nseg == 1) ? orow + h * 32 : my + (size_t)row * D + h * 32;
+          const float sc = (nseg == 1) ? inv : 1.f;
+#pragma unroll
+          for (int c = 0; c < 32; c += 4)
+            *reinterpret_cast<float4*>(dst + c) =
+                make_float4(ov[c] * sc, ov[c + 1] * sc, ov[c + 2] * sc, ov[c + 3] * sc);
+        }
+      }
+      if (active && nseg > 1) {
+        my[(size_t)p.M * D + row] = m_use;
+        my[(size_t)p.M * D + p.M + row] = l;
+      }
+      fence_before();
+      if (nseg > 1) {
+        __threadfence();
+        softmax_sync();
+        if (stid == 0) {
+          const int old = atomicAdd(&p.counters[u], 1);
+          *sm_flag = (old == nseg - 1);
+        }
+        softmax_sync();
+        if (*sm_flag) {
+          __threadfence();
+          if (active)   // one thread per query row merges that row
+            combine_row(p.ws, rec, c_lo, c_hi, ufirst, NT, p.ctas, p.M, D, row, orow);
+          if (stid == 0) p.counters[u] = 0;
+        }
+        softmax_sync();
+      }
+      tcount += n;
+      first_item = false;
+      i = iend;
+    }
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (warp == 1) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+  }
+}
+
+}  // namespace tc
+
+// ------------------------------------------------------------------ host
+
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled encode_fn() {
+  static PFN_encodeTiled fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled>(p);
+  }
+  return fn;
+}
+
+static cudaError_t make_map(CUtensorMap* m, const void* base, long long rows) {
+  PFN_encodeTiled fn = encode_fn();
+  if (!fn) return cudaErrorNotSupported;
+  const cuuint64_t dims[2] = {(cuuint64_t)tc::D, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)tc::D * 2};
+  const cuuint32_t box[2] = {64, (cuuint32_t)tc::KT};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+bool attn_tc_supported(int D, int dtype, int M) {
+  return D == 128 && dtype == BMC_BF16 && M >= 1 && M <= tc::MM && encode_fn() != nullptr;
+}
+
+cudaError_t launch_attn_tc(const AttnStepArgs& a, int num_sms, cudaStream_t s) {
+  static int attr_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev != dev) {
+    cudaError_t e = cudaFuncSetAttribute(tc::attn_tc_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmem);
+    if (e != cudaSuccess) return e;
+    attr_dev = dev;
+  }
+  const AttnLayer& h = a.layers[0];
+  tc::Params p;
+  const long long U = (long long)a.B * a.H_kv;
+  cudaError_t e = make_map(&p.tmK, h.K, U * h.cap);
+  if (e == cudaSuccess) e = make_map(&p.tmV, h.V, U * h.cap);
+  if (e != cudaSuccess) return e;
+  p.Q = (const __nv_bfloat16*)h.Q;
+  p.O = h.O;
+  p.ws = h.ws;
+  p.counters = h.counters;
+  p.cap = h.cap;
+  p.tpu = (int)((h.cap + tc::KT - 1) / tc::KT);
+  p.U = (int)U;
+  p.total_tiles = U * p.tpu;
+  p.H_kv = a.H_kv;
+  p.H_q = a.H_q;
+  p.G = a.H_q / a.H_kv;
+  p.t = a.t;
+  p.M = p.G * a.t;
+  p.qscale = tc::kLog2e / sqrtf((float)tc::D);
+  for (int b = 0; b < a.B; ++b) p.valid[b] = a.valid[b];
+  int ctas = a.ctas > 0 ? a.ctas : num_sms;
+  if (ctas > p.total_tiles) ctas = (int)p.total_tiles;
+  p.ctas = ctas;
+  if (p.total_tiles == 0) return cudaSuccess;
+  tc::attn_tc_kernel<<<ctas, tc::kThreads, tc::kSmem, s>>>(p);
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace bmc

@@ -43,6 +43,7 @@ struct bmc_ctx {
   bmc::Arena* arena = nullptr;
   int arena_kind = 1;   // stream-ordered pool (measured fastest); 0 = VMM slots
   float* ws = nullptr;
+  size_t ws_floats = 0;
   int* counters = nullptr;
   int num_sms = 148;
   int max_ctas = 148;
@@ -64,6 +65,7 @@ struct bmc_ctx {
 };
 
 static thread_local std::string g_err;
+static constexpr int kTcMinM = 2;   // auto path: tcgen05 for M = G*t > kTcMinM
 
 static int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
 static int fail(int code, const char* fmt, ...) {
@@ -211,6 +213,17 @@ static int flush_pending(bmc_t h) {
   return rc;
 }
 
+// Partial-record workspace for up to M query rows per unit (grown on demand).
+static int ensure_workspace(bmc_t h, int M) {
+  const size_t need = bmc::attn_workspace_floats(M, h->D, h->max_ctas);
+  if (need <= h->ws_floats) return 0;
+  cudaFreeAsync(h->ws, h->stream);
+  h->ws = nullptr;
+  CK(h, cudaMallocAsync((void**)&h->ws, need * sizeof(float), h->stream), "workspace");
+  h->ws_floats = need;
+  return 0;
+}
+
 static void fill_layer(bmc_t h, const void* Q, float* O, bmc::AttnLayer* l) {
   l->K = h->kbuf.ptr;
   l->V = h->vbuf.ptr;
@@ -283,6 +296,7 @@ int bmc_create_ex(int B, int H_kv, int H_q, int D, int r, int N_max, bmc_dtype d
   int err = 0;
   h->arena = bmc::arena_create(device, (size_t)h->U * N_max * h->row_bytes, &err);
   const size_t wsf = bmc::attn_workspace_floats(8, D, h->max_ctas);
+  h->ws_floats = wsf;
   // stream-ordered: creating a handle never synchronises the device
   cudaError_t e = cudaMallocAsync((void**)&h->ws, wsf * sizeof(float), h->stream);
   if (e == cudaSuccess) e = cudaMallocAsync((void**)&h->counters, (size_t)h->U * sizeof(int), h->stream);
@@ -410,13 +424,32 @@ int bmc_sdpa(bmc_t h, const void* Q, int n_valid, float* O) {
     }
     od = h->stage_out;
   }
+  const int M = (h->H_q / h->H_kv) * t;
+  // tensor cores when M = G*t makes a real tile (north_star item 4); the
+  // crossover measured on B200 is M = 3..4 (tcgen05 1.4x faster at M=4,
+  // 2.1x at M=5), CUDA cores keep M <= 2 (6.2-6.4 TB/s at M=1)
+  const bool use_tc = h->attn_path == 2 ||
+                      (h->attn_path == 0 && M > kTcMinM && bmc::attn_tc_supported(h->D, h->dt, M));
+  if (use_tc) {
+    if (!bmc::attn_tc_supported(h->D, h->dt, M))
+      return fail(BMC_ERR_UNSUPPORTED, "tcgen05 path needs bf16, D=128, G*t<=128");
+    rc = ensure_workspace(h, M);
+    if (rc) return rc;
+    if (h->n_app || h->n_draft) rc = flush_pending(h);
+    if (rc) return rc;
+  }
   bmc::AttnLayer layer;
   fill_layer(h, qd, od, &layer);
   bmc::AttnStepArgs a;
   fill_args(h, t, &a);
   a.L = 1;
   a.layers = &layer;
-  CK(h, bmc::launch_attn_step(a, h->num_sms, h->stream), "attn_step");
+  if (use_tc) {
+    a.ctas = std::min(h->attn_ctas, h->num_sms);
+    CK(h, bmc::launch_attn_tc(a, h->num_sms, h->stream), "attn_tc");
+  } else {
+    CK(h, bmc::launch_attn_step(a, h->num_sms, h->stream), "attn_step");
+  }
   h->n_app = h->n_draft = 0;
   account_sdpa(h, t);
   if (host_out) {

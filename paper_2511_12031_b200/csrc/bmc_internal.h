@@ -64,9 +64,18 @@ struct AttnStepArgs {
   const AttnLayer* layers;
 };
 size_t attn_workspace_floats(int M, int D, int max_ctas);
+// floats of one split-K partial record (M rows of o[D], then M maxima and M
+// sums), rounded up to 16 bytes so every record starts 16-byte aligned
+__host__ __device__ inline size_t rec_floats(int M, int D) {
+  return ((size_t)M * (D + 2) + 3) / 4 * 4;
+}
 // Masked SDPA of L layers in one persistent launch (per 32 layers), with the
 // pending appended / drafted rows written into each cache on the way.
 cudaError_t launch_attn_step(const AttnStepArgs& a, int num_sms, cudaStream_t s);
+// tcgen05 verify attention (single layer, bf16, D = 128, M = G*t <= 128);
+// pending rows must have been flushed (the kernel does not write rows).
+bool attn_tc_supported(int D, int dtype, int M);
+cudaError_t launch_attn_tc(const AttnStepArgs& a, int num_sms, cudaStream_t s);
 
 void count_launch();
 unsigned long long launch_count();

@@ -175,3 +175,36 @@ def test_launch_count_increments():
     _decode(p, 16, check_every=4)
     assert bmc.bmc_launch_count() - n0 >= 16 + 4
     p.close()
+
+
+@pytest.mark.parametrize("H_kv,H_q,k,ctas", [(2, 2, 0, 0), (2, 8, 0, 0), (2, 16, 0, 0),
+                                             (1, 8, 8, 0), (2, 16, 8, 5), (1, 16, 7, 0),
+                                             (2, 2, 4, 7), (3, 3, 4, 11)])
+def test_tcgen05_verify_path(H_kv, H_q, k, ctas):
+    """The tensor-core verify kernel (forced with BMC_OPT_ATTN_PATH=2) against
+    the oracle: M = G*(1+k_adm) from 1 to 128 query rows per KV head, ragged
+    caps (r=24 does not divide the 64-key tile), split units (ctas=5)."""
+    p = Pair(2, H_kv, H_q, 128, 24, 300, dtype="bf16", seed=23, ctas=ctas)
+    p.gpu.set_option(bmc.BMC_OPT_ATTN_PATH, 2)
+    for _ in range(3):
+        p.append()
+    p.sdpa()
+    it = 0
+    while p.orc.stats()["valid_max"] < 280:
+        p.append()
+        k_adm = p.spec_write(k) if k else 0
+        p.sdpa(n_valid=-1)
+        if k_adm:
+            p.commit_rows(synth.acceptance(23, it, 2, k_adm))
+        it += 1
+    p.check_state()
+    p.close()
+
+
+def test_tcgen05_peaky_long():
+    """Near one-hot rows through the tensor-core path: P is split into
+    bf16 hi + lo so its rounding stays far inside the 2e-3 budget."""
+    p = Pair(2, 2, 16, 128, 64, 1500, dtype="bf16", seed=29, variant="peaky")
+    p.gpu.set_option(bmc.BMC_OPT_ATTN_PATH, 2)
+    _decode(p, 1500, check_every=61)
+    p.close()

@@ -16,7 +16,7 @@ import torch  # noqa: E402
 from paper_2511_12031_b200 import bmc  # noqa: E402
 
 
-def attn_at(B, H_kv, H_q, D, cap, t=1, reps=50, dtype="bf16", ctas=0, layers=8):
+def attn_at(B, H_kv, H_q, D, cap, t=1, reps=50, dtype="bf16", ctas=0, layers=8, path=0):
     """SDPA over `layers` independent handles filled to `cap` rows (upfront
     policy so the buffer is exactly cap rows), round-robin so each launch reads
     an L2-cold cache."""
@@ -27,6 +27,7 @@ def attn_at(B, H_kv, H_q, D, cap, t=1, reps=50, dtype="bf16", ctas=0, layers=8):
         h = bmc.KVCache(B, H_kv, H_q, D, cap, cap, dtype=dtype, policy="upfront")
         if ctas:
             h.set_option(bmc.BMC_OPT_ATTN_CTAS, ctas)
+        h.set_option(bmc.BMC_OPT_ATTN_PATH, path)
         hs.append(h)
     k = torch.randn(B, H_kv, D, device="cuda").to(tdt)
     for h in hs:
@@ -51,7 +52,8 @@ def attn_at(B, H_kv, H_q, D, cap, t=1, reps=50, dtype="bf16", ctas=0, layers=8):
     by = 2.0 * B * H_kv * cap * D * eb + B * H_q * t * D * (eb + 4)
     for h in hs:
         h.close()
-    return {"cap": cap, "t": t, "us": ms * 1e3, "GBps": by / ms / 1e6}
+    return {"cap": cap, "t": t, "M": (H_q // H_kv) * t, "path": path, "us": ms * 1e3,
+            "GBps": by / ms / 1e6}
 
 
 def copy_at(B, H_kv, D, cap_old, r, reps=20, arena=0):
@@ -128,6 +130,20 @@ def main():
         out["attn_7b"] = [attn_at(16, 32, 32, 128, c) for c in (64, 256, 1024, 2048, 4096)]
         out["attn_l3"] = [attn_at(64, 8, 32, 128, c) for c in (1024, 8192)]
         out["attn_sd5"] = [attn_at(32, 32, 32, 128, c, t=5) for c in (1024, 4096)]
+    if args.what in ("all", "tc"):
+        # verify shapes: 70B (G=8, t=1+k), L3-8B GQA (G=4), 7B-SD (t=5): CUDA cores vs tcgen05
+        out["verify"] = []
+        for (B, Hk, Hq, cap, t) in [(8, 8, 64, 8192, 9), (8, 8, 64, 8192, 1),
+                                    (64, 8, 32, 4096, 1), (32, 32, 32, 2048, 5)]:
+            for pa in (1, 2):
+                print("config", B, Hk, Hq, cap, t, pa, file=sys.stderr, flush=True)
+                out["verify"].append(attn_at(B, Hk, Hq, 128, cap, t=t, path=pa, reps=20,
+                                             layers=4))
+                print(out["verify"][-1], file=sys.stderr, flush=True)
+    if args.what == "tc72":           # ncu target: 70B-shaped verify, M = 72
+        out["verify"] = [attn_at(8, 8, 64, 128, 8192, t=9, path=2, reps=6, layers=2)]
+    if args.what == "tcrepro":
+        out["verify"] = [attn_at(8, 8, 64, 128, 1024, t=9, path=1, reps=4, layers=2)]
     if args.what == "attn4096":       # ncu target: 7B shape at full context
         out["attn_7b"] = [attn_at(16, 32, 32, 128, 4096, reps=10)]
     if args.what in ("all", "copy"):
