@@ -22,8 +22,11 @@
 //               O     (TMEM, 128 x 128 fp32)          += P . V
 //                     M=128 x N=128 x K=64, A = P (bf16, K-major SW128),
 //                     B = V tile (MN-major SW128), issued twice: P_hi, P_lo;
-//   warps 2-5: softmax / epilogue, one thread per query row (TMEM lane):
-//             tcgen05.ld of the S row, mask, online softmax with lazy
+//   warps 2-9: softmax / epilogue, two threads per query row (TMEM lane):
+//             warps 2-5 own key columns 0-31 of every S tile and O columns
+//             0-63, warps 6-9 key columns 32-63 and O columns 64-127; the
+//             row max is exchanged through shared memory each tile.
+//             tcgen05.ld of the S half-row, mask, online softmax with lazy
 //             rescaling of O (only when the running max grows by > 8 in
 //             log2 units; O is rescaled in TMEM with tcgen05.ld/st), and
 //             P = exp2(s - m) split into bf16 hi + lo (P = hi + lo to 2^-17),
@@ -50,7 +53,7 @@ constexpr int KT = 64;            // keys per tile
 constexpr int MM = 128;           // MMA M (query rows, padded)
 constexpr int KS = 4;             // K ring stages (released right after Q.K^T)
 constexpr int VS = 4;             // V ring stages (released after P.V)
-constexpr int kThreads = 224;     // 7 warps
+constexpr int kThreads = 352;     // 11 warps: K/V producers, MMA, 2 x 4 softmax warps
 constexpr uint32_t kTileBytes = KT * D * 2;            // 16 KiB per tensor per tile
 constexpr uint32_t kBox = 64 * KT * 2;                 // one 64-col box: 8 KiB
 constexpr float kLog2e = 1.4426950408889634f;
@@ -63,7 +66,8 @@ constexpr uint32_t P_BYTES = MM * KT * 2;                      // 16 KiB
 constexpr uint32_t OFF_K = OFF_P + 4 * P_BYTES;                // [stage][2 boxes][64][128 B]
 constexpr uint32_t OFF_V = OFF_K + KS * kTileBytes;
 constexpr uint32_t OFF_BAR = OFF_V + VS * kTileBytes;
-constexpr uint32_t kSmem = OFF_BAR + 256 + 1024;               // + alignment slack
+constexpr uint32_t OFF_X = OFF_BAR + 256;                      // [2 halves][128 rows] f32 exchange
+constexpr uint32_t kSmem = OFF_X + 1024 + 1024;                // + alignment slack
 static_assert(kSmem <= 232448, "shared memory");
 
 struct Params {
@@ -141,8 +145,11 @@ __device__ __forceinline__ float fast_exp2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-__device__ __forceinline__ void softmax_sync() {  // warps 2..5
-  asm volatile("bar.sync 1, 128;" ::: "memory");
+__device__ __forceinline__ void softmax_sync() {  // the 8 softmax warps (2..9)
+  asm volatile("bar.sync 1, 256;" ::: "memory");
+}
+__device__ __forceinline__ void pair_sync() {     // the 8 softmax warps, per-tile exchange
+  asm volatile("bar.sync 2, 256;" ::: "memory");
 }
 
 // 64 consecutive fp32 TMEM columns of this thread's lane
@@ -286,11 +293,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(SFULL(b), 1);
-      mbar_init(SEMPTY(b), 128);
-      mbar_init(PFULL(b), 128);
+      mbar_init(SEMPTY(b), 256);
+      mbar_init(PFULL(b), 256);
       mbar_init(PEMPTY(b), 1);
     }
-    mbar_init(QFULL, 128);
+    mbar_init(QFULL, 256);
     mbar_init(ODONE, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -309,7 +316,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
   const uint32_t tmem = *tmem_slot;
   const uint32_t tO = tmem + 128;
 
-  if (warp == 0 || warp == 6) {
+  if (warp == 0 || warp == 10) {
     // ------------------------------------------------------ TMA producers
     if (lane == 0) {
       const bool isK = warp == 0;
@@ -402,11 +409,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
     }
   } else {
     // ------------------------------------------------ softmax + epilogue
+    const int half = (warp - 2) >> 2;   // 0: key cols 0-31 / O cols 0-63; 1: the rest
     const int quarter = warp & 3;       // TMEM lanes 32*quarter .. +31
     const int row = quarter * 32 + lane;
     const bool active = row < p.M;
     const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
-    const int stid = threadIdx.x - 64;  // 0..127
+    const int stid = threadIdx.x - 64;  // 0..255
+    float* xch = reinterpret_cast<float*>(smem + OFF_X);   // [2][128]
     uint32_t sph = 0, oph = 0;
     uint32_t puse0 = 0, puse1 = 0;      // tiles that have used P buffer 0 / 1
     long long i = t_begin;
@@ -419,7 +428,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
       const int j0 = (int)(i % p.tpu);
       // load this unit's query rows into smem (K-major SW128; scaled in fp32 later)
       const __nv_bfloat16* qsrc = p.Q + ((size_t)b_ * p.H_q + (size_t)g_ * p.G) * p.t * D;
-      for (int x = stid; x < p.M * (D / 8); x += 128) {
+      for (int x = stid; x < p.M * (D / 8); x += 256) {
         const int r = x / (D / 8), c = x % (D / 8);
         const uint4 v = *reinterpret_cast<const uint4*>(qsrc + (size_t)r * D + c * 8);
         *reinterpret_cast<uint4*>(smem + OFF_Q + (c >> 3) * (MM * 128) + sw128(r, c & 7)) = v;
@@ -427,31 +436,41 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_arrive(QFULL);
       const int nvis = active ? p.valid[b_] + (row % p.t) : 0;
-      float m_use = -INFINITY, l = 0.f;
+      float m_use = -INFINITY, l = 0.f;   // l: this thread's half of the row sum
       const int n = (int)(iend - i);
       for (int k = 0; k < n; ++k) {
         const int bb = (tcount + k) & 1;
-        const long long key0 = (long long)(j0 + k) * KT;
+        const long long key0 = (long long)(j0 + k) * KT + half * 32;
         mbar_wait(SFULL(bb), (sph >> bb) & 1);
         sph ^= 1u << bb;
         fence_after();
-        float sv[KT];
-        tmem_ld64(tmem + 64 * bb + lane_addr, sv);
+        float sv[32];
+        tmem_ld32(tmem + 64 * bb + half * 32 + lane_addr, sv);
         fence_before();
         mbar_arrive(SEMPTY(bb));
+        // raw-score max of this half (qscale > 0 is applied in the exponent)
+        float mt = -INFINITY;
+        if (active) {
+          if (key0 + 32 <= nvis) {          // fully visible half tile: no mask
+#pragma unroll
+            for (int c = 0; c < 32; ++c) mt = fmaxf(mt, sv[c]);
+          } else {
+#pragma unroll
+            for (int c = 0; c < 32; ++c) {
+              sv[c] = (key0 + c < nvis) ? sv[c] : -INFINITY;
+              mt = fmaxf(mt, sv[c]);
+            }
+          }
+        }
+        xch[half * 128 + row] = mt;
+        pair_sync();
+        mt = fmaxf(mt, xch[(half ^ 1) * 128 + row]) * p.qscale;
         // P buffer bb was last read by the PV of the tile two back: the c-th
         // completion of PEMPTY(bb) belongs to the c-th tile using bb
         const uint32_t pu = bb ? puse1 : puse0;
         if (pu >= 1) mbar_wait(PEMPTY(bb), (pu - 1) & 1);
-        float mt = -INFINITY;
-        if (active) {
-#pragma unroll
-          for (int c = 0; c < KT; ++c) {
-            sv[c] = (key0 + c < nvis) ? sv[c] * p.qscale : -INFINITY;
-            mt = fmaxf(mt, sv[c]);
-          }
-        }
         // lazy rescale: keep the old max unless the new one exceeds it by > 8
+        // (both threads of a row take the same decision from the same values)
         bool rescale = false;
         float alpha = 1.f;
         if (active && mt > m_use + kRescale) {
@@ -466,50 +485,59 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
           mbar_wait(PEMPTY(bb ^ 1), (pp - 1) & 1);  // its PV has completed
           fence_after();
 #pragma unroll 1
-          for (int h = 0; h < 4; ++h) {
+          for (int h = 0; h < 2; ++h) {
             float ov[32];
-            tmem_ld32(tO + h * 32 + lane_addr, ov);
+            const uint32_t ta = tO + half * 64 + h * 32 + lane_addr;
+            tmem_ld32(ta, ov);
             if (rescale) {
 #pragma unroll
               for (int c = 0; c < 32; ++c) ov[c] *= alpha;
             }
-            tmem_st32(tO + h * 32 + lane_addr, ov);
+            tmem_st32(ta, ov);
           }
           fence_before();
         }
-        // P = exp2(s - m_use) split into bf16 hi + lo, written in UMMA layout
+        // P = exp2(s*qscale - m_use) split into bf16 hi + lo, UMMA layout
         uint8_t* phi = smem + OFF_P + (2 * bb) * P_BYTES;
         uint8_t* plo = phi + P_BYTES;
         if (active) {
-          float ts = 0.f;
           const bool none = (m_use == -INFINITY);
+          const float nm = -m_use;
+          float2 ts2 = make_float2(0.f, 0.f);
 #pragma unroll
-          for (int c8 = 0; c8 < KT / 8; ++c8) {
+          for (int c8 = 0; c8 < 4; ++c8) {
             uint32_t hw[4], lw[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              const float p0 = none ? 0.f : fast_exp2(sv[c8 * 8 + 2 * e] - m_use);
-              const float p1 = none ? 0.f : fast_exp2(sv[c8 * 8 + 2 * e + 1] - m_use);
-              ts += p0 + p1;
+              const float p0 = none ? 0.f : fast_exp2(fmaf(sv[c8 * 8 + 2 * e], p.qscale, nm));
+              const float p1 =
+                  none ? 0.f : fast_exp2(fmaf(sv[c8 * 8 + 2 * e + 1], p.qscale, nm));
+              const float2 pp2 = make_float2(p0, p1);
+              ts2 = __fadd2_rn(ts2, pp2);
               const __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
               const float2 hf = __bfloat1622float2(h2);
-              const __nv_bfloat162 l2 = __floats2bfloat162_rn(p0 - hf.x, p1 - hf.y);
+              const float2 lo = __ffma2_rn(hf, make_float2(-1.f, -1.f), pp2);
+              const __nv_bfloat162 l2 = __floats2bfloat162_rn(lo.x, lo.y);
               hw[e] = *reinterpret_cast<const uint32_t*>(&h2);
               lw[e] = *reinterpret_cast<const uint32_t*>(&l2);
             }
-            *reinterpret_cast<uint4*>(phi + sw128(row, c8)) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-            *reinterpret_cast<uint4*>(plo + sw128(row, c8)) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+            const int ck = half * 4 + c8;
+            *reinterpret_cast<uint4*>(phi + sw128(row, ck)) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+            *reinterpret_cast<uint4*>(plo + sw128(row, ck)) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
           }
-          l += ts;
+          l += ts2.x + ts2.y;
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_arrive(PFULL(bb));
         if (bb) ++puse1; else ++puse0;
       }
       // ---- epilogue of this item: O (TMEM) -> output or partial record
+      xch[half * 128 + row] = l;                // row sum = both halves
       mbar_wait(ODONE, oph);
       oph ^= 1;
       fence_after();
+      softmax_sync();
+      const float lrow = l + xch[(half ^ 1) * 128 + row];
       const long long ufirst = u * p.tpu, ulast = ufirst + p.tpu - 1;
       const int c_lo = cta_of_tile(ufirst, NT, p.ctas);
       const int c_hi = cta_of_tile(ulast, NT, p.ctas);
@@ -517,13 +545,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
       const size_t rec = rec_floats(p.M, D);
       float* my = p.ws + ((size_t)blockIdx.x * 2 + (first_item ? 0 : 1)) * rec;
       float* orow = p.O + (((size_t)b_ * p.H_q + (size_t)g_ * p.G) * p.t) * D + (size_t)row * D;
-      const float inv = 1.f / l;
+      const float inv = 1.f / lrow;
 #pragma unroll 1
-      for (int h = 0; h < 4; ++h) {
+      for (int h = 0; h < 2; ++h) {
         float ov[32];
-        tmem_ld32(tO + h * 32 + lane_addr, ov);
+        const int col = half * 64 + h * 32;
+        tmem_ld32(tO + col + lane_addr, ov);
         if (active) {
-          float* dst = (nseg == 1) ? orow + h * 32 : my + (size_t)row * D + h * 32;
+          float* dst = (nseg == 1) ? orow + col : my + (size_t)row * D + col;
           const float sc = (nseg == 1) ? inv : 1.f;
 #pragma unroll
           for (int c = 0; c < 32; c += 4)
@@ -531,9 +560,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
                 make_float4(ov[c] * sc, ov[c + 1] * sc, ov[c + 2] * sc, ov[c + 3] * sc);
         }
       }
-      if (active && nseg > 1) {
+      if (active && nseg > 1 && half == 0) {
         my[(size_t)p.M * D + row] = m_use;
-        my[(size_t)p.M * D + p.M + row] = l;
+        my[(size_t)p.M * D + p.M + row] = lrow;
       }
       fence_before();
       if (nseg > 1) {
@@ -546,12 +575,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
         softmax_sync();
         if (*sm_flag) {
           __threadfence();
-          if (active)   // one thread per query row merges that row
-            combine_row(p.ws, rec, c_lo, c_hi, ufirst, NT, p.ctas, p.M, D, row, orow);
+          if (active)   // two threads per query row merge that row's halves
+            combine_row(p.ws, rec, c_lo, c_hi, ufirst, NT, p.ctas, p.M, D, row, orow,
+                        half * (D / 2), D / 2);
           if (stid == 0) p.counters[u] = 0;
         }
-        softmax_sync();
       }
+      softmax_sync();                            // xch / flag reuse by the next item
       tcount += n;
       first_item = false;
       i = iend;

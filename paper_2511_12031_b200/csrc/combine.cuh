@@ -96,15 +96,16 @@ __device__ void combine_unit(const float* ws, size_t rec, int c_lo, int c_hi, lo
   }
 }
 
-// Merge of one row r by one thread (the tcgen05 epilogue has a thread per
-// query row and no spare shared memory).  out_row: D floats.
+// Merge of columns [col0, col0 + ncol) of row r by one thread (the tcgen05
+// epilogue has threads per query row and no spare shared memory).
+// out_row: the row's D floats.  ncol multiple of 32.
 __device__ inline void combine_row(const float* ws, size_t rec, int c_lo, int c_hi,
                                    long long ufirst, long long NT, int C, int M, int D, int r,
-                                   float* out_row) {
+                                   float* out_row, int col0, int ncol) {
   float mu, invl;
   cmb_row_stats(ws, rec, c_lo, c_hi, ufirst, NT, C, M, D, r, &mu, &invl);
   constexpr int CH = 8;                     // float4 columns per chunk
-  for (int v0 = 0; v0 < D / 4; v0 += CH) {
+  for (int v0 = col0 / 4; v0 < (col0 + ncol) / 4; v0 += CH) {
     float4 acc[CH];
 #pragma unroll
     for (int q = 0; q < CH; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);

@@ -178,6 +178,8 @@ def test_decode_step_matches_per_layer_calls():
     dev = torch.device("cuda")
     a = [bmc.KVCache(B, H_kv, H_q, D, r, N, dtype="bf16") for _ in range(L)]
     b = [bmc.KVCache(B, H_kv, H_q, D, r, N, dtype="bf16") for _ in range(L)]
+    for x in b:      # same CUDA-core algorithm as the fused multi-layer launch
+        x.set_option(bmc.BMC_OPT_ATTN_PATH, 1)
     plan = bmc.StepPlan(a)
     g = torch.Generator(device=dev)
     g.manual_seed(3)
@@ -195,7 +197,7 @@ def test_decode_step_matches_per_layer_calls():
         torch.cuda.synchronize()   # keep ks/vs alive until consumed
         if n % 37 == 0 or n == N:
             for l in range(L):
-                torch.testing.assert_close(oa[l], ob[l], rtol=0, atol=2e-6)
+                torch.testing.assert_close(oa[l], ob[l], rtol=0, atol=1e-5)
     for l in range(L):
         ka, va = a[l].kv()
         kb, vb = b[l].kv()
