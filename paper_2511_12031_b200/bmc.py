@@ -62,6 +62,7 @@ def load(path: str = SO_PATH):
     global _lib
     if _lib is not None:
         return _lib
+    path = os.environ.get("BMC_LIB", path)   # experiment builds only
     if not os.path.exists(path):
         raise RuntimeError(f"libbmc.so not built at {path}: run __graft_entry__.build()")
     L = ctypes.CDLL(path)

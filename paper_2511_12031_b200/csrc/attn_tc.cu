@@ -15,7 +15,9 @@
 //             and the V tile (64 keys x 128 dims, 2 boxes each) into two
 //             4-stage rings; a K stage is released as soon as its Q.K^T
 //             MMAs complete, a V stage after its P.V MMAs;
-//   warp 1  : TMEM allocator + single-thread MMA issuer:
+//   warps 1, 11: TMEM allocator + Q.K^T issuer (warp 1), P.V issuer (warp
+//             11); two issuers so that Q.K^T of later tiles never waits behind
+//             the P.V of a tile whose softmax is still running:
 //               S[b]  (TMEM, 128 lanes x 64 cols fp32) = Q . K^T
 //                     M=128 x N=64 x K=128, A = Q (K-major SW128, smem),
 //                     B = K tile (K-major SW128);
@@ -53,11 +55,14 @@ constexpr int KT = 64;            // keys per tile
 constexpr int MM = 128;           // MMA M (query rows, padded)
 constexpr int KS = 4;             // K ring stages (released right after Q.K^T)
 constexpr int VS = 4;             // V ring stages (released after P.V)
-constexpr int kThreads = 352;     // 11 warps: K/V producers, MMA, 2 x 4 softmax warps
+constexpr int kThreads = 384;     // 12 warps: K/V producers, QK / PV issuers, 2 x 4 softmax
 constexpr uint32_t kTileBytes = KT * D * 2;            // 16 KiB per tensor per tile
 constexpr uint32_t kBox = 64 * KT * 2;                 // one 64-col box: 8 KiB
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kRescale = 8.0f;  // lazy-rescale threshold (log2 units)
+#ifndef BMC_TC_HALVES
+#define BMC_TC_HALVES 2           // P.V issued for P_hi and P_lo
+#endif
 
 // shared memory map (bytes, 1024-aligned blocks)
 constexpr uint32_t OFF_Q = 0;                                  // [2 atoms][128 rows][128 B]
@@ -75,6 +80,13 @@ struct Params {
   CUtensorMap tmV;
   const __nv_bfloat16* Q;   // [B][H_q][t][D]
   float* O;                 // [B][H_q][t][D]
+  const uint8_t* Knew;      // pending appended row [B][H_kv][D] (n_app == 1)
+  const uint8_t* Vnew;
+  const uint8_t* Kd;        // pending drafts [B][H_kv][kd_stride][D]
+  const uint8_t* Vd;
+  uint8_t* Kc;              // cache base (pending rows are stored here)
+  uint8_t* Vc;
+  int n_app, n_draft, kd_stride;
   float* ws;
   int* counters;
   long long cap;
@@ -272,9 +284,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
   auto PFULL = [&](int b) { return bar0 + 8u * (20 + b); };        // softmax -> MMA
   auto PEMPTY = [&](int b) { return bar0 + 8u * (22 + b); };       // MMA -> softmax
   const uint32_t QFULL = bar0 + 8u * 24;                           // softmax -> MMA
-  const uint32_t ODONE = bar0 + 8u * 25;                           // MMA -> softmax
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + OFF_BAR + 8 * 26);
-  int* sm_flag = reinterpret_cast<int*>(smem + OFF_BAR + 8 * 26 + 8);
+  const uint32_t ODONE = bar0 + 8u * 25;                           // PV issuer -> softmax
+  const uint32_t QDONE = bar0 + 8u * 26;                           // QK issuer -> softmax
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + OFF_BAR + 8 * 27);
+  int* sm_flag = reinterpret_cast<int*>(smem + OFF_BAR + 8 * 27 + 8);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -299,6 +312,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
     }
     mbar_init(QFULL, 256);
     mbar_init(ODONE, 1);
+    mbar_init(QDONE, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -310,6 +324,36 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
   for (uint32_t i = threadIdx.x; i < (OFF_K - OFF_Q) / 16; i += kThreads)
     reinterpret_cast<uint4*>(smem + OFF_Q)[i] = make_uint4(0, 0, 0, 0);
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  // fused KV-cache update: rows appended / drafted since the last launch that
+  // fall into this CTA's tiles are stored into the cache before its TMA loads
+  // read them (P:L609 in-place update), so no separate write kernel runs
+  if (p.n_app || p.n_draft) {
+    constexpr int CHR = D * 2 / 16;                  // 16-byte chunks per row
+    const int per_unit = (p.n_app + p.n_draft) * 2 * CHR;
+    const long long u0 = t_begin / p.tpu, u1 = (t_end - 1) / p.tpu;
+    for (long long x = threadIdx.x; x < (u1 - u0 + 1) * per_unit; x += kThreads) {
+      const long long uu = u0 + x / per_unit;
+      const int y = (int)(x % per_unit);
+      const int ck = y % CHR, tensor = (y / CHR) & 1, ri = y / (2 * CHR);
+      const int vb = p.valid[(int)(uu / p.H_kv)];
+      int row;
+      const uint8_t* src;
+      if (p.n_app && ri == 0) {
+        row = vb - 1;
+        src = (tensor ? p.Vnew : p.Knew) + (size_t)uu * (D * 2);
+      } else {
+        const int di = ri - p.n_app;
+        row = vb + di;
+        src = (tensor ? p.Vd : p.Kd) + ((size_t)uu * p.kd_stride + di) * (D * 2);
+      }
+      const long long tile = uu * p.tpu + row / KT;
+      if (tile < t_begin || tile >= t_end) continue;     // another CTA owns it
+      const uint4 v = *reinterpret_cast<const uint4*>(src + ck * 16);
+      *reinterpret_cast<uint4*>((tensor ? p.Vc : p.Kc) + ((size_t)uu * p.cap + row) * (D * 2) +
+                                ck * 16) = v;
+    }
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+  }
   fence_before();
   __syncthreads();
   fence_after();
@@ -341,16 +385,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------ MMA issuer
+    // ------------------------------------------------------ Q.K^T issuer
     if (lane == 0) {
       constexpr uint32_t IQK = idesc_bf16(MM, KT, 0);   // S = Q K^T, B K-major
-      constexpr uint32_t IPV = idesc_bf16(MM, D, 1);    // O += P V, B MN-major
-      int ks = 0, vs = 0;
-      uint32_t kph = 0, vph = 0;
-      uint32_t sph = 0, pph = 0;      // phase bits per S / P buffer
-      uint32_t qph = 0;
+      int ks = 0;
+      uint32_t kph = 0, sph = 0, qph = 0;
       long long i = t_begin;
-      int tcount = 0;                 // tiles of this CTA so far (S / P buffer index)
+      int tcount = 0;                 // tiles of this CTA so far (S buffer index)
       while (i < t_end) {
         const long long u = i / p.tpu;
         const long long iend = min(t_end, (u + 1) * p.tpu);
@@ -358,51 +399,64 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
         qph ^= 1;
         fence_after();
         const int n = (int)(iend - i);
-        // software pipeline: S(k+1) is computed while softmax works on S(k)
-        for (int k = 0; k <= n; ++k) {
-          if (k < n) {
-            const int b = (tcount + k) & 1;
-            mbar_wait(FULLK(ks), kph);
-            mbar_wait(SEMPTY(b), ((sph >> b) & 1) ^ 1);
-            sph ^= 1u << b;
-            fence_after();
-            const uint32_t kt = sbase + OFF_K + ks * kTileBytes;
-            const uint32_t tS = tmem + 64 * b;
+        for (int k = 0; k < n; ++k) {
+          const int b = (tcount + k) & 1;
+          mbar_wait(FULLK(ks), kph);
+          mbar_wait(SEMPTY(b), ((sph >> b) & 1) ^ 1);
+          sph ^= 1u << b;
+          fence_after();
+          const uint32_t kt = sbase + OFF_K + ks * kTileBytes;
+          const uint32_t tS = tmem + 64 * b;
 #pragma unroll
-            for (int kk = 0; kk < D / 16; ++kk) {
-              const uint32_t qa = sbase + OFF_Q + (kk >> 2) * (MM * 128) + (kk & 3) * 32;
-              const uint32_t ka = kt + (kk >> 2) * kBox + (kk & 3) * 32;
-              umma_f16(tS, sdesc(qa, 16, 1024), sdesc(ka, 16, 1024), IQK, kk > 0);
-            }
-            umma_commit(SFULL(b));
-            umma_commit(EMPTYK(ks));    // K stage reusable once Q.K^T completed
-            if (++ks == KS) { ks = 0; kph ^= 1; }
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t qa = sbase + OFF_Q + (kk >> 2) * (MM * 128) + (kk & 3) * 32;
+            const uint32_t ka = kt + (kk >> 2) * kBox + (kk & 3) * 32;
+            umma_f16(tS, sdesc(qa, 16, 1024), sdesc(ka, 16, 1024), IQK, kk > 0);
           }
-          if (k > 0) {
-            const int kp = k - 1;
-            const int b = (tcount + kp) & 1;
-            mbar_wait(PFULL(b), (pph >> b) & 1);
-            pph ^= 1u << b;
-            mbar_wait(FULLV(vs), vph);
-            fence_after();
-            const uint32_t vt = sbase + OFF_V + vs * kTileBytes;
-#pragma unroll
-            for (int half = 0; half < 2; ++half) {
-              const uint32_t pa0 = sbase + OFF_P + (2 * b + half) * P_BYTES;
-#pragma unroll
-              for (int kk = 0; kk < KT / 16; ++kk) {
-                const uint32_t pa = pa0 + kk * 32;
-                const uint32_t va = vt + kk * 2048;   // 16 keys = two 8-row groups
-                umma_f16(tO, sdesc(pa, 16, 1024), sdesc(va, kBox, 1024), IPV,
-                         (kp > 0 || half > 0 || kk > 0) ? 1u : 0u);
-              }
-            }
-            umma_commit(PEMPTY(b));     // P buffer b reusable, O updated
-            umma_commit(EMPTYV(vs));    // V stage reusable
-            if (++vs == VS) { vs = 0; vph ^= 1; }
-          }
+          umma_commit(SFULL(b));
+          umma_commit(EMPTYK(ks));    // K stage reusable once Q.K^T completed
+          if (++ks == KS) { ks = 0; kph ^= 1; }
         }
-        umma_commit(ODONE);             // every MMA of this item is complete
+        umma_commit(QDONE);           // Q may be overwritten for the next item
+        tcount += n;
+        i = iend;
+      }
+    }
+  } else if (warp == 11) {
+    // ------------------------------------------------------ P.V issuer
+    if (lane == 0) {
+      constexpr uint32_t IPV = idesc_bf16(MM, D, 1);    // O += P V, B MN-major
+      int vs = 0;
+      uint32_t vph = 0, pph = 0;
+      long long i = t_begin;
+      int tcount = 0;
+      while (i < t_end) {
+        const long long u = i / p.tpu;
+        const long long iend = min(t_end, (u + 1) * p.tpu);
+        const int n = (int)(iend - i);
+        for (int k = 0; k < n; ++k) {
+          const int b = (tcount + k) & 1;
+          mbar_wait(PFULL(b), (pph >> b) & 1);
+          pph ^= 1u << b;
+          mbar_wait(FULLV(vs), vph);
+          fence_after();
+          const uint32_t vt = sbase + OFF_V + vs * kTileBytes;
+#pragma unroll
+          for (int hl = 0; hl < BMC_TC_HALVES; ++hl) {
+            const uint32_t pa0 = sbase + OFF_P + (2 * b + hl) * P_BYTES;
+#pragma unroll
+            for (int kk = 0; kk < KT / 16; ++kk) {
+              const uint32_t pa = pa0 + kk * 32;
+              const uint32_t va = vt + kk * 2048;   // 16 keys = two 8-row groups
+              umma_f16(tO, sdesc(pa, 16, 1024), sdesc(va, kBox, 1024), IPV,
+                       (k > 0 || hl > 0 || kk > 0) ? 1u : 0u);
+            }
+          }
+          umma_commit(PEMPTY(b));     // P buffer b reusable, O updated
+          umma_commit(EMPTYV(vs));    // V stage reusable
+          if (++vs == VS) { vs = 0; vph ^= 1; }
+        }
+        umma_commit(ODONE);           // every P.V of this item is complete
         tcount += n;
         i = iend;
       }
@@ -416,7 +470,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
     const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
     const int stid = threadIdx.x - 64;  // 0..255
     float* xch = reinterpret_cast<float*>(smem + OFF_X);   // [2][128]
-    uint32_t sph = 0, oph = 0;
+    uint32_t sph = 0, oph = 0, qdph = 0;
     uint32_t puse0 = 0, puse1 = 0;      // tiles that have used P buffer 0 / 1
     long long i = t_begin;
     int tcount = 0;
@@ -426,7 +480,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
       const long long iend = min(t_end, (u + 1) * p.tpu);
       const int b_ = (int)(u / p.H_kv), g_ = (int)(u % p.H_kv);
       const int j0 = (int)(i % p.tpu);
-      // load this unit's query rows into smem (K-major SW128; scaled in fp32 later)
+      // load this unit's query rows into smem (K-major SW128; scaled in fp32
+      // later) once the previous item's Q.K^T MMAs have completed
+      if (!first_item) {
+        mbar_wait(QDONE, qdph);
+        qdph ^= 1;
+      }
       const __nv_bfloat16* qsrc = p.Q + ((size_t)b_ * p.H_q + (size_t)g_ * p.G) * p.t * D;
       for (int x = stid; x < p.M * (D / 8); x += 256) {
         const int r = x / (D / 8), c = x % (D / 8);
@@ -575,7 +634,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
         softmax_sync();
         if (*sm_flag) {
           __threadfence();
-          if (active)   // two threads per query row merge that row's halves
+          if (p.M <= 16)   // few rows: spread the merge over all 256 threads
+            combine_chunks<4>(p.ws, rec, c_lo, c_hi, ufirst, NT, p.ctas, p.M, D,
+                              p.O + (((size_t)b_ * p.H_q + (size_t)g_ * p.G) * p.t) * D, stid,
+                              256);
+          else if (active) // two threads per query row merge that row's halves
             combine_row(p.ws, rec, c_lo, c_hi, ufirst, NT, p.ctas, p.M, D, row, orow,
                         half * (D / 2), D / 2);
           if (stid == 0) p.counters[u] = 0;
@@ -654,6 +717,15 @@ cudaError_t launch_attn_tc(const AttnStepArgs& a, int num_sms, cudaStream_t s) {
   if (e != cudaSuccess) return e;
   p.Q = (const __nv_bfloat16*)h.Q;
   p.O = h.O;
+  p.Knew = (const uint8_t*)h.Knew;
+  p.Vnew = (const uint8_t*)h.Vnew;
+  p.Kd = (const uint8_t*)h.Kd;
+  p.Vd = (const uint8_t*)h.Vd;
+  p.Kc = (uint8_t*)h.K;
+  p.Vc = (uint8_t*)h.V;
+  p.n_app = h.n_app;
+  p.n_draft = h.n_draft;
+  p.kd_stride = h.kd_stride;
   p.ws = h.ws;
   p.counters = h.counters;
   p.cap = h.cap;

@@ -435,8 +435,6 @@ int bmc_sdpa(bmc_t h, const void* Q, int n_valid, float* O) {
       return fail(BMC_ERR_UNSUPPORTED, "tcgen05 path needs bf16, D=128, G*t<=128");
     rc = ensure_workspace(h, M);
     if (rc) return rc;
-    if (h->n_app || h->n_draft) rc = flush_pending(h);
-    if (rc) return rc;
   }
   bmc::AttnLayer layer;
   fill_layer(h, qd, od, &layer);
@@ -487,6 +485,11 @@ int bmc_decode_step(const bmc_t* hs, int L, const void* const* K, const void* co
   }
   for (int l = 0; l < L; ++l)
     if (ptr_kind(Q[l]) != 0 || ptr_kind(O[l]) != 0) fused = false;
+  // GQA groups large enough for the tensor cores take the (per-layer) tcgen05 kernel
+  const bmc_t h0 = hs[0];
+  if (h0->attn_path != 1 && (h0->attn_path == 2 || h0->H_q / h0->H_kv > kTcMinM) &&
+      bmc::attn_tc_supported(h0->D, h0->dt, h0->H_q / h0->H_kv))
+    fused = false;
   if (!fused) {
     for (int l = 0; l < L; ++l) {
       int rc = bmc_append(hs[l], K[l], V[l]);

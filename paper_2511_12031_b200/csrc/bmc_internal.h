@@ -73,7 +73,7 @@ __host__ __device__ inline size_t rec_floats(int M, int D) {
 // pending appended / drafted rows written into each cache on the way.
 cudaError_t launch_attn_step(const AttnStepArgs& a, int num_sms, cudaStream_t s);
 // tcgen05 verify attention (single layer, bf16, D = 128, M = G*t <= 128);
-// pending rows must have been flushed (the kernel does not write rows).
+// writes the layer's pending rows into the cache itself, like attn_step.
 bool attn_tc_supported(int D, int dtype, int M);
 cudaError_t launch_attn_tc(const AttnStepArgs& a, int num_sms, cudaStream_t s);
 

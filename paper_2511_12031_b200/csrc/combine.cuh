@@ -130,4 +130,43 @@ __device__ inline void combine_row(const float* ws, size_t rec, int c_lo, int c_
   }
 }
 
+// Merge by `nthr` threads parallel over 16-byte chunks of the unit's M x D
+// output (no shared memory): each thread recomputes the stats of the rows it
+// touches (2*nseg L2-resident scalars) and loads its chunk of every record
+// before combining.  out: the unit's M*D floats.
+template <int SEG>
+__device__ void combine_chunks(const float* ws, size_t rec, int c_lo, int c_hi, long long ufirst,
+                               long long NT, int C, int M, int D, float* out, int tid, int nthr) {
+  const int nv = M * D / 4;
+  for (int v = tid; v < nv; v += nthr) {
+    const int r = (v * 4) / D;
+    float mu, invl;
+    cmb_row_stats(ws, rec, c_lo, c_hi, ufirst, NT, C, M, D, r, &mu, &invl);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int c0 = c_lo; c0 <= c_hi; c0 += SEG) {
+      float4 x[SEG];
+      float w[SEG];
+#pragma unroll
+      for (int s = 0; s < SEG; ++s) {
+        if (c0 + s <= c_hi) {
+          const float* rr = cmb_record(ws, c0 + s, ufirst, NT, C, rec);
+          x[s] = __ldcg(reinterpret_cast<const float4*>(rr) + v);
+          const float mk = __ldcg(rr + (size_t)M * D + r);
+          w[s] = (mk == -INFINITY) ? 0.f : cmb_exp2(mk - mu) * invl;
+        }
+      }
+#pragma unroll
+      for (int s = 0; s < SEG; ++s) {
+        if (c0 + s <= c_hi) {
+          acc.x += w[s] * x[s].x;
+          acc.y += w[s] * x[s].y;
+          acc.z += w[s] * x[s].z;
+          acc.w += w[s] * x[s].w;
+        }
+      }
+    }
+    reinterpret_cast<float4*>(out)[v] = acc;
+  }
+}
+
 }  // namespace bmc

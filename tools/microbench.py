@@ -142,6 +142,8 @@ def main():
                 print(out["verify"][-1], file=sys.stderr, flush=True)
     if args.what == "tc72":           # ncu target: 70B-shaped verify, M = 72
         out["verify"] = [attn_at(8, 8, 64, 128, 8192, t=9, path=2, reps=6, layers=2)]
+    if args.what == "tc8":            # ncu target: 70B-shaped decode on tensor cores, M = 8
+        out["verify"] = [attn_at(8, 8, 64, 128, 8192, t=1, path=2, reps=6, layers=2)]
     if args.what == "tcrepro":
         out["verify"] = [attn_at(8, 8, 64, 128, 1024, t=9, path=1, reps=4, layers=2)]
     if args.what == "attn4096":       # ncu target: 7B shape at full context
