@@ -1,0 +1,45 @@
+"""Small workload for compute-sanitizer (memcheck / racecheck / synccheck):
+the toy config through every kernel: growth copies, fused appends, the CUDA-
+core attention (single layer and multi-layer step), SD with rollback, and the
+tcgen05 verify kernel; outputs checked against the oracle."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+import torch  # noqa: E402
+
+from harness import Pair  # noqa: E402
+from paper_2511_12031_b200 import bmc, synth  # noqa: E402
+
+# toy config (BASELINE configs[0]), fp32, CUDA cores
+p = Pair(1, 2, 2, 64, 16, 128, dtype="f32")
+for _ in range(40):
+    p.append()
+    p.sdpa()
+p.check_state()
+p.close()
+# SD with per-row commits, bf16, tensor cores (M = 4 * (1 + 3))
+p = Pair(2, 1, 4, 128, 16, 96, dtype="bf16", seed=3, ctas=3)
+p.gpu.set_option(bmc.BMC_OPT_ATTN_PATH, 2)
+for it in range(12):
+    p.append()
+    k = p.spec_write(3)
+    p.sdpa(n_valid=-1)
+    p.commit_rows(synth.acceptance(3, it, 2, k))
+p.check_state()
+p.close()
+# multi-layer step
+caches = [bmc.KVCache(1, 2, 2, 128, 8, 32, dtype="bf16") for _ in range(3)]
+plan = bmc.StepPlan(caches)
+ks = [torch.randn(1, 2, 128, device="cuda").to(torch.bfloat16) for _ in range(3)]
+qs = [torch.randn(1, 2, 1, 128, device="cuda").to(torch.bfloat16) for _ in range(3)]
+os_ = [torch.empty(1, 2, 1, 128, device="cuda") for _ in range(3)]
+for n in range(1, 20):
+    bmc.bmc_decode_step(plan, plan.ptrs(ks), plan.ptrs(ks), plan.ptrs(qs), plan.ptrs(os_), n)
+torch.cuda.synchronize()
+for c in caches:
+    c.close()
+print("sanitize target ok")
