@@ -71,8 +71,8 @@ constexpr uint32_t P_BYTES = MM * KT * 2;                      // 16 KiB
 constexpr uint32_t OFF_K = OFF_P + 4 * P_BYTES;                // [stage][2 boxes][64][128 B]
 constexpr uint32_t OFF_V = OFF_K + KS * kTileBytes;
 constexpr uint32_t OFF_BAR = OFF_V + VS * kTileBytes;
-constexpr uint32_t OFF_X = OFF_BAR + 256;                      // [2 halves][128 rows] f32 exchange
-constexpr uint32_t kSmem = OFF_X + 1024 + 1024;                // + alignment slack
+constexpr uint32_t OFF_X = OFF_BAR + 256;                      // [2 parity][2 halves][128] f32
+constexpr uint32_t kSmem = OFF_X + 2048;   // the dynamic window starts 1024-aligned (checked)
 static_assert(kSmem <= 232448, "shared memory");
 
 struct Params {
@@ -269,10 +269,11 @@ __device__ __forceinline__ long long tile_begin(int c, long long NT, int C) {
 }
 
 __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_constant__ Params p) {
-  extern __shared__ uint8_t smem_raw[];
-  // 1024-byte alignment for the swizzle atoms
-  uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // the SWIZZLE_128B atoms need 1024-byte alignment of the dynamic window
+  uint8_t* smem = smem_raw;
   const uint32_t sbase = su32(smem);
+  if (sbase & 1023u) __trap();
   const uint32_t bar0 = sbase + OFF_BAR;
   // mbarriers (8 bytes each)
   auto FULLK = [&](int s) { return bar0 + 8u * s; };               // TMA -> MMA
@@ -521,9 +522,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
             }
           }
         }
-        xch[half * 128 + row] = mt;
+        // exchange buffer alternates with the tile parity: the per-tile barrier
+        // keeps the two threads of a row within one tile of each other
+        float* xk = xch + ((tcount + k) & 1) * 256;
+        xk[half * 128 + row] = mt;
         pair_sync();
-        mt = fmaxf(mt, xch[(half ^ 1) * 128 + row]) * p.qscale;
+        mt = fmaxf(mt, xk[(half ^ 1) * 128 + row]) * p.qscale;
         // P buffer bb was last read by the PV of the tile two back: the c-th
         // completion of PEMPTY(bb) belongs to the c-th tile using bb
         const uint32_t pu = bb ? puse1 : puse0;
@@ -591,12 +595,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
         if (bb) ++puse1; else ++puse0;
       }
       // ---- epilogue of this item: O (TMEM) -> output or partial record
-      xch[half * 128 + row] = l;                // row sum = both halves
+      float* xl = xch + ((tcount + n) & 1) * 256;   // the parity no tile reads now
+      xl[half * 128 + row] = l;                 // row sum = both halves
       mbar_wait(ODONE, oph);
       oph ^= 1;
       fence_after();
       softmax_sync();
-      const float lrow = l + xch[(half ^ 1) * 128 + row];
+      const float lrow = l + xl[(half ^ 1) * 128 + row];
       const long long ufirst = u * p.tpu, ulast = ufirst + p.tpu - 1;
       const int c_lo = cta_of_tile(ufirst, NT, p.ctas);
       const int c_hi = cta_of_tile(ulast, NT, p.ctas);

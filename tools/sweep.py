@@ -51,16 +51,22 @@ def main():
     ap.add_argument("--config", default="7b")
     ap.add_argument("--rs", default="8,32,64,128,512")
     ap.add_argument("--baselines", default="iterative,upfront")
+    ap.add_argument("--n-max", type=int, default=0, help="override N_max (quick runs)")
     args = ap.parse_args()
     cfg = dict(bench.CONFIGS[args.config])
+    if args.n_max:
+        cfg["N"] = args.n_max
+        cfg["workload"] += f" [N_max overridden to {args.n_max}]"
     bmc.load()
     pts = []
-    for pol in [p for p in args.baselines.split(",") if p]:
-        r = cfg["N"] if pol == "upfront" else 1
-        pts.append(run_point(cfg, pol, r))
-        print(json.dumps(pts[-1]), file=sys.stderr, flush=True)
+    # BMC points first; the iterative baseline (one pool allocation per layer
+    # and token) runs last so its allocator churn cannot affect the others
     for r in [int(x) for x in args.rs.split(",") if x]:
         pts.append(run_point(cfg, "bmc", r))
+        print(json.dumps(pts[-1]), file=sys.stderr, flush=True)
+    for pol in sorted([p for p in args.baselines.split(",") if p], key=lambda x: x == "iterative"):
+        r = cfg["N"] if pol == "upfront" else 1
+        pts.append(run_point(cfg, pol, r))
         print(json.dumps(pts[-1]), file=sys.stderr, flush=True)
     by = {(p["policy"], p["r"]): p["tokens_per_s"] for p in pts}
     best = max((p for p in pts if p["policy"] == "bmc"), key=lambda p: p["tokens_per_s"])
