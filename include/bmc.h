@@ -124,7 +124,12 @@ int bmc_commit_rows(bmc_t h, const int* n_accepted_host);
    layer l = 0..L-1: bmc_append(hs[l], K[l], V[l]) then
    bmc_sdpa(hs[l], Q[l], n_valid, O[l]) (n_valid = the committed length AFTER
    the append, or BMC_PER_ROW).  Arrays of L pointers.  Every layer is
-   validated before anything is enqueued.  One call instead of 2L. */
+   validated before anything is enqueued.  One call instead of 2L.
+   When every K, V, Q and O is a HOST pointer the step is pipelined: the
+   inputs are staged on an internal copy stream (double-buffered, so the copy
+   of step s+1 overlaps the kernels of step s) and the outputs are copied back
+   on it; with pinned buffers everything is asynchronous -- read O after
+   bmc_sync(hs[0]) and keep inputs unchanged until then. */
 int bmc_decode_step(const bmc_t* hs, int L, const void* const* K, const void* const* V,
                     const void* const* Q, float* const* O, int n_valid);
 

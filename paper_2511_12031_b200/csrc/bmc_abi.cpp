@@ -62,7 +62,35 @@ struct bmc_ctx {
   const void* kd = nullptr;
   const void* vd = nullptr;
   int n_app = 0, n_draft = 0, kd_stride = 0;
+  struct Pipe* pipe = nullptr;   // host-I/O pipeline of bmc_decode_step (first layer owns it)
 };
+
+// Host-I/O pipeline of bmc_decode_step: two staging slots, a copy stream and
+// events, so that the host->device copy of step s+1 and the device->host copy
+// of step s's outputs overlap the kernels of step s (e2e path).
+struct Pipe {
+  cudaStream_t copy = nullptr;
+  cudaEvent_t in_ready[2] = {}, compute_done[2] = {}, out_done[2] = {};
+  char* in_slot[2] = {nullptr, nullptr};
+  char* out_slot[2] = {nullptr, nullptr};
+  size_t in_bytes = 0, out_bytes = 0;
+  long long step = 0;
+  bool primed[2] = {false, false};
+};
+
+static void pipe_destroy(Pipe* p) {
+  if (!p) return;
+  if (p->copy) cudaStreamSynchronize(p->copy);
+  for (int i = 0; i < 2; ++i) {
+    if (p->in_ready[i]) cudaEventDestroy(p->in_ready[i]);
+    if (p->compute_done[i]) cudaEventDestroy(p->compute_done[i]);
+    if (p->out_done[i]) cudaEventDestroy(p->out_done[i]);
+    if (p->in_slot[i]) cudaFree(p->in_slot[i]);
+    if (p->out_slot[i]) cudaFree(p->out_slot[i]);
+  }
+  if (p->copy) cudaStreamDestroy(p->copy);
+  delete p;
+}
 
 static thread_local std::string g_err;
 static constexpr int kTcMinM = 2;   // auto path: tcgen05 for M = G*t > kTcMinM
@@ -457,9 +485,21 @@ int bmc_sdpa(bmc_t h, const void* Q, int n_valid, float* O) {
   return 0;
 }
 
+static int decode_step_host(const bmc_t* hs, int L, const void* const* K, const void* const* V,
+                            const void* const* Q, float* const* O, int n_valid);
+
 int bmc_decode_step(const bmc_t* hs, int L, const void* const* K, const void* const* V,
                     const void* const* Q, float* const* O, int n_valid) {
   if (!hs || L < 1 || !K || !V || !Q || !O) return fail(BMC_ERR_ARG, "null argument");
+  {
+    // all-host arguments take the pipelined host-I/O path
+    bool all_host = true;
+    for (int l = 0; l < L && all_host; ++l)
+      if (!K[l] || !V[l] || !Q[l] || !O[l] || ptr_kind(K[l]) == 0 || ptr_kind(V[l]) == 0 ||
+          ptr_kind(Q[l]) == 0 || ptr_kind(O[l]) == 0)
+        all_host = false;
+    if (all_host) return decode_step_host(hs, L, K, V, Q, O, n_valid);
+  }
   // validate every layer before enqueueing anything
   for (int l = 0; l < L; ++l) {
     bmc_t h = hs[l];
@@ -517,6 +557,74 @@ int bmc_decode_step(const bmc_t* hs, int L, const void* const* K, const void* co
   return 0;
 }
 
+// Host-pointer decode step: stage every layer's K, V, Q on the copy stream
+// into slot s%2, run the device-pointer step on the compute stream, and copy
+// the outputs back on the copy stream.  Pinned host buffers make all copies
+// asynchronous (outputs are readable after bmc_sync); inputs must stay
+// unchanged until the copy stream has passed them.
+static int decode_step_host(const bmc_t* hs, int L, const void* const* K, const void* const* V,
+                            const void* const* Q, float* const* O, int n_valid) {
+  bmc_t h0 = hs[0];
+  int rc = enter(h0);
+  if (rc) return rc;
+  for (int l = 1; l < L; ++l)
+    if (hs[l]->B != h0->B || hs[l]->H_kv != h0->H_kv || hs[l]->H_q != h0->H_q ||
+        hs[l]->D != h0->D || hs[l]->dt != h0->dt || hs[l]->stream != h0->stream ||
+        hs[l]->device != h0->device)
+      return fail(BMC_ERR_ARG, "host-I/O decode step needs layers of one shape and stream");
+  const size_t kv = (size_t)h0->U * h0->row_bytes;
+  const size_t q = (size_t)h0->B * h0->H_q * h0->row_bytes;
+  const size_t o = (size_t)h0->B * h0->H_q * h0->D * sizeof(float);
+  auto al = [](size_t x) { return (x + 255) / 256 * 256; };
+  const size_t per_in = 2 * al(kv) + al(q), per_out = al(o);
+  Pipe* pp = h0->pipe;
+  if (!pp || pp->in_bytes < per_in * L || pp->out_bytes < per_out * L) {
+    if (pp) {
+      cudaStreamSynchronize(h0->stream);
+      pipe_destroy(pp);
+    }
+    pp = new Pipe();
+    h0->pipe = pp;
+    CK(h0, cudaStreamCreateWithFlags(&pp->copy, cudaStreamNonBlocking), "pipe stream");
+    for (int i = 0; i < 2; ++i) {
+      CK(h0, cudaEventCreateWithFlags(&pp->in_ready[i], cudaEventDisableTiming), "pipe event");
+      CK(h0, cudaEventCreateWithFlags(&pp->compute_done[i], cudaEventDisableTiming), "pipe event");
+      CK(h0, cudaEventCreateWithFlags(&pp->out_done[i], cudaEventDisableTiming), "pipe event");
+      CK(h0, cudaMalloc((void**)&pp->in_slot[i], per_in * L), "pipe staging");
+      CK(h0, cudaMalloc((void**)&pp->out_slot[i], per_out * L), "pipe staging");
+    }
+    pp->in_bytes = per_in * L;
+    pp->out_bytes = per_out * L;
+  }
+  const int slot = (int)(pp->step & 1);
+  std::vector<const void*> dK(L), dV(L), dQ(L);
+  std::vector<float*> dO(L);
+  if (pp->primed[slot]) CK(h0, cudaStreamWaitEvent(pp->copy, pp->compute_done[slot], 0), "wait");
+  for (int l = 0; l < L; ++l) {
+    char* base = pp->in_slot[slot] + per_in * l;
+    dK[l] = base;
+    dV[l] = base + al(kv);
+    dQ[l] = base + 2 * al(kv);
+    dO[l] = reinterpret_cast<float*>(pp->out_slot[slot] + per_out * l);
+    CK(h0, cudaMemcpyAsync((void*)dK[l], K[l], kv, cudaMemcpyHostToDevice, pp->copy), "H2D");
+    CK(h0, cudaMemcpyAsync((void*)dV[l], V[l], kv, cudaMemcpyHostToDevice, pp->copy), "H2D");
+    CK(h0, cudaMemcpyAsync((void*)dQ[l], Q[l], q, cudaMemcpyHostToDevice, pp->copy), "H2D");
+  }
+  CK(h0, cudaEventRecord(pp->in_ready[slot], pp->copy), "record");
+  CK(h0, cudaStreamWaitEvent(h0->stream, pp->in_ready[slot], 0), "wait");
+  if (pp->primed[slot]) CK(h0, cudaStreamWaitEvent(h0->stream, pp->out_done[slot], 0), "wait");
+  rc = bmc_decode_step(hs, L, dK.data(), dV.data(), dQ.data(), dO.data(), n_valid);
+  if (rc) return rc;
+  CK(h0, cudaEventRecord(pp->compute_done[slot], h0->stream), "record");
+  CK(h0, cudaStreamWaitEvent(pp->copy, pp->compute_done[slot], 0), "wait");
+  for (int l = 0; l < L; ++l)
+    CK(h0, cudaMemcpyAsync(O[l], dO[l], o, cudaMemcpyDeviceToHost, pp->copy), "D2H");
+  CK(h0, cudaEventRecord(pp->out_done[slot], pp->copy), "record");
+  pp->primed[slot] = true;
+  pp->step += 1;
+  return 0;
+}
+
 static int commit_impl(bmc_t h, const int* m) {
   if (h->n_app || h->n_draft) {
     int rc = flush_pending(h);
@@ -569,6 +677,8 @@ int bmc_destroy(bmc_t h) {
   cudaSetDevice(h->device);
   if (!h->sticky && (h->n_app || h->n_draft)) flush_pending(h);
   cudaStreamSynchronize(h->stream);
+  pipe_destroy(h->pipe);
+  h->pipe = nullptr;
   bmc::arena_release(h->arena, &h->kbuf, h->stream);
   bmc::arena_release(h->arena, &h->vbuf, h->stream);
   for (int i = 0; i < 3; ++i)
@@ -637,6 +747,7 @@ int bmc_sync(bmc_t h) {
     if (rc) return rc;
   }
   CK(h, cudaStreamSynchronize(h->stream), "sync");
+  if (h->pipe) CK(h, cudaStreamSynchronize(h->pipe->copy), "sync copy stream");
   return 0;
 }
 

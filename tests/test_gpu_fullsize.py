@@ -205,3 +205,36 @@ def test_decode_step_matches_per_layer_calls():
         assert a[l].stats() == b[l].stats()
     for x in a + b:
         x.close()
+
+
+def test_decode_step_host_io_pipeline():
+    """bmc_decode_step with pinned host K/V/Q/O (the pipelined end-to-end path:
+    copy stream, double-buffered staging) equals the device-pointer step."""
+    B, H_kv, H_q, D, N, r, L = 3, 2, 2, 128, 150, 16, 4
+    dev = torch.device("cuda")
+    a = [bmc.KVCache(B, H_kv, H_q, D, r, N, dtype="bf16") for _ in range(L)]
+    b = [bmc.KVCache(B, H_kv, H_q, D, r, N, dtype="bf16") for _ in range(L)]
+    pa, pb = bmc.StepPlan(a), bmc.StepPlan(b)
+    g = torch.Generator().manual_seed(9)
+    oa = [torch.empty(B, H_q, 1, D).pin_memory() for _ in range(L)]
+    ob = [torch.empty(B, H_q, 1, D, device=dev) for _ in range(L)]
+    for n in range(1, N + 1):
+        ks = [torch.randn(B, H_kv, D, generator=g).to(torch.bfloat16).pin_memory() for _ in range(L)]
+        vs = [torch.randn(B, H_kv, D, generator=g).to(torch.bfloat16).pin_memory() for _ in range(L)]
+        qs = [torch.randn(B, H_q, 1, D, generator=g).to(torch.bfloat16).pin_memory()
+              for _ in range(L)]
+        bmc.bmc_decode_step(pa, pa.ptrs(ks), pa.ptrs(vs), pa.ptrs(qs), pa.ptrs(oa), n)
+        kd = [x.to(dev) for x in ks]
+        vd = [x.to(dev) for x in vs]
+        qd = [x.to(dev) for x in qs]
+        bmc.bmc_decode_step(pb, pb.ptrs(kd), pb.ptrs(vd), pb.ptrs(qd), pb.ptrs(ob), n)
+        a[0].sync()                      # host outputs readable; inputs reusable
+        torch.cuda.synchronize()
+        for l in range(L):
+            assert torch.equal(oa[l], ob[l].cpu()), (n, l)
+    for x, y in zip(a, b):
+        kx, vx = x.kv()
+        ky, vy = y.kv()
+        assert torch.equal(_bits(kx), _bits(ky)) and torch.equal(_bits(vx), _bits(vy))
+    for x in a + b:
+        x.close()
