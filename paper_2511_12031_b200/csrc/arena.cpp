@@ -309,7 +309,7 @@ void arena_destroy(Arena* a) {
 // device range never turns into host memory under UVA), so repeat calls with
 // pointers into known device allocations cost a short scan.
 namespace {
-struct Range { uintptr_t base, end; };
+struct Range { uintptr_t base, end; int kind; };
 std::mutex g_rmu;
 std::vector<Range> g_ranges;
 }  // namespace
@@ -320,8 +320,9 @@ int pointer_kind(const void* ptr) {
     std::lock_guard<std::mutex> lk(g_rmu);
     for (size_t i = 0; i < g_ranges.size(); ++i) {
       if (p >= g_ranges[i].base && p < g_ranges[i].end) {
+        const int k = g_ranges[i].kind;
         if (i > 0) std::swap(g_ranges[i], g_ranges[i - 1]);  // keep hot ranges in front
-        return 0;
+        return k;
       }
     }
   }
@@ -330,17 +331,24 @@ int pointer_kind(const void* ptr) {
     cudaGetLastError();
     return 2;
   }
-  if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) {
+  const int kind = (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) ? 0
+                   : (a.type == cudaMemoryTypeHost ? 1 : 2);
+  if (kind < 2) {
+    // device and page-locked host allocations are mapped into the unified
+    // address space: remember their whole range (pageable memory is not)
     CUdeviceptr base = 0;
     size_t size = 0;
-    if (drv().ok && drv().range(&base, &size, (CUdeviceptr)p) == CUDA_SUCCESS && size > 0) {
+    const CUdeviceptr q = kind == 0 ? (CUdeviceptr)p : (CUdeviceptr)a.devicePointer;
+    if (drv().ok && q == (CUdeviceptr)p && drv().range(&base, &size, q) == CUDA_SUCCESS &&
+        size > 0) {
       std::lock_guard<std::mutex> lk(g_rmu);
       if (g_ranges.size() >= 256) g_ranges.pop_back();
-      g_ranges.insert(g_ranges.begin(), Range{(uintptr_t)base, (uintptr_t)base + size});
+      g_ranges.insert(g_ranges.begin(), Range{(uintptr_t)base, (uintptr_t)base + size, kind});
+    } else {
+      cudaGetLastError();
     }
-    return 0;
   }
-  return a.type == cudaMemoryTypeHost ? 1 : 2;
+  return kind;
 }
 
 void forget_range(const void* ptr) {

@@ -575,10 +575,10 @@ static int decode_step_host(const bmc_t* hs, int L, const void* const* K, const 
   const size_t kv = (size_t)h0->U * h0->row_bytes;
   const size_t q = (size_t)h0->B * h0->H_q * h0->row_bytes;
   const size_t o = (size_t)h0->B * h0->H_q * h0->D * sizeof(float);
-  auto al = [](size_t x) { return (x + 255) / 256 * 256; };
-  const size_t per_in = 2 * al(kv) + al(q), per_out = al(o);
+  // staging slot: [K of every layer][V ...][Q ...]; output slot [O ...]
+  const size_t per_in = (2 * kv + q) * L, per_out = o * L;
   Pipe* pp = h0->pipe;
-  if (!pp || pp->in_bytes < per_in * L || pp->out_bytes < per_out * L) {
+  if (!pp || pp->in_bytes < per_in || pp->out_bytes < per_out) {
     if (pp) {
       cudaStreamSynchronize(h0->stream);
       pipe_destroy(pp);
@@ -590,26 +590,42 @@ static int decode_step_host(const bmc_t* hs, int L, const void* const* K, const 
       CK(h0, cudaEventCreateWithFlags(&pp->in_ready[i], cudaEventDisableTiming), "pipe event");
       CK(h0, cudaEventCreateWithFlags(&pp->compute_done[i], cudaEventDisableTiming), "pipe event");
       CK(h0, cudaEventCreateWithFlags(&pp->out_done[i], cudaEventDisableTiming), "pipe event");
-      CK(h0, cudaMalloc((void**)&pp->in_slot[i], per_in * L), "pipe staging");
-      CK(h0, cudaMalloc((void**)&pp->out_slot[i], per_out * L), "pipe staging");
+      CK(h0, cudaMalloc((void**)&pp->in_slot[i], per_in), "pipe staging");
+      CK(h0, cudaMalloc((void**)&pp->out_slot[i], per_out), "pipe staging");
     }
-    pp->in_bytes = per_in * L;
-    pp->out_bytes = per_out * L;
+    pp->in_bytes = per_in;
+    pp->out_bytes = per_out;
   }
   const int slot = (int)(pp->step & 1);
   std::vector<const void*> dK(L), dV(L), dQ(L);
   std::vector<float*> dO(L);
-  if (pp->primed[slot]) CK(h0, cudaStreamWaitEvent(pp->copy, pp->compute_done[slot], 0), "wait");
+  char* kb = pp->in_slot[slot];
+  char* vb = kb + kv * L;
+  char* qb = vb + kv * L;
+  char* ob = pp->out_slot[slot];
   for (int l = 0; l < L; ++l) {
-    char* base = pp->in_slot[slot] + per_in * l;
-    dK[l] = base;
-    dV[l] = base + al(kv);
-    dQ[l] = base + 2 * al(kv);
-    dO[l] = reinterpret_cast<float*>(pp->out_slot[slot] + per_out * l);
-    CK(h0, cudaMemcpyAsync((void*)dK[l], K[l], kv, cudaMemcpyHostToDevice, pp->copy), "H2D");
-    CK(h0, cudaMemcpyAsync((void*)dV[l], V[l], kv, cudaMemcpyHostToDevice, pp->copy), "H2D");
-    CK(h0, cudaMemcpyAsync((void*)dQ[l], Q[l], q, cudaMemcpyHostToDevice, pp->copy), "H2D");
+    dK[l] = kb + kv * l;
+    dV[l] = vb + kv * l;
+    dQ[l] = qb + q * l;
+    dO[l] = reinterpret_cast<float*>(ob + o * l);
   }
+  // one copy per tensor when the caller's per-layer buffers are contiguous
+  auto contiguous = [&](const void* const* a, size_t sz) {
+    for (int l = 1; l < L; ++l)
+      if ((const char*)a[l] != (const char*)a[0] + sz * l) return false;
+    return true;
+  };
+  auto h2d = [&](char* dst, const void* const* src, size_t sz) -> int {
+    if (contiguous(src, sz)) {
+      CK(h0, cudaMemcpyAsync(dst, src[0], sz * L, cudaMemcpyHostToDevice, pp->copy), "H2D");
+    } else {
+      for (int l = 0; l < L; ++l)
+        CK(h0, cudaMemcpyAsync(dst + sz * l, src[l], sz, cudaMemcpyHostToDevice, pp->copy), "H2D");
+    }
+    return 0;
+  };
+  if (pp->primed[slot]) CK(h0, cudaStreamWaitEvent(pp->copy, pp->compute_done[slot], 0), "wait");
+  if ((rc = h2d(kb, K, kv)) || (rc = h2d(vb, V, kv)) || (rc = h2d(qb, Q, q))) return rc;
   CK(h0, cudaEventRecord(pp->in_ready[slot], pp->copy), "record");
   CK(h0, cudaStreamWaitEvent(h0->stream, pp->in_ready[slot], 0), "wait");
   if (pp->primed[slot]) CK(h0, cudaStreamWaitEvent(h0->stream, pp->out_done[slot], 0), "wait");
@@ -617,8 +633,12 @@ static int decode_step_host(const bmc_t* hs, int L, const void* const* K, const 
   if (rc) return rc;
   CK(h0, cudaEventRecord(pp->compute_done[slot], h0->stream), "record");
   CK(h0, cudaStreamWaitEvent(pp->copy, pp->compute_done[slot], 0), "wait");
-  for (int l = 0; l < L; ++l)
-    CK(h0, cudaMemcpyAsync(O[l], dO[l], o, cudaMemcpyDeviceToHost, pp->copy), "D2H");
+  if (contiguous((const void* const*)O, o)) {
+    CK(h0, cudaMemcpyAsync(O[0], ob, o * L, cudaMemcpyDeviceToHost, pp->copy), "D2H");
+  } else {
+    for (int l = 0; l < L; ++l)
+      CK(h0, cudaMemcpyAsync(O[l], dO[l], o, cudaMemcpyDeviceToHost, pp->copy), "D2H");
+  }
   CK(h0, cudaEventRecord(pp->out_done[slot], pp->copy), "record");
   pp->primed[slot] = true;
   pp->step += 1;
