@@ -69,7 +69,8 @@ struct bmc_ctx {
 // events, so that the host->device copy of step s+1 and the device->host copy
 // of step s's outputs overlap the kernels of step s (e2e path).
 struct Pipe {
-  cudaStream_t copy = nullptr;
+  cudaStream_t copy = nullptr;   // uploads (host -> device)
+  cudaStream_t down = nullptr;   // downloads (device -> host), so neither waits for the other
   cudaEvent_t in_ready[2] = {}, compute_done[2] = {}, out_done[2] = {};
   char* in_slot[2] = {nullptr, nullptr};
   char* out_slot[2] = {nullptr, nullptr};
@@ -81,6 +82,7 @@ struct Pipe {
 static void pipe_destroy(Pipe* p) {
   if (!p) return;
   if (p->copy) cudaStreamSynchronize(p->copy);
+  if (p->down) cudaStreamSynchronize(p->down);
   for (int i = 0; i < 2; ++i) {
     if (p->in_ready[i]) cudaEventDestroy(p->in_ready[i]);
     if (p->compute_done[i]) cudaEventDestroy(p->compute_done[i]);
@@ -89,6 +91,7 @@ static void pipe_destroy(Pipe* p) {
     if (p->out_slot[i]) cudaFree(p->out_slot[i]);
   }
   if (p->copy) cudaStreamDestroy(p->copy);
+  if (p->down) cudaStreamDestroy(p->down);
   delete p;
 }
 
@@ -586,6 +589,7 @@ static int decode_step_host(const bmc_t* hs, int L, const void* const* K, const 
     pp = new Pipe();
     h0->pipe = pp;
     CK(h0, cudaStreamCreateWithFlags(&pp->copy, cudaStreamNonBlocking), "pipe stream");
+    CK(h0, cudaStreamCreateWithFlags(&pp->down, cudaStreamNonBlocking), "pipe stream");
     for (int i = 0; i < 2; ++i) {
       CK(h0, cudaEventCreateWithFlags(&pp->in_ready[i], cudaEventDisableTiming), "pipe event");
       CK(h0, cudaEventCreateWithFlags(&pp->compute_done[i], cudaEventDisableTiming), "pipe event");
@@ -632,14 +636,14 @@ static int decode_step_host(const bmc_t* hs, int L, const void* const* K, const 
   rc = bmc_decode_step(hs, L, dK.data(), dV.data(), dQ.data(), dO.data(), n_valid);
   if (rc) return rc;
   CK(h0, cudaEventRecord(pp->compute_done[slot], h0->stream), "record");
-  CK(h0, cudaStreamWaitEvent(pp->copy, pp->compute_done[slot], 0), "wait");
+  CK(h0, cudaStreamWaitEvent(pp->down, pp->compute_done[slot], 0), "wait");
   if (contiguous((const void* const*)O, o)) {
-    CK(h0, cudaMemcpyAsync(O[0], ob, o * L, cudaMemcpyDeviceToHost, pp->copy), "D2H");
+    CK(h0, cudaMemcpyAsync(O[0], ob, o * L, cudaMemcpyDeviceToHost, pp->down), "D2H");
   } else {
     for (int l = 0; l < L; ++l)
-      CK(h0, cudaMemcpyAsync(O[l], dO[l], o, cudaMemcpyDeviceToHost, pp->copy), "D2H");
+      CK(h0, cudaMemcpyAsync(O[l], dO[l], o, cudaMemcpyDeviceToHost, pp->down), "D2H");
   }
-  CK(h0, cudaEventRecord(pp->out_done[slot], pp->copy), "record");
+  CK(h0, cudaEventRecord(pp->out_done[slot], pp->down), "record");
   pp->primed[slot] = true;
   pp->step += 1;
   return 0;
@@ -767,7 +771,10 @@ int bmc_sync(bmc_t h) {
     if (rc) return rc;
   }
   CK(h, cudaStreamSynchronize(h->stream), "sync");
-  if (h->pipe) CK(h, cudaStreamSynchronize(h->pipe->copy), "sync copy stream");
+  if (h->pipe) {
+    CK(h, cudaStreamSynchronize(h->pipe->copy), "sync copy stream");
+    CK(h, cudaStreamSynchronize(h->pipe->down), "sync copy stream");
+  }
   return 0;
 }
 
