@@ -3,14 +3,17 @@
 // BMC reallocates every r tokens; the paper's implementation
 // calls the framework allocator each time.  Here a handle
 // (one layer) owns one Arena:
-//   kind 0 (VMM, default): for each tensor (K, V) two ping-pong slots of
-//     reserved virtual address space, each large enough for N_max rows.  A
-//     growth maps physical chunks (cuMemCreate, from a process-wide pool) into
-//     the slot not holding the live buffer, the realloc kernel copies, and the
-//     old slot is released once the stream has passed the copy (CUDA event):
-//     its chunks are unmapped and returned to the pool for any layer's next
-//     growth.  No cudaMalloc/cudaFree on the hot path; virtual addresses of a
-//     handle only ever take two values per tensor.
+//   kind 0 (VMM): for each tensor (K, V) two ping-pong slots of reserved
+//     virtual address space, each large enough for N_max rows.  A growth maps
+//     only the physical chunks (cuMemCreate, from a process-wide pool) that
+//     the slot not holding the live buffer still lacks, the realloc kernel
+//     copies, and the old slot simply becomes the target of the next growth:
+//     mappings persist, so a growth costs at most a few cuMemMap calls, never
+//     an unmap or a host synchronisation.  The price is physical memory: both
+//     slots stay mapped (about 2x the live cache), since all layers grow in
+//     the same step and cannot lend chunks to each other.  Chunks return to
+//     the pool when the handle is destroyed.  Virtual addresses of a handle
+//     take only two values per tensor.
 //   kind 1 (pool): cudaMallocFromPoolAsync / cudaFreeAsync on a per-device
 //     memory pool with an unbounded release threshold (stream-ordered reuse).
 #include <cuda.h>
@@ -147,17 +150,6 @@ static void unmap_slot(Arena* a, Slot& s, int tensor, int slot) {
   }
 }
 
-// Reclaim every released slot whose event has completed (all arenas).
-static void reclaim_locked() {
-  for (Arena* a : g_arenas) {
-    for (int t = 0; t < 2; ++t)
-      for (int s = 0; s < 2; ++s) {
-        Slot& sl = a->slots[t][s];
-        if (sl.pending && cudaEventQuery(sl.pending) == cudaSuccess) unmap_slot(a, sl, t, s);
-      }
-  }
-}
-
 Arena* arena_create(int device, size_t max_bytes_per_tensor, int* err) {
   *err = 0;
   Arena* a = new Arena();
@@ -234,12 +226,14 @@ int arena_alloc(Arena* a, int tensor, size_t bytes, int kind, const Buffer* keep
   if (bytes == 0) bytes = 16;
   if (kind == 0 && a->vmm_ok) {
     std::lock_guard<std::mutex> lk(g_mu);
-    reclaim_locked();
     int slot = (keep && keep->ptr && keep->kind == 0) ? 1 - keep->slot : 0;
     Slot& sl = a->slots[tensor][slot];
-    if (sl.pending) {  // the GPU may still read it: wait for the release event
-      cudaEventSynchronize(sl.pending);
-      unmap_slot(a, sl, tensor, slot);
+    // the slot's previous contents were last used earlier on this stream, so
+    // the realloc kernel may overwrite them in stream order: only missing
+    // chunks are mapped (persistent mappings)
+    if (sl.pending) {
+      cudaEventDestroy(sl.pending);
+      sl.pending = nullptr;
     }
     int rc = map_slot(a, tensor, slot, bytes);
     if (rc) return rc;
@@ -273,17 +267,9 @@ int arena_release(Arena* a, Buffer* b, cudaStream_t s) {
   if (b->kind == 1) {
     rc = cudaFreeAsync(b->ptr, s) == cudaSuccess ? 0 : BMC_ERR_CUDA;
   } else {
-    std::lock_guard<std::mutex> lk(g_mu);
-    const int tensor = (int)(((CUdeviceptr)b->ptr - a->base) / a->slot_bytes) / 2;
-    Slot& sl = a->slots[tensor][b->slot];
-    cudaEvent_t ev = nullptr;
-    if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventRecord(ev, s) != cudaSuccess) {
-      rc = BMC_ERR_CUDA;
-    } else {
-      if (sl.pending) cudaEventDestroy(sl.pending);
-      sl.pending = ev;
-    }
+    // VMM slot: the mapping persists for the next growth (see header); nothing
+    // to do until the arena is destroyed
+    (void)a;
   }
   *b = Buffer();
   return rc;
