@@ -168,10 +168,15 @@ int bmc_sync(bmc_t h);
      1 BMC_OPT_ATTN_CTAS      CTAs of the attention kernel (0 = auto)
      2 BMC_OPT_ATTN_PATH      0 auto, 1 CUDA-core split-K, 2 tcgen05 verify
      3 BMC_OPT_ARENA          0 VMM ping-pong slots, 1 stream-ordered pool
-                              (default; takes effect at the next growth)  */
+                              (default; takes effect at the next growth)
+     4 BMC_OPT_SKIP_PADDING   1 = length-aware ABLATION: SDPA streams only the
+                              rows some query sees instead of all cap rows
+                              (not the method: P:L441, L853; results are
+                              identical, bytes differ)  */
 #define BMC_OPT_ATTN_CTAS 1
 #define BMC_OPT_ATTN_PATH 2
 #define BMC_OPT_ARENA 3
+#define BMC_OPT_SKIP_PADDING 4
 int bmc_set_option(bmc_t h, int key, long long value);
 
 /* Kernels launched by this library in this process so far (all handles). */

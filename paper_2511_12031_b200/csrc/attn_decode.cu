@@ -125,7 +125,8 @@ struct LayerDesc {
   const uint8_t* Vd;
   float* ws;             // partial records of this layer's split units
   int* counters;         // [U] arrival counters, zero between launches
-  long long cap;
+  long long cap;         // rows per unit slab (row stride)
+  long long scan;        // rows streamed per unit (= cap; less only in the length-aware ablation)
   long long tile0;       // first tile of this layer in the launch's tile stream
   int tpu;               // tiles per unit
   int n_app, n_draft, kd_stride;
@@ -241,7 +242,7 @@ __global__ void __launch_bounds__(kThreads, CTAS) attn_step_kernel(const __grid_
   auto issue = [&]() {
     const LayerDesc& ld = p.layer[pc.l];
     const long long row0 = (long long)pc.j * C::TR;
-    const long long rows = min((long long)C::TR, ld.cap - row0);
+    const long long rows = min((long long)C::TR, ld.scan - row0);
     const uint32_t bytes = (uint32_t)(rows * C::ROWB);
     const size_t off = (size_t)(pc.u * ld.cap + row0) * C::ROWB;
     uint8_t* dk = ring + (size_t)ps_stage * 2 * kStageBytes;
@@ -280,7 +281,7 @@ __global__ void __launch_bounds__(kThreads, CTAS) attn_step_kernel(const __grid_
   for (long long i = t_begin; i < t_end; ++i) {
     const LayerDesc& ld = p.layer[cc.l];
     const long long row0 = (long long)cc.j * C::TR;
-    const int rows_in_tile = (int)min((long long)C::TR, ld.cap - row0);
+    const int rows_in_tile = (int)min((long long)C::TR, ld.scan - row0);
     const int vb = p.valid[cc.b];
 
     if (seg_start) {
@@ -631,7 +632,8 @@ cudaError_t launch_chunk(const AttnStepArgs& a, int l0, int nl, int num_sms, cud
     d.ws = h.ws;
     d.counters = h.counters;
     d.cap = h.cap;
-    d.tpu = (int)((h.cap + TR - 1) / TR);
+    d.scan = h.scan > 0 ? h.scan : h.cap;
+    d.tpu = (int)((d.scan + TR - 1) / TR);
     d.tile0 = tiles;
     d.n_app = h.n_app;
     d.n_draft = h.n_draft;

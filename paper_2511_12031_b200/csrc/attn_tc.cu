@@ -734,7 +734,7 @@ cudaError_t launch_attn_tc(const AttnStepArgs& a, int num_sms, cudaStream_t s) {
   p.ws = h.ws;
   p.counters = h.counters;
   p.cap = h.cap;
-  p.tpu = (int)((h.cap + tc::KT - 1) / tc::KT);
+  p.tpu = (int)(((h.scan > 0 ? h.scan : h.cap) + tc::KT - 1) / tc::KT);
   p.U = (int)U;
   p.total_tiles = U * p.tpu;
   p.H_kv = a.H_kv;

@@ -49,6 +49,7 @@ struct bmc_ctx {
   int max_ctas = 148;
   int attn_ctas = 0;
   int attn_path = 0;
+  int skip_padding = 0;          // length-aware ablation, off by default
   bmc_stats_t st = {};
   int sticky = 0;
   // staging of host-pointer arguments: 0 appended rows, 1 drafts, 2 Q
@@ -267,6 +268,13 @@ static void fill_layer(bmc_t h, const void* Q, float* O, bmc::AttnLayer* l) {
   l->ws = h->ws;
   l->counters = h->counters;
   l->cap = h->cap;
+  // ablation only: stream just the rows some query can see (the method's
+  // contract reads all cap rows)
+  l->scan = 0;
+  if (h->skip_padding) {
+    const long long vis = (long long)max_valid(h) + h->staged;
+    l->scan = std::max(1LL, std::min<long long>(h->cap, vis));
+  }
   l->n_app = h->n_app;
   l->n_draft = h->n_draft;
   l->kd_stride = h->kd_stride;
@@ -792,6 +800,10 @@ int bmc_set_option(bmc_t h, int key, long long value) {
     case BMC_OPT_ARENA:
       if (value < 0 || value > 1) return fail(BMC_ERR_ARG, "arena kind");
       h->arena_kind = (int)value;
+      return 0;
+    case BMC_OPT_SKIP_PADDING:
+      if (value < 0 || value > 1) return fail(BMC_ERR_ARG, "skip padding");
+      h->skip_padding = (int)value;
       return 0;
     default:
       return fail(BMC_ERR_ARG, "unknown option %d", key);

@@ -53,6 +53,7 @@ struct AttnLayer {
   float* ws;                              // partial records
   int* counters;                          // [U], zero between launches
   long long cap;
+  long long scan;                         // rows to stream per unit (0 = cap)
   int n_app, n_draft, kd_stride;
 };
 constexpr int kMaxLayersPerLaunch = 32;

@@ -208,3 +208,19 @@ def test_tcgen05_peaky_long():
     p.gpu.set_option(bmc.BMC_OPT_ATTN_PATH, 2)
     _decode(p, 1500, check_every=61)
     p.close()
+
+
+@pytest.mark.parametrize("path,policy", [(1, "bmc"), (2, "bmc"), (1, "upfront")])
+def test_length_aware_ablation(path, policy):
+    """BMC_OPT_SKIP_PADDING (SURVEY NEXT-4 ablation): streaming only visible
+    rows leaves every output and the cache unchanged."""
+    p = Pair(2, 2, 8, 128, 40, 260, dtype="bf16", policy=policy, seed=31)
+    p.gpu.set_option(bmc.BMC_OPT_SKIP_PADDING, 1)
+    p.gpu.set_option(bmc.BMC_OPT_ATTN_PATH, path)
+    for it in range(60):
+        p.append()
+        k = p.spec_write(3)
+        p.sdpa(n_valid=-1)
+        p.commit_rows(synth.acceptance(31, it, 2, k))
+    p.check_state()
+    p.close()

@@ -23,7 +23,7 @@ import bench  # noqa: E402
 from paper_2511_12031_b200 import bmc  # noqa: E402
 
 
-def run_point(cfg, policy, r, reps=1):
+def run_point(cfg, policy, r, reps=1, skip_padding=False):
     dev = torch.device("cuda", 0)
     stream = torch.cuda.current_stream(dev)
     B = cfg["B"]
@@ -32,6 +32,7 @@ def run_point(cfg, policy, r, reps=1):
     outs = {t: [torch.empty(B, cfg["H_q"], t, cfg["D"], dtype=torch.float32, device=dev)
                 for _ in range(cfg["L"])] for t in range(1, t_all + 1)}
     gen = bench.Generation(cfg, B, r, policy, ring, outs, stream, 0)
+    gen.skip_padding = skip_padding
     gen.run()                                   # warm-up
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -42,7 +43,7 @@ def run_point(cfg, policy, r, reps=1):
     e1.record(stream)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
-    return {"policy": policy, "r": r, "T": -(-cfg["N"] // r) if policy == "bmc" else None,
+    return {"policy": policy + ("+length-aware" if skip_padding else ""), "r": r, "T": -(-cfg["N"] // r) if policy == "bmc" else None,
             "tokens_per_s": tok / (ms / 1e3), "ms_per_generation": ms / reps}
 
 
@@ -52,6 +53,8 @@ def main():
     ap.add_argument("--rs", default="8,32,64,128,512")
     ap.add_argument("--baselines", default="iterative,upfront")
     ap.add_argument("--n-max", type=int, default=0, help="override N_max (quick runs)")
+    ap.add_argument("--ablation", action="store_true",
+                    help="also run the length-aware ablation (SURVEY NEXT-4)")
     args = ap.parse_args()
     cfg = dict(bench.CONFIGS[args.config])
     if args.n_max:
@@ -68,7 +71,12 @@ def main():
         r = cfg["N"] if pol == "upfront" else 1
         pts.append(run_point(cfg, pol, r))
         print(json.dumps(pts[-1]), file=sys.stderr, flush=True)
-    by = {(p["policy"], p["r"]): p["tokens_per_s"] for p in pts}
+    if args.ablation:
+        # what the padded-GEMV contract costs: the same runs streaming only
+        # visible rows (UPFRONT + length-aware = a contiguous exact-prefix kernel)
+        for pol, r in (("bmc", 128), ("upfront", cfg["N"])):
+            pts.append(run_point(cfg, pol, r, skip_padding=True))
+            print(json.dumps(pts[-1]), file=sys.stderr, flush=True)
     best = max((p for p in pts if p["policy"] == "bmc"), key=lambda p: p["tokens_per_s"])
     out = {"config": cfg["workload"], "points": pts, "best_bmc": best}
     it = next((p for p in pts if p["policy"] == "iterative"), None)
