@@ -74,9 +74,12 @@ def lib():
         L.oracle_read_cache.argtypes = [vp, vp, vp]
         L.oracle_destroy.argtypes = [vp]
         L.oracle_exact_sdpa.argtypes = [vp, vp, vp, i, i, vp]
+        L.oracle_spec_write_tree.argtypes = [vp, vp, vp, i, ip]
+        L.oracle_commit_path.argtypes = [vp, ip, ip, i]
         for f in ("oracle_create", "oracle_append", "oracle_spec_write", "oracle_sdpa",
                   "oracle_commit", "oracle_commit_rows", "oracle_stats", "oracle_valid",
-                  "oracle_read_cache", "oracle_destroy", "oracle_exact_sdpa"):
+                  "oracle_read_cache", "oracle_destroy", "oracle_exact_sdpa",
+                  "oracle_spec_write_tree", "oracle_commit_path"):
             getattr(L, f).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -147,6 +150,32 @@ class Oracle:
         out = np.zeros((self.B, self.H_q, t, self.D), dtype=np.float64)
         self._check(lib().oracle_sdpa(self._h, _ptr(q), n_valid, _ptr(out)), "oracle_sdpa")
         return out
+
+    def spec_write_tree(self, Kd, Vd, k: int, parent) -> int:
+        par = np.ascontiguousarray(np.asarray(parent, dtype=np.int32))
+        assert par.size == k
+        if k == 0:
+            return self._check(lib().oracle_spec_write_tree(
+                self._h, None, None, 0, par.ctypes.data_as(ctypes.POINTER(ctypes.c_int))),
+                "spec_write_tree")
+        kd, vd = _raw(Kd, self.dtype), _raw(Vd, self.dtype)
+        assert kd.size == self.B * self.H_kv * k * self.D and vd.size == kd.size
+        return self._check(lib().oracle_spec_write_tree(
+            self._h, _ptr(kd), _ptr(vd), k, par.ctypes.data_as(ctypes.POINTER(ctypes.c_int))),
+            "oracle_spec_write_tree")
+
+    def commit_path(self, paths):
+        """paths: list (one per batch row) of node-index lists (root first)."""
+        assert len(paths) == self.B
+        depth = max([len(p) for p in paths] + [1])
+        arr = np.zeros((self.B, depth), dtype=np.int32)
+        m = np.zeros(self.B, dtype=np.int32)
+        for b, pth in enumerate(paths):
+            arr[b, :len(pth)] = pth
+            m[b] = len(pth)
+        ip = ctypes.POINTER(ctypes.c_int)
+        return self._check(lib().oracle_commit_path(
+            self._h, arr.ctypes.data_as(ip), m.ctypes.data_as(ip), depth), "oracle_commit_path")
 
     def commit(self, n_accepted: int):
         return self._check(lib().oracle_commit(self._h, n_accepted), "oracle_commit")

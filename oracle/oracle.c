@@ -40,6 +40,8 @@ struct oracle_ctx {
   long cap;        /* rows allocated per (b, h_kv) unit */
   int* valid;      /* [B] committed rows per batch row */
   int staged;      /* speculative rows written but not committed */
+  int tree;        /* staged rows form a token tree (else a chain) */
+  int parent[64];  /* tree topology of the staged nodes */
   unsigned char* K;
   unsigned char* V;
   oracle_stats_t st;
@@ -259,11 +261,24 @@ int oracle_spec_write(oracle_t h, const void* Kd, const void* Vd, int k) {
 
 /* -------------------------------------------------------------------- sdpa */
 
+/* Is key row j visible to query row tau of batch row b?  Chain drafts
+   (reading R7): rows [0, valid_b + tau).  Token tree: the
+   committed rows, plus node (tau-1) and its ancestors. */
+static int visible(const struct oracle_ctx* h, int b, int tau, long j) {
+  const long vb = h->valid[b];
+  if (!h->tree) return j < vb + tau;
+  if (j < vb) return 1;
+  if (tau == 0) return 0;
+  for (int x = tau - 1; x >= 0; x = h->parent[x])
+    if (j - vb == x) return 1;
+  return 0;
+}
+
 /* Masked SDPA over all cap rows of one unit for one query row
    (mask P:L853):
-     s_j = (q . k_j) / sqrt(D) + bias_j,  bias_j = 0 (j < n_vis) else -1e9
+     s_j = (q . k_j) / sqrt(D) + bias_j,  bias_j = 0 (visible) else -1e9
      p_j = exp(s_j - max_j s_j),  o = (sum_j p_j v_j) / (sum_j p_j).        */
-static void sdpa_row(const struct oracle_ctx* h, long u, const double* q, long n_vis,
+static void sdpa_row(const struct oracle_ctx* h, long u, const double* q, int b, int tau,
                      double* s, double* o) {
   const double scale = 1.0 / sqrt((double)h->D);   /* reading R4: d = head_dim */
   long cap = h->cap;
@@ -271,7 +286,7 @@ static void sdpa_row(const struct oracle_ctx* h, long u, const double* q, long n
     const unsigned char* kr = row_ptr(h, h->K, u, j);
     double dot = 0.0;
     for (int x = 0; x < h->D; ++x) dot += q[x] * elem(h, kr + (size_t)x * h->eb);
-    s[j] = dot * scale + (j < n_vis ? 0.0 : MASK_BIAS);
+    s[j] = dot * scale + (visible(h, b, tau, j) ? 0.0 : MASK_BIAS);
   }
   double mu = s[0];
   for (long j = 1; j < cap; ++j)
@@ -319,8 +334,7 @@ int oracle_sdpa(oracle_t h, const void* Q, int n_valid, double* O) {
       for (int tau = 0; tau < t; ++tau) {
         size_t qi = (((size_t)b * h->H_q + hq) * t + tau) * D;
         for (int x = 0; x < D; ++x) q[x] = elem(h, q_raw + (qi + x) * h->eb);
-        long n_vis = (long)h->valid[b] + tau;             /* chain-causal visibility */
-        sdpa_row(h, u, q, n_vis, s, O + qi);
+        sdpa_row(h, u, q, b, tau, s, O + qi);
       }
       free(s);
       free(q);
@@ -355,8 +369,10 @@ int oracle_commit(oracle_t h, int n_accepted) {
   if (!h) return OR_ERR_ARG;
   if (h->staged == 0 && n_accepted > 0) return OR_ERR_STATE;
   if (n_accepted < 0 || n_accepted > h->staged) return OR_ERR_ARG;
+  if (h->tree && n_accepted > 0) return OR_ERR_STATE;   /* trees commit paths */
   for (int b = 0; b < h->B; ++b) commit_row(h, b, n_accepted);
   h->staged = 0;
+  h->tree = 0;
   return OR_OK;
 }
 
@@ -365,9 +381,67 @@ int oracle_commit_rows(oracle_t h, const int* n_accepted) {
   for (int b = 0; b < h->B; ++b) {
     if (h->staged == 0 && n_accepted[b] > 0) return OR_ERR_STATE;
     if (n_accepted[b] < 0 || n_accepted[b] > h->staged) return OR_ERR_ARG;
+    if (h->tree && n_accepted[b] > 0) return OR_ERR_STATE;
   }
   for (int b = 0; b < h->B; ++b) commit_row(h, b, n_accepted[b]);
   h->staged = 0;
+  h->tree = 0;
+  return OR_OK;
+}
+
+/* ------------------------------------------------------------ token tree */
+
+int oracle_spec_write_tree(oracle_t h, const void* Kd, const void* Vd, int k,
+                           const int* parent) {
+  if (!h || k < 0 || k > 64) return OR_ERR_ARG;
+  if (k > 0 && (!Kd || !Vd || !parent)) return OR_ERR_ARG;
+  if (h->staged > 0) return OR_ERR_STATE;
+  for (int i = 0; i < k; ++i)
+    if (parent[i] < -1 || parent[i] >= i) return OR_ERR_ARG;   /* BFS order */
+  int k_adm = oracle_spec_write(h, Kd, Vd, k);                  /* same placement */
+  if (k_adm < 0) return k_adm;
+  for (int i = 0; i < k_adm; ++i) h->parent[i] = parent[i];
+  h->tree = k_adm > 0;
+  return k_adm;
+}
+
+int oracle_commit_path(oracle_t h, const int* path, const int* m, int max_depth) {
+  if (!h || !m || max_depth < 0) return OR_ERR_ARG;
+  for (int b = 0; b < h->B; ++b) {
+    if (m[b] < 0 || m[b] > max_depth || m[b] > h->staged) return OR_ERR_ARG;
+    if (m[b] > 0 && !path) return OR_ERR_ARG;
+    for (int i = 0; i < m[b]; ++i) {
+      const int x = path[b * max_depth + i];
+      if (x < 0 || x >= h->staged) return OR_ERR_ARG;
+      const int want = i == 0 ? -1 : path[b * max_depth + i - 1];
+      const int par = h->tree ? h->parent[x] : x - 1;          /* a chain's parents */
+      if (par != want) return OR_ERR_ARG;
+    }
+  }
+  size_t row_bytes = (size_t)h->D * h->eb;
+  for (int b = 0; b < h->B; ++b) {
+    for (int g = 0; g < h->H_kv; ++g) {
+      long u = (long)b * h->H_kv + g;
+      /* ascending moves are safe: path[i] >= i, so a destination never holds
+         a row that a later step still has to read */
+      for (int i = 0; i < m[b]; ++i) {
+        long src = (long)h->valid[b] + path[b * max_depth + i];
+        long dst = (long)h->valid[b] + i;
+        if (src != dst) {
+          memmove(row_ptr(h, h->K, u, dst), row_ptr(h, h->K, u, src), row_bytes);
+          memmove(row_ptr(h, h->V, u, dst), row_ptr(h, h->V, u, src), row_bytes);
+        }
+      }
+      for (int i = m[b]; i < h->staged; ++i) {
+        long row = (long)h->valid[b] + i;
+        memset(row_ptr(h, h->K, u, row), 0, row_bytes);
+        memset(row_ptr(h, h->V, u, row), 0, row_bytes);
+      }
+    }
+    h->valid[b] += m[b];
+  }
+  h->staged = 0;
+  h->tree = 0;
   return OR_OK;
 }
 

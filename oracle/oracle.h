@@ -54,6 +54,23 @@ int oracle_spec_write(oracle_t h, const void* Kd, const void* Vd, int k); /* [B]
 int oracle_sdpa(oracle_t h, const void* Q, int n_valid, double* O);   /* Q [B][H_q][t][D], O fp64 */
 int oracle_commit(oracle_t h, int n_accepted);
 int oracle_commit_rows(oracle_t h, const int* n_accepted);            /* [B] */
+
+/* Token-tree speculation (Sequoia-style candidate tree).
+   k nodes in breadth-first order, parent[i] in [-1, i) (-1: child of the last
+   committed token), one topology for all batch rows.  Admission as for chain
+   drafts (k_adm = min(k, free rows); a BFS prefix keeps every
+   parent before its children).  Node i sits in row valid_b + i; query row
+   tau = 1 + i sees the committed rows [0, valid_b) and the rows of node i's
+   ancestors and of node i itself, nothing else (ancestor rule).
+   Returns k_adm. */
+int oracle_spec_write_tree(oracle_t h, const void* Kd, const void* Vd, int k,
+                           const int* parent);
+/* Commit an accepted root-to-node path per row:
+   path[b*max_depth + i], i < m[b], node indices of increasing depth (path[0]
+   a root, path[i] a child of path[i-1]).  The accepted rows are moved to
+   valid_b .. valid_b + m_b - 1, all other staged rows are zeroed, valid_b +=
+   m_b.  A chain commit of n (oracle_commit) is the path 0..n-1. */
+int oracle_commit_path(oracle_t h, const int* path, const int* m, int max_depth);
 int oracle_stats(oracle_t h, oracle_stats_t* out);
 int oracle_valid(oracle_t h, int* valid);                              /* [B] */
 int oracle_read_cache(oracle_t h, void* K, void* V);                   /* raw [B*H_kv][cap][D] */

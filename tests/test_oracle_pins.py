@@ -424,3 +424,129 @@ def test_footprint_example():
     (the layout's bytes per row x rows, 2 tensors)."""
     B, L, D, N, eb = 64, 64, 4096, 2048, 2
     assert abs(2 * B * L * N * D * eb / 1e9 - 137.4) < 0.1
+
+
+# ------------------------------------------------------------ token trees
+
+def _tree_ancestors(parent, i):
+    out = []
+    while i >= 0:
+        out.append(i)
+        i = parent[i]
+    return sorted(out)
+
+
+def test_tree_worked_example(oracle_mod):
+    """P:L863-866 with the figure's 4-node tree: S11 (root), S21 and S22
+    (children of S11), S31 (child of S21), BFS order [S11, S21, S22, S31];
+    7 free rows -> 3 wasted; (S11, S22) accepted -> next tree leaves 1; S'11
+    accepted -> next tree leaves 0; no reallocation."""
+    B, H, d, r = 1, 1, 2, 8
+    orc = O.Oracle(B, H, H, d, r, 64, dtype=O.F32, policy=O.POLICY_BMC)
+    x = synth.step_inputs(5, 0, 0, B=B, H_kv=H, H_q=H, D=d, dtype="f32")
+    orc.append(x["k"], x["v"])
+    parent = [-1, 0, 0, 1]
+    allocs = orc.stats()["alloc_events"]
+    for i, (wasted, path) in enumerate([(3, [0, 2]), (1, [0]), (0, [])]):
+        xd = synth.step_inputs(5, 0, 200 + i, B=B, H_kv=H, H_q=H, D=d, k_draft=4, dtype="f32")
+        assert orc.spec_write_tree(xd["kd"], xd["vd"], 4, parent) == 4
+        s = orc.stats()
+        assert s["capacity"] - s["valid_max"] - s["staged"] == wasted
+        orc.commit_path([path])
+    assert orc.stats()["alloc_events"] == allocs
+
+
+def test_tree_mask_is_ancestor_rule(oracle_mod):
+    """Each node's output equals textbook SDPA over exactly the committed
+    prefix, its ancestors and itself (S:L351-355 ancestor rule); siblings and
+    cousins are invisible.  Bit-exact in fp64 (masked terms are exact zeros)."""
+    rng = np.random.default_rng(3)
+    B, H, d, n0 = 2, 2, 8, 9
+    for trial in range(4):
+        k = int(rng.integers(2, 12))
+        parent = [-1] + [int(rng.integers(-1, i)) for i in range(1, k)]
+        orc = O.Oracle(B, H, H, d, 32, 64, dtype=O.F32, policy=O.POLICY_BMC)
+        Ks, Vs = [], []
+        for n in range(n0):
+            x = synth.step_inputs(11 + trial, 0, n, B=B, H_kv=H, H_q=H, D=d, dtype="f32")
+            orc.append(x["k"], x["v"])
+            Ks.append(x["k"].numpy()); Vs.append(x["v"].numpy())
+        xd = synth.step_inputs(11 + trial, 0, 99, B=B, H_kv=H, H_q=H, D=d, t=1 + k,
+                               k_draft=k, dtype="f32")
+        k_adm = orc.spec_write_tree(xd["kd"], xd["vd"], k, parent)
+        assert k_adm == k
+        out = orc.sdpa(xd["q"], n0)
+        for b in range(B):
+            for h in range(H):
+                pre_k = [Ks[n][b, h] for n in range(n0)]
+                pre_v = [Vs[n][b, h] for n in range(n0)]
+                q = xd["q"].numpy()[b, h]
+                ref0 = O.exact_sdpa(q[0], np.array(pre_k, dtype=np.float64),
+                                    np.array(pre_v, dtype=np.float64))
+                assert np.array_equal(out[b, h, 0], ref0)
+                for i in range(k):
+                    rows = _tree_ancestors(parent, i)
+                    Kg = np.array(pre_k + [xd["kd"].numpy()[b, h, j] for j in rows],
+                                  dtype=np.float64)
+                    Vg = np.array(pre_v + [xd["vd"].numpy()[b, h, j] for j in rows],
+                                  dtype=np.float64)
+                    assert np.array_equal(out[b, h, 1 + i], O.exact_sdpa(q[1 + i], Kg, Vg))
+
+
+def test_chain_tree_equals_chain_drafts(oracle_mod):
+    """A chain is the tree parent[i] = i-1: outputs, commit and cache equal
+    the chain-draft calls (commit(n) == commit_path([0..n-1]))."""
+    B, H, d = 2, 1, 4
+    a = O.Oracle(B, H, H, d, 8, 64, dtype=O.BF16, policy=O.POLICY_BMC)
+    b = O.Oracle(B, H, H, d, 8, 64, dtype=O.BF16, policy=O.POLICY_BMC)
+    for n in range(3):
+        x = synth.step_inputs(21, 0, n, B=B, H_kv=H, H_q=H, D=d, dtype="bf16")
+        a.append(x["k"], x["v"]); b.append(x["k"], x["v"])
+    xd = synth.step_inputs(21, 0, 50, B=B, H_kv=H, H_q=H, D=d, t=5, k_draft=4, dtype="bf16")
+    assert a.spec_write(xd["kd"], xd["vd"], 4) == 4
+    assert b.spec_write_tree(xd["kd"], xd["vd"], 4, [-1, 0, 1, 2]) == 4
+    assert np.array_equal(a.sdpa(xd["q"], 3), b.sdpa(xd["q"], 3))
+    a.commit_rows([2, 3])
+    b.commit_path([[0, 1], [0, 1, 2]])
+    for x, y in zip(a.read_cache(), b.read_cache()):
+        assert np.array_equal(x, y)
+
+
+def test_commit_path_equals_appending_the_path(oracle_mod):
+    """Committing an accepted root-to-node path moves exactly those rows, in
+    depth order, behind the committed prefix: the cache equals
+    appending the path's K/V rows; other staged rows are zero again."""
+    B, H, d = 1, 2, 4
+    parent = [-1, -1, 0, 1, 1, 3, 2]
+    path = [1, 3, 5]
+    a = O.Oracle(B, H, H, d, 16, 64, dtype=O.F32, policy=O.POLICY_BMC)
+    b = O.Oracle(B, H, H, d, 16, 64, dtype=O.F32, policy=O.POLICY_BMC)
+    x = synth.step_inputs(23, 0, 0, B=B, H_kv=H, H_q=H, D=d, dtype="f32")
+    a.append(x["k"], x["v"]); b.append(x["k"], x["v"])
+    xd = synth.step_inputs(23, 0, 1, B=B, H_kv=H, H_q=H, D=d, k_draft=len(parent), dtype="f32")
+    a.spec_write_tree(xd["kd"], xd["vd"], len(parent), parent)
+    a.commit_path([path])
+    for j in path:
+        b.append(xd["kd"][:, :, j].contiguous(), xd["vd"][:, :, j].contiguous())
+    for u, w in zip(a.read_cache(), b.read_cache()):
+        assert np.array_equal(u, w)
+    assert list(a.valid()) == [1 + len(path)]
+
+
+def test_tree_errors(oracle_mod):
+    orc = O.Oracle(1, 1, 1, 2, 8, 64, dtype=O.F32, policy=O.POLICY_BMC)
+    z = _f32([0.5, 0.5])
+    orc.append(z, z)
+    kd = _f32(np.ones((3, 2)))
+    with pytest.raises(O.OracleError) as e:
+        orc.spec_write_tree(kd, kd, 3, [-1, 1, 0])         # parent not before child
+    assert e.value.code == -1
+    orc.spec_write_tree(kd, kd, 3, [-1, 0, 0])
+    with pytest.raises(O.OracleError) as e:
+        orc.commit(1)                                      # trees commit paths
+    assert e.value.code == -2
+    with pytest.raises(O.OracleError) as e:
+        orc.commit_path([[0, 0]])                          # not parent-linked
+    assert e.value.code == -1
+    orc.commit_path([[0, 2]])
+    assert list(orc.valid()) == [3]
