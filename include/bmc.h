@@ -103,6 +103,16 @@ int bmc_append(bmc_t h, const void* K, const void* V);
    are already staged). */
 int bmc_spec_write(bmc_t h, const void* K_draft, const void* V_draft, int k);
 
+/* bmc_spec_write_tree: place a token TREE of k candidate rows (P:L863-866,
+   Sequoia-style).  Nodes in breadth-first order; parent_host[i] in [-1, i)
+   (-1: child of the last committed token); one topology for every batch row.
+   Admitted like chain drafts (k_adm = min(k, free rows), a BFS prefix keeps
+   parents before children, never grows).  Node i sits in row valid_b + i;
+   at bmc_sdpa its query row tau = 1 + i sees the committed rows, its
+   ancestors and itself only.  k <= 32 (else UNSUPPORTED).  Returns k_adm. */
+int bmc_spec_write_tree(bmc_t h, const void* K_draft, const void* V_draft, int k,
+                        const int* parent_host);
+
 /* bmc_sdpa: masked scaled-dot-product attention over ALL cap rows of the
    padded cache (mask P:L846-853).
    Q: [B][H_q][t][D] in the cache dtype, t = 1 + staged (implicit).  Query
@@ -119,6 +129,15 @@ int bmc_commit(bmc_t h, int n_accepted);
 
 /* bmc_commit_rows: per-row acceptance, n_accepted_host[B] (host array). */
 int bmc_commit_rows(bmc_t h, const int* n_accepted_host);
+
+/* bmc_commit_path: commit one accepted root-to-node path per batch row
+   (P:L447): path_host[b * max_depth + i], i < m_host[b], node
+   indices of increasing depth (path[0] a root, path[i] a child of
+   path[i-1]; for chain drafts the path 0..n-1).  The accepted rows are
+   moved to valid_b .. valid_b + m_b - 1, every other staged row is zeroed,
+   valid_b += m_b.  Chain commits (bmc_commit*) of a staged tree are a STATE
+   error unless they reject everything. */
+int bmc_commit_path(bmc_t h, const int* path_host, const int* m_host, int max_depth);
 
 /* bmc_decode_step: one plain decode step of a whole model, i.e. for every
    layer l = 0..L-1: bmc_append(hs[l], K[l], V[l]) then

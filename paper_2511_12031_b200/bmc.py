@@ -34,7 +34,8 @@ _NAMES = {0: "OK", -1: "ARG", -2: "STATE", -3: "CAPACITY", -4: "OOM", -5: "CUDA"
           -6: "UNSUPPORTED"}
 
 EXPORTS = ["bmc_create", "bmc_create_ex", "bmc_append", "bmc_spec_write", "bmc_sdpa",
-           "bmc_commit", "bmc_commit_rows", "bmc_decode_step", "bmc_destroy", "bmc_stats", "bmc_kv_view",
+           "bmc_commit", "bmc_commit_rows", "bmc_commit_path", "bmc_spec_write_tree",
+           "bmc_decode_step", "bmc_destroy", "bmc_stats", "bmc_kv_view",
            "bmc_valid", "bmc_read_cache", "bmc_sync", "bmc_set_option", "bmc_launch_count", "bmc_last_error"]
 
 
@@ -75,6 +76,8 @@ def load(path: str = SO_PATH):
     L.bmc_commit.argtypes = [vp, i]
     L.bmc_commit_rows.argtypes = [vp, ctypes.POINTER(ctypes.c_int)]
     L.bmc_destroy.argtypes = [vp]
+    L.bmc_spec_write_tree.argtypes = [vp, vp, vp, i, ctypes.POINTER(ctypes.c_int)]
+    L.bmc_commit_path.argtypes = [vp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int), i]
     L.bmc_decode_step.argtypes = [vp, i, vp, vp, vp, vp, i]
     L.bmc_stats.argtypes = [vp, ctypes.POINTER(Stats)]
     L.bmc_kv_view.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(i)]
@@ -163,6 +166,24 @@ def bmc_decode_step(plan: StepPlan, K, V, Q, O, n_valid: int) -> int:
                   "bmc_decode_step")
 
 
+def bmc_spec_write_tree(h, K_draft, V_draft, k: int, parent) -> int:
+    par = (ctypes.c_int * max(1, k))(*[int(x) for x in parent])
+    return _check(load().bmc_spec_write_tree(h, _ptr(K_draft), _ptr(V_draft), k, par),
+                  "bmc_spec_write_tree")
+
+
+def bmc_commit_path(h, paths) -> int:
+    """paths: one list of node indices (root first) per batch row."""
+    depth = max([len(p) for p in paths] + [1])
+    flat = (ctypes.c_int * (len(paths) * depth))()
+    m = (ctypes.c_int * len(paths))()
+    for b, pth in enumerate(paths):
+        m[b] = len(pth)
+        for i, x in enumerate(pth):
+            flat[b * depth + i] = int(x)
+    return _check(load().bmc_commit_path(h, flat, m, depth), "bmc_commit_path")
+
+
 def bmc_destroy(h) -> int:
     return _check(load().bmc_destroy(h), "bmc_destroy")
 
@@ -237,6 +258,16 @@ class KVCache:
     def spec_write(self, Kd, Vd, k):
         rc = bmc_spec_write(self.h, Kd, Vd, k)
         self._keep = self._keep + (Kd, Vd)
+        return rc
+
+    def spec_write_tree(self, Kd, Vd, k, parent):
+        rc = bmc_spec_write_tree(self.h, Kd, Vd, k, parent)
+        self._keep = self._keep + (Kd, Vd)
+        return rc
+
+    def commit_path(self, paths):
+        rc = bmc_commit_path(self.h, paths)
+        self._keep = ()
         return rc
 
     def sdpa(self, Q, n_valid, O=None):

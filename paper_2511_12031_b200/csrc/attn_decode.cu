@@ -140,6 +140,8 @@ struct Params {
   int m0;                 // first query row of the unit handled by this launch
   int ctas;
   float qscale;           // log2(e) / sqrt(D)
+  int tree;               // staged rows form a token tree (else a chain)
+  uint32_t anc[32];       // tree: bit j of anc[i] = node j is node i or its ancestor
   int valid[BMC_MAX_B];   // committed rows per batch row (incl. a pending append)
   LayerDesc layer[MAXL];
 };
@@ -269,6 +271,7 @@ __global__ void __launch_bounds__(kThreads, CTAS) attn_step_kernel(const __grid_
   float2 o2[MAXM][C::EL2];
   float mw[MAXM], lsum[MAXM];
   int nvis[MAXM];
+  uint32_t qmask[MAXM];            // tree: visible staged rows (bit j = row valid_b + j)
   int max_vis = 0;
   bool seg_first = true;
   bool seg_start = true;
@@ -296,14 +299,19 @@ __global__ void __launch_bounds__(kThreads, CTAS) attn_step_kernel(const __grid_
         mw[m] = -INFINITY;
         lsum[m] = 0.f;
         nvis[m] = 0;
+        qmask[m] = 0;
 #pragma unroll
         for (int e = 0; e < C::EL2; ++e) {
           o2[m][e] = make_float2(0.f, 0.f);
           q2[m][e] = make_float2(0.f, 0.f);
         }
         if (m < p.M) {
-          nvis[m] = vb + (p.m0 + m) % p.t;
-          max_vis = max(max_vis, nvis[m]);
+          // chain (reading R7): rows [0, valid_b + tau); token tree:
+          // the committed rows plus the node's ancestors and itself
+          const int tau = (p.m0 + m) % p.t;
+          nvis[m] = p.tree ? vb : vb + tau;
+          qmask[m] = (p.tree && tau > 0) ? p.anc[tau - 1] : 0u;
+          max_vis = max(max_vis, vb + tau);
 #pragma unroll
           for (int c = 0; c < CPL; ++c) {
             const uint4 raw =
@@ -408,7 +416,10 @@ __global__ void __launch_bounds__(kThreads, CTAS) attn_step_kernel(const __grid_
 #pragma unroll
           for (int ps = 0; ps < C::PASSES; ++ps) {
             const long long jr = row0 + warp * C::RPW + ps * C::RPP + rip;
-            if (jr >= nvis[m]) sc[ps][m] = -INFINITY;
+            const long long js = jr - vb;       // index among the staged rows
+            const bool vis = jr < nvis[m] ||
+                             (js >= 0 && js < 32 && ((qmask[m] >> (js & 31)) & 1u));
+            if (!vis) sc[ps][m] = -INFINITY;
             mt = fmaxf(mt, sc[ps][m]);
           }
 #pragma unroll
@@ -616,6 +627,8 @@ cudaError_t launch_chunk(const AttnStepArgs& a, int l0, int nl, int num_sms, cud
   prm.t = a.t;
   prm.ctas = a.ctas;
   prm.qscale = kLog2e / sqrtf((float)a.D);
+  prm.tree = a.tree;
+  for (int i = 0; i < 32; ++i) prm.anc[i] = a.anc[i];
   for (int b = 0; b < a.B; ++b) prm.valid[b] = a.valid[b];
   long long tiles = 0;
   for (int i = 0; i < nl; ++i) {

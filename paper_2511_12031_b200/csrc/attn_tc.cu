@@ -93,6 +93,8 @@ struct Params {
   long long total_tiles;
   int tpu, U, H_kv, H_q, G, t, M, ctas;
   float qscale;
+  int tree;                 // staged rows form a token tree (else a chain)
+  uint32_t anc[32];         // tree: bit j of anc[i] = node j is node i or its ancestor
   int valid[BMC_MAX_B];
 };
 
@@ -495,7 +497,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_arrive(QFULL);
-      const int nvis = active ? p.valid[b_] + (row % p.t) : 0;
+      // chain (reading R7): keys [0, valid_b + tau); token tree:
+      // the committed keys plus the node's ancestors and itself
+      const int vb_ = p.valid[b_];
+      const int tau = row % p.t;
+      const int nvis = active ? (p.tree ? vb_ : vb_ + tau) : 0;
+      const uint32_t qmask = (active && p.tree && tau > 0) ? p.anc[tau - 1] : 0u;
       float m_use = -INFINITY, l = 0.f;   // l: this thread's half of the row sum
       const int n = (int)(iend - i);
       for (int k = 0; k < n; ++k) {
@@ -517,7 +524,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
           } else {
 #pragma unroll
             for (int c = 0; c < 32; ++c) {
-              sv[c] = (key0 + c < nvis) ? sv[c] : -INFINITY;
+              const long long js = key0 + c - vb_;      // index among the staged rows
+              const bool vis = key0 + c < nvis ||
+                               (js >= 0 && js < 32 && ((qmask >> (js & 31)) & 1u));
+              sv[c] = vis ? sv[c] : -INFINITY;
               mt = fmaxf(mt, sv[c]);
             }
           }
@@ -743,6 +753,8 @@ cudaError_t launch_attn_tc(const AttnStepArgs& a, int num_sms, cudaStream_t s) {
   p.t = a.t;
   p.M = p.G * a.t;
   p.qscale = tc::kLog2e / sqrtf((float)tc::D);
+  p.tree = a.tree;
+  for (int i = 0; i < 32; ++i) p.anc[i] = a.anc[i];
   for (int b = 0; b < a.B; ++b) p.valid[b] = a.valid[b];
   int ctas = a.ctas > 0 ? a.ctas : num_sms;
   if (ctas > p.total_tiles) ctas = (int)p.total_tiles;

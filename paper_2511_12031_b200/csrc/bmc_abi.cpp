@@ -63,6 +63,8 @@ struct bmc_ctx {
   const void* kd = nullptr;
   const void* vd = nullptr;
   int n_app = 0, n_draft = 0, kd_stride = 0;
+  int tree = 0;                  // staged rows form a token tree
+  uint32_t anc[32] = {};         // bit j of anc[i]: node j is node i or its ancestor
   struct Pipe* pipe = nullptr;   // host-I/O pipeline of bmc_decode_step (first layer owns it)
 };
 
@@ -288,6 +290,8 @@ static void fill_args(bmc_t h, int t, bmc::AttnStepArgs* a) {
   a->t = t;
   a->dtype = h->dt;
   a->ctas = std::min(h->attn_ctas, h->max_ctas);
+  a->tree = h->tree;
+  for (int i = 0; i < 32; ++i) a->anc[i] = h->anc[i];
   for (int b = 0; b < h->B; ++b) a->valid[b] = h->valid[b];
 }
 
@@ -430,6 +434,26 @@ int bmc_spec_write(bmc_t h, const void* K_draft, const void* V_draft, int k) {
     h->st.append_written_bytes += 2LL * h->U * k_adm * h->row_bytes;
   }
   h->staged = k_adm;
+  return k_adm;
+}
+
+int bmc_spec_write_tree(bmc_t h, const void* K_draft, const void* V_draft, int k,
+                        const int* parent_host) {
+  int rc = enter(h);
+  if (rc) return rc;
+  if (k < 0) return fail(BMC_ERR_ARG, "k=%d < 0", k);
+  if (k > 32) return fail(BMC_ERR_UNSUPPORTED, "token trees of more than 32 nodes");
+  if (k > 0 && !parent_host) return fail(BMC_ERR_ARG, "parent is null");
+  for (int i = 0; i < k; ++i)
+    if (parent_host[i] < -1 || parent_host[i] >= i)
+      return fail(BMC_ERR_ARG, "parent[%d]=%d not in [-1, %d) (breadth-first order)", i,
+                  parent_host[i], i);
+  const int k_adm = bmc_spec_write(h, K_draft, V_draft, k);
+  if (k_adm < 0) return k_adm;
+  for (int i = 0; i < 32; ++i) h->anc[i] = 0;
+  for (int i = 0; i < k_adm; ++i)
+    h->anc[i] = (1u << i) | (parent_host[i] >= 0 ? h->anc[parent_host[i]] : 0u);
+  h->tree = k_adm > 0;
   return k_adm;
 }
 
@@ -678,6 +702,49 @@ static int commit_impl(bmc_t h, const int* m) {
   if (z.max_rows > 0) CK(h, bmc::launch_zero_rows(z, h->stream), "zero_rows");
   for (int b = 0; b < h->B; ++b) h->valid[b] += m[b];
   h->staged = 0;
+  h->tree = 0;
+  return 0;
+}
+
+int bmc_commit_path(bmc_t h, const int* path_host, const int* m_host, int max_depth) {
+  int rc = enter(h);
+  if (rc) return rc;
+  if (!m_host || max_depth < 0) return fail(BMC_ERR_ARG, "null argument");
+  for (int b = 0; b < h->B; ++b) {
+    const int m = m_host[b];
+    if (m < 0 || m > max_depth || m > h->staged || m > 32)
+      return fail(BMC_ERR_ARG, "path length %d of row %d invalid (staged %d)", m, b, h->staged);
+    if (m > 0 && !path_host) return fail(BMC_ERR_ARG, "null path");
+    for (int i = 0; i < m; ++i) {
+      const int x = path_host[b * max_depth + i];
+      if (x < 0 || x >= h->staged) return fail(BMC_ERR_ARG, "path node %d out of range", x);
+      const int par = h->tree ? (int)(31 - __builtin_clz(h->anc[x] & ~(1u << x) | 1u)) : x - 1;
+      const int has_par = h->tree ? ((h->anc[x] & ~(1u << x)) != 0) : (x > 0);
+      const int want = i == 0 ? -1 : path_host[b * max_depth + i - 1];
+      if ((has_par ? par : -1) != want) return fail(BMC_ERR_ARG, "row %d: path is not parent-linked", b);
+    }
+  }
+  if (h->n_app || h->n_draft) {
+    rc = flush_pending(h);
+    if (rc) return rc;
+  }
+  bmc::PathArgs a;
+  a.k = h->kbuf.ptr;
+  a.v = h->vbuf.ptr;
+  a.B = h->B;
+  a.H_kv = h->H_kv;
+  a.staged = h->staged;
+  a.cap = h->cap;
+  a.row_bytes = h->row_bytes;
+  for (int b = 0; b < h->B; ++b) {
+    a.valid[b] = h->valid[b];
+    a.m[b] = (unsigned char)m_host[b];
+    for (int i = 0; i < m_host[b]; ++i) a.path[b][i] = (unsigned char)path_host[b * max_depth + i];
+  }
+  CK(h, bmc::launch_commit_path(a, h->stream), "commit_path");
+  for (int b = 0; b < h->B; ++b) h->valid[b] += m_host[b];
+  h->staged = 0;
+  h->tree = 0;
   return 0;
 }
 
@@ -687,6 +754,8 @@ int bmc_commit(bmc_t h, int n_accepted) {
   if (h->staged == 0 && n_accepted > 0) return fail(BMC_ERR_STATE, "nothing staged");
   if (n_accepted < 0 || n_accepted > h->staged)
     return fail(BMC_ERR_ARG, "n_accepted=%d outside [0, %d]", n_accepted, h->staged);
+  if (h->tree && n_accepted > 0)
+    return fail(BMC_ERR_STATE, "a staged token tree is committed with bmc_commit_path");
   std::vector<int> m(h->B, n_accepted);
   return commit_impl(h, m.data());
 }
@@ -700,6 +769,8 @@ int bmc_commit_rows(bmc_t h, const int* n_accepted_host) {
     if (n_accepted_host[b] < 0 || n_accepted_host[b] > h->staged)
       return fail(BMC_ERR_ARG, "n_accepted[%d]=%d outside [0, %d]", b, n_accepted_host[b],
                   h->staged);
+    if (h->tree && n_accepted_host[b] > 0)
+      return fail(BMC_ERR_STATE, "a staged token tree is committed with bmc_commit_path");
   }
   return commit_impl(h, n_accepted_host);
 }

@@ -43,6 +43,19 @@ struct ZeroArgs {
 };
 cudaError_t launch_zero_rows(const ZeroArgs& a, cudaStream_t s);
 
+struct PathArgs {
+  void* k; void* v;                       // [U][cap][D]
+  int B, H_kv, staged;
+  long long cap;
+  int row_bytes;
+  int valid[BMC_MAX_B];                   // committed rows before the commit
+  unsigned char m[BMC_MAX_B];             // accepted path length per batch row
+  unsigned char path[BMC_MAX_B][32];      // accepted node indices, root first
+};
+// Compact the accepted tree path of every unit behind its committed rows and
+// zero the remaining staged rows (one warp per (unit, tensor)).
+cudaError_t launch_commit_path(const PathArgs& a, cudaStream_t s);
+
 // One layer of an attention launch.
 struct AttnLayer {
   const void* K; const void* V;           // cache [U][cap][D]
@@ -60,6 +73,8 @@ constexpr int kMaxLayersPerLaunch = 32;
 struct AttnStepArgs {
   int B, H_kv, H_q, D, t, dtype;
   int ctas;                               // 0 = auto
+  int tree;                               // staged rows form a token tree
+  uint32_t anc[32];                       // tree: bit j of anc[i] = node j is i or an ancestor
   int valid[BMC_MAX_B];                   // committed rows incl. the pending append
   int L;
   const AttnLayer* layers;

@@ -134,4 +134,32 @@ cudaError_t launch_zero_rows(const ZeroArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// One warp per (unit, tensor): rows are moved in depth order (path[i] >= i,
+// so no destination is a row still to be read), then the rest is zeroed.
+__global__ void commit_path_kernel(const __grid_constant__ PathArgs a) {
+  const long long u = blockIdx.x;
+  const int tensor = blockIdx.y;
+  const int b = (int)(u / a.H_kv);
+  const int lane = threadIdx.x;
+  const int row_vec = a.row_bytes / 16;
+  int4* base = (int4*)(tensor == 0 ? a.k : a.v) + (u * a.cap + a.valid[b]) * row_vec;
+  const int m = a.m[b];
+  for (int i = 0; i < m; ++i) {
+    const int src = a.path[b][i];
+    if (src != i)
+      for (int c = lane; c < row_vec; c += 32) base[(long long)i * row_vec + c] = base[(long long)src * row_vec + c];
+    __syncwarp();
+  }
+  for (int x = lane; x < (a.staged - m) * row_vec; x += 32)
+    base[(long long)m * row_vec + x] = make_int4(0, 0, 0, 0);
+}
+
+cudaError_t launch_commit_path(const PathArgs& a, cudaStream_t s) {
+  const long long U = (long long)a.B * a.H_kv;
+  if (U == 0 || a.staged == 0) return cudaSuccess;
+  commit_path_kernel<<<dim3((unsigned)U, 2), 32, 0, s>>>(a);
+  count_launch();
+  return cudaGetLastError();
+}
+
 }  // namespace bmc

@@ -66,6 +66,20 @@ class Pair:
         assert a == b, (a, b)
         return a
 
+    def spec_write_tree(self, k, parent):
+        x = synth.step_inputs(self.seed, self.layer, self.step, B=self.B, H_kv=self.H_kv,
+                              H_q=self.H_q, D=self.D, dtype=self.dtype, k_draft=k,
+                              want=("kd", "vd"))
+        self.step += 1
+        a = self.gpu.spec_write_tree(self._dev(x["kd"]), self._dev(x["vd"]), k, parent)
+        b = self.orc.spec_write_tree(x["kd"], x["vd"], k, parent)
+        assert a == b, (a, b)
+        return a
+
+    def commit_path(self, paths):
+        self.gpu.commit_path(paths)
+        self.orc.commit_path(paths)
+
     def sdpa(self, n_valid=None):
         st = self.orc.stats()
         t = 1 + st["staged"]

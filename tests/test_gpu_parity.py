@@ -224,3 +224,60 @@ def test_length_aware_ablation(path, policy):
         p.commit_rows(synth.acceptance(31, it, 2, k))
     p.check_state()
     p.close()
+
+
+def _random_tree(rng, k):
+    return [-1] + [int(rng.integers(-1, i)) for i in range(1, k)]
+
+
+def _random_path(rng, parent, k_adm):
+    """A root-to-node path among the admitted nodes (possibly empty)."""
+    if k_adm == 0 or rng.random() < 0.15:
+        return []
+    node = int(rng.integers(0, k_adm))
+    path = []
+    while node >= 0:
+        path.append(node)
+        node = parent[node]
+    return path[::-1][: int(rng.integers(1, len(path) + 1))]
+
+
+@pytest.mark.parametrize("path,H_kv,H_q,k", [(1, 2, 2, 6), (2, 2, 2, 6), (2, 2, 8, 12),
+                                             (1, 1, 4, 26), (2, 1, 4, 26)])
+def test_token_tree_speculation(path, H_kv, H_q, k):
+    """Token-tree speculation: nodes in BFS order in the padded
+    rows, ancestor-rule mask in both attention kernels (CUDA cores: path 1,
+    tcgen05: path 2), per-row accepted paths compacted on commit; every
+    output row and the final cache against the oracle."""
+    rng = np.random.default_rng(7 * k + path)
+    p = Pair(3, H_kv, H_q, 128, 32, 600, dtype="bf16", seed=37 + k)
+    p.gpu.set_option(bmc.BMC_OPT_ATTN_PATH, path)
+    for _ in range(4):
+        p.append()
+    p.sdpa()
+    it = 0
+    while p.orc.stats()["valid_max"] < 560 and it < 45:
+        p.append()
+        parent = _random_tree(rng, k)
+        k_adm = p.spec_write_tree(k, parent)
+        p.sdpa(n_valid=-1)
+        p.commit_path([_random_path(rng, parent, k_adm) for _ in range(3)])
+        it += 1
+        if it % 15 == 0:
+            p.check_state()
+    p.check_state()
+    p.close()
+
+
+def test_token_tree_paper_example_gpu():
+    """The figure's 4-node tree on the GPU: 7 -> 3 -> 1 -> 0 wasted rows."""
+    p = Pair(1, 1, 1, 128, 8, 64, dtype="bf16", seed=41)
+    p.append()
+    for wasted, pth in [(3, [0, 2]), (1, [0]), (0, [])]:
+        assert p.spec_write_tree(4, [-1, 0, 0, 1]) == 4
+        s = p.gpu.stats()
+        assert s["capacity"] - s["valid_max"] - s["staged"] == wasted
+        p.sdpa()
+        p.commit_path([pth])
+    p.check_state()
+    p.close()
