@@ -53,8 +53,9 @@ namespace tc {
 constexpr int D = 128;            // head dim (bf16)
 constexpr int KT = 64;            // keys per tile
 constexpr int MM = 128;           // MMA M (query rows, padded)
-constexpr int KS = 4;             // K ring stages (released right after Q.K^T)
-constexpr int VS = 4;             // V ring stages (released after P.V)
+constexpr int KS = 3;             // K ring stages (released right after Q.K^T)
+constexpr int VS = 5;             // V ring stages (held until P.V completes: deeper)
+constexpr int NB = 2;             // S (TMEM) and P (smem) buffers: tiles in flight
 constexpr int kThreads = 384;     // 12 warps: K/V producers, QK / PV issuers, 2 x 4 softmax
 constexpr uint32_t kTileBytes = KT * D * 2;            // 16 KiB per tensor per tile
 constexpr uint32_t kBox = 64 * KT * 2;                 // one 64-col box: 8 KiB
@@ -66,12 +67,12 @@ constexpr float kRescale = 8.0f;  // lazy-rescale threshold (log2 units)
 
 // shared memory map (bytes, 1024-aligned blocks)
 constexpr uint32_t OFF_Q = 0;                                  // [2 atoms][128 rows][128 B]
-constexpr uint32_t OFF_P = OFF_Q + MM * D * 2;                 // [2 buf][hi,lo][128 rows][128 B]
+constexpr uint32_t OFF_P = OFF_Q + MM * D * 2;                 // [NB buf][hi,lo][128 rows][128 B]
 constexpr uint32_t P_BYTES = MM * KT * 2;                      // 16 KiB
-constexpr uint32_t OFF_K = OFF_P + 4 * P_BYTES;                // [stage][2 boxes][64][128 B]
+constexpr uint32_t OFF_K = OFF_P + 2 * NB * P_BYTES;           // [stage][2 boxes][64][128 B]
 constexpr uint32_t OFF_V = OFF_K + KS * kTileBytes;
 constexpr uint32_t OFF_BAR = OFF_V + VS * kTileBytes;
-constexpr uint32_t OFF_X = OFF_BAR + 256;                      // [2 parity][2 halves][128] f32
+constexpr uint32_t OFF_X = OFF_BAR + 512;                      // [2 parity][2 halves][128] f32
 constexpr uint32_t kSmem = OFF_X + 2048;   // the dynamic window starts 1024-aligned (checked)
 static_assert(kSmem <= 232448, "shared memory");
 
@@ -279,18 +280,18 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
   const uint32_t bar0 = sbase + OFF_BAR;
   // mbarriers (8 bytes each)
   auto FULLK = [&](int s) { return bar0 + 8u * s; };               // TMA -> MMA
-  auto EMPTYK = [&](int s) { return bar0 + 8u * (4 + s); };        // MMA -> TMA
-  auto FULLV = [&](int s) { return bar0 + 8u * (8 + s); };
-  auto EMPTYV = [&](int s) { return bar0 + 8u * (12 + s); };
-  auto SFULL = [&](int b) { return bar0 + 8u * (16 + b); };        // MMA -> softmax
-  auto SEMPTY = [&](int b) { return bar0 + 8u * (18 + b); };       // softmax -> MMA
-  auto PFULL = [&](int b) { return bar0 + 8u * (20 + b); };        // softmax -> MMA
-  auto PEMPTY = [&](int b) { return bar0 + 8u * (22 + b); };       // MMA -> softmax
-  const uint32_t QFULL = bar0 + 8u * 24;                           // softmax -> MMA
-  const uint32_t ODONE = bar0 + 8u * 25;                           // PV issuer -> softmax
-  const uint32_t QDONE = bar0 + 8u * 26;                           // QK issuer -> softmax
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + OFF_BAR + 8 * 27);
-  int* sm_flag = reinterpret_cast<int*>(smem + OFF_BAR + 8 * 27 + 8);
+  auto EMPTYK = [&](int s) { return bar0 + 8u * (6 + s); };        // MMA -> TMA
+  auto FULLV = [&](int s) { return bar0 + 8u * (12 + s); };
+  auto EMPTYV = [&](int s) { return bar0 + 8u * (24 + s); };
+  auto SFULL = [&](int b) { return bar0 + 8u * (36 + b); };        // MMA -> softmax
+  auto SEMPTY = [&](int b) { return bar0 + 8u * (40 + b); };       // softmax -> MMA
+  auto PFULL = [&](int b) { return bar0 + 8u * (44 + b); };        // softmax -> MMA
+  auto PEMPTY = [&](int b) { return bar0 + 8u * (48 + b); };       // MMA -> softmax
+  const uint32_t QFULL = bar0 + 8u * 52;                           // softmax -> MMA
+  const uint32_t ODONE = bar0 + 8u * 53;                           // PV issuer -> softmax
+  const uint32_t QDONE = bar0 + 8u * 54;                           // QK issuer -> softmax
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + OFF_BAR + 8 * 55);
+  int* sm_flag = reinterpret_cast<int*>(smem + OFF_BAR + 8 * 55 + 8);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -307,7 +308,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
       mbar_init(FULLV(s), 1);
       mbar_init(EMPTYV(s), 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NB; ++b) {
       mbar_init(SFULL(b), 1);
       mbar_init(SEMPTY(b), 256);
       mbar_init(PFULL(b), 256);
@@ -319,7 +320,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
                      su32(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
@@ -361,7 +362,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
   __syncthreads();
   fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tO = tmem + 128;
+  const uint32_t tO = tmem + 256;      // S buffers use columns [0, 64*NB)
 
   if (warp == 0 || warp == 10) {
     // ------------------------------------------------------ TMA producers
@@ -392,7 +393,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
     if (lane == 0) {
       constexpr uint32_t IQK = idesc_bf16(MM, KT, 0);   // S = Q K^T, B K-major
       int ks = 0;
-      uint32_t kph = 0, sph = 0, qph = 0;
+      uint32_t kph = 0, qph = 0;
       long long i = t_begin;
       int tcount = 0;                 // tiles of this CTA so far (S buffer index)
       while (i < t_end) {
@@ -403,10 +404,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
         fence_after();
         const int n = (int)(iend - i);
         for (int k = 0; k < n; ++k) {
-          const int b = (tcount + k) & 1;
+          // tile c uses buffer c % NB for the (c / NB)-th time: every phase
+          // parity follows from the CTA's tile counter
+          const int tc = tcount + k;
+          const int b = tc % NB;
           mbar_wait(FULLK(ks), kph);
-          mbar_wait(SEMPTY(b), ((sph >> b) & 1) ^ 1);
-          sph ^= 1u << b;
+          mbar_wait(SEMPTY(b), ((tc / NB) & 1) ^ 1);   // released by its previous use
           fence_after();
           const uint32_t kt = sbase + OFF_K + ks * kTileBytes;
           const uint32_t tS = tmem + 64 * b;
@@ -430,7 +433,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
     if (lane == 0) {
       constexpr uint32_t IPV = idesc_bf16(MM, D, 1);    // O += P V, B MN-major
       int vs = 0;
-      uint32_t vph = 0, pph = 0;
+      uint32_t vph = 0;
       long long i = t_begin;
       int tcount = 0;
       while (i < t_end) {
@@ -438,9 +441,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
         const long long iend = min(t_end, (u + 1) * p.tpu);
         const int n = (int)(iend - i);
         for (int k = 0; k < n; ++k) {
-          const int b = (tcount + k) & 1;
-          mbar_wait(PFULL(b), (pph >> b) & 1);
-          pph ^= 1u << b;
+          const int tc = tcount + k;
+          const int b = tc % NB;
+          mbar_wait(PFULL(b), (tc / NB) & 1);
           mbar_wait(FULLV(vs), vph);
           fence_after();
           const uint32_t vt = sbase + OFF_V + vs * kTileBytes;
@@ -473,8 +476,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
     const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
     const int stid = threadIdx.x - 64;  // 0..255
     float* xch = reinterpret_cast<float*>(smem + OFF_X);   // [2][128]
-    uint32_t sph = 0, oph = 0, qdph = 0;
-    uint32_t puse0 = 0, puse1 = 0;      // tiles that have used P buffer 0 / 1
+    uint32_t oph = 0, qdph = 0;
     long long i = t_begin;
     int tcount = 0;
     bool first_item = true;
@@ -506,10 +508,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
       float m_use = -INFINITY, l = 0.f;   // l: this thread's half of the row sum
       const int n = (int)(iend - i);
       for (int k = 0; k < n; ++k) {
-        const int bb = (tcount + k) & 1;
+        const int tc = tcount + k;          // this CTA's tile counter
+        const int bb = tc % NB;
         const long long key0 = (long long)(j0 + k) * KT + half * 32;
-        mbar_wait(SFULL(bb), (sph >> bb) & 1);
-        sph ^= 1u << bb;
+        mbar_wait(SFULL(bb), (tc / NB) & 1);
         fence_after();
         float sv[32];
         tmem_ld32(tmem + 64 * bb + half * 32 + lane_addr, sv);
@@ -519,8 +521,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
         float mt = -INFINITY;
         if (active) {
           if (key0 + 32 <= nvis) {          // fully visible half tile: no mask
+            float m4[4] = {sv[0], sv[1], sv[2], sv[3]};   // 4 independent chains
 #pragma unroll
-            for (int c = 0; c < 32; ++c) mt = fmaxf(mt, sv[c]);
+            for (int c = 4; c < 32; ++c) m4[c & 3] = fmaxf(m4[c & 3], sv[c]);
+            mt = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
           } else {
 #pragma unroll
             for (int c = 0; c < 32; ++c) {
@@ -538,10 +542,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
         xk[half * 128 + row] = mt;
         pair_sync();
         mt = fmaxf(mt, xk[(half ^ 1) * 128 + row]) * p.qscale;
-        // P buffer bb was last read by the PV of the tile two back: the c-th
+        // P buffer bb was last read by the PV of tile tc - NB: the c-th
         // completion of PEMPTY(bb) belongs to the c-th tile using bb
-        const uint32_t pu = bb ? puse1 : puse0;
-        if (pu >= 1) mbar_wait(PEMPTY(bb), (pu - 1) & 1);
+        if (tc >= NB) mbar_wait(PEMPTY(bb), ((tc / NB) - 1) & 1);
         // lazy rescale: keep the old max unless the new one exceeds it by > 8
         // (both threads of a row take the same decision from the same values)
         bool rescale = false;
@@ -554,8 +557,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
         }
         // O must not be written by PV(k-1) while it is rescaled
         if (__any_sync(0xffffffffu, rescale)) {
-          const uint32_t pp = bb ? puse0 : puse1;   // buffer of the previous tile
-          mbar_wait(PEMPTY(bb ^ 1), (pp - 1) & 1);  // its PV has completed
+          const int tp = tc - 1;                    // the previous tile's PV has completed
+          mbar_wait(PEMPTY(tp % NB), (tp / NB) & 1);
           fence_after();
 #pragma unroll 1
           for (int h = 0; h < 2; ++h) {
@@ -576,7 +579,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
         if (active) {
           const bool none = (m_use == -INFINITY);
           const float nm = -m_use;
-          float2 ts2 = make_float2(0.f, 0.f);
+          float2 ts2a = make_float2(0.f, 0.f), ts2b = make_float2(0.f, 0.f);
 #pragma unroll
           for (int c8 = 0; c8 < 4; ++c8) {
             uint32_t hw[4], lw[4];
@@ -586,7 +589,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
               const float p1 =
                   none ? 0.f : fast_exp2(fmaf(sv[c8 * 8 + 2 * e + 1], p.qscale, nm));
               const float2 pp2 = make_float2(p0, p1);
-              ts2 = __fadd2_rn(ts2, pp2);
+              if (e & 1) ts2b = __fadd2_rn(ts2b, pp2); else ts2a = __fadd2_rn(ts2a, pp2);
               const __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
               const float2 hf = __bfloat1622float2(h2);
               const float2 lo = __ffma2_rn(hf, make_float2(-1.f, -1.f), pp2);
@@ -598,11 +601,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
             *reinterpret_cast<uint4*>(phi + sw128(row, ck)) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
             *reinterpret_cast<uint4*>(plo + sw128(row, ck)) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
           }
-          l += ts2.x + ts2.y;
+          l += (ts2a.x + ts2b.x) + (ts2a.y + ts2b.y);
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_arrive(PFULL(bb));
-        if (bb) ++puse1; else ++puse0;
       }
       // ---- epilogue of this item: O (TMEM) -> output or partial record
       float* xl = xch + ((tcount + n) & 1) * 256;   // the parity no tile reads now
@@ -669,7 +671,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
   __syncthreads();
   fence_after();
   if (warp == 1) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }
 }
 
