@@ -53,9 +53,9 @@ namespace tc {
 constexpr int D = 128;            // head dim (bf16)
 constexpr int KT = 64;            // keys per tile
 constexpr int MM = 128;           // MMA M (query rows, padded)
-constexpr int KS = 3;             // K ring stages (released right after Q.K^T)
-constexpr int VS = 5;             // V ring stages (held until P.V completes: deeper)
-constexpr int NB = 2;             // S (TMEM) and P (smem) buffers: tiles in flight
+constexpr int KS = 6;             // K ring stages (released right after Q.K^T)
+constexpr int VS = 7;             // V ring stages (held until P.V completes: deeper)
+constexpr int NB = 2;             // S and P buffers (tiles in flight)
 constexpr int kThreads = 384;     // 12 warps: K/V producers, QK / PV issuers, 2 x 4 softmax
 constexpr uint32_t kTileBytes = KT * D * 2;            // 16 KiB per tensor per tile
 constexpr uint32_t kBox = 64 * KT * 2;                 // one 64-col box: 8 KiB
@@ -65,16 +65,43 @@ constexpr float kRescale = 8.0f;  // lazy-rescale threshold (log2 units)
 #define BMC_TC_HALVES 2           // P.V issued for P_hi and P_lo
 #endif
 
-// shared memory map (bytes, 1024-aligned blocks)
-constexpr uint32_t OFF_Q = 0;                                  // [2 atoms][128 rows][128 B]
-constexpr uint32_t OFF_P = OFF_Q + MM * D * 2;                 // [NB buf][hi,lo][128 rows][128 B]
-constexpr uint32_t P_BYTES = MM * KT * 2;                      // 16 KiB
-constexpr uint32_t OFF_K = OFF_P + 2 * NB * P_BYTES;           // [stage][2 boxes][64][128 B]
+// Tensor memory (512 columns x 128 lanes x 32 bit):
+constexpr uint32_t TM_S = 0;      // S[b]: 64 fp32 columns each (b < NB)
+constexpr uint32_t TM_O = 128;    // O: 128 fp32 columns
+constexpr uint32_t TM_Q = 256;    // Q: 128 bf16 = 64 packed columns (MMA A operand)
+constexpr uint32_t TM_P = 320;    // P[b][hi|lo]: 64 bf16 = 32 packed columns each
+// Shared memory holds only the K and V rings: the MMA A operands (Q, P) are
+// read from TMEM, so per 64-key tile the tensor core reads just K (16 KiB) and
+// V (2 x 16 KiB) from shared memory instead of also Q (32 KiB) and P (32 KiB).
+constexpr uint32_t OFF_K = 0;                                  // [stage][2 boxes][64][128 B]
 constexpr uint32_t OFF_V = OFF_K + KS * kTileBytes;
 constexpr uint32_t OFF_BAR = OFF_V + VS * kTileBytes;
 constexpr uint32_t OFF_X = OFF_BAR + 512;                      // [2 parity][2 halves][128] f32
 constexpr uint32_t kSmem = OFF_X + 2048;   // the dynamic window starts 1024-aligned (checked)
 static_assert(kSmem <= 232448, "shared memory");
+
+#ifdef BMC_TC_TRACE
+// Debug timeline (CTA 0 only): trace[event][tile] = clock64 at that point.
+__device__ long long g_tc_trace[16][256];
+__device__ long long g_tc_mma[2][256][9];
+__device__ long long g_tc_sm[8][256][4];
+__device__ long long g_tc_cta[160][4];   // per CTA: clock64 / globaltimer at entry and exit
+__device__ __forceinline__ long long gtime() {
+  long long c;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(c));
+  return c;
+}    // per softmax warp: S ready, pair, Pempty, Pfull
+#define TRACE_W(ev, i) do { if (blockIdx.x == 0 && lane == 0 && (i) < 256) g_tc_sm[warp - 2][i][ev] = clk(); } while (0)   // per issuer, per tile: before each MMA + after last
+__device__ __forceinline__ long long clk() {
+  long long c;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+  return c;
+}
+#define TRACE(ev, i) do { if (blockIdx.x == 0 && (i) < 256) g_tc_trace[ev][i] = clk(); } while (0)
+#else
+#define TRACE(ev, i) do { } while (0)
+#define TRACE_W(ev, i) do { } while (0)
+#endif
 
 struct Params {
   CUtensorMap tmK;   // [U*cap rows][128] bf16, box 64 x 64, SWIZZLE_128B
@@ -154,6 +181,28 @@ __device__ __forceinline__ void umma_f16(uint32_t dtmem, uint64_t adesc, uint64_
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(dtmem),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
       : "memory");
+}
+// D[tmem] (+)= A[tmem] . B[smem]  (A from tensor memory, the "TS" form)
+__device__ __forceinline__ void umma_f16_ts(uint32_t dtmem, uint32_t atmem, uint64_t bdesc,
+                                            uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(dtmem),
+      "r"(atmem), "l"(bdesc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+      "r"(r[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 __device__ __forceinline__ float fast_exp2(float x) {
   float y;
@@ -277,6 +326,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
   uint8_t* smem = smem_raw;
   const uint32_t sbase = su32(smem);
   if (sbase & 1023u) __trap();
+#ifdef BMC_TC_TRACE
+  if (threadIdx.x == 0) { g_tc_cta[blockIdx.x][0] = clk(); g_tc_cta[blockIdx.x][1] = gtime(); }
+#endif
   const uint32_t bar0 = sbase + OFF_BAR;
   // mbarriers (8 bytes each)
   auto FULLK = [&](int s) { return bar0 + 8u * s; };               // TMA -> MMA
@@ -324,10 +376,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
                      su32(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  // zero the padded rows of Q and P once (rows >= M are never written again)
-  for (uint32_t i = threadIdx.x; i < (OFF_K - OFF_Q) / 16; i += kThreads)
-    reinterpret_cast<uint4*>(smem + OFF_Q)[i] = make_uint4(0, 0, 0, 0);
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  // Rows >= M of Q and P in TMEM are never initialised: they only feed rows
+  // of S and O that are never read (each output row depends on its own A row).
   // fused KV-cache update: rows appended / drafted since the last launch that
   // fall into this CTA's tiles are stored into the cache before its TMA loads
   // read them (P:L609 in-place update), so no separate write kernel runs
@@ -362,7 +412,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
   __syncthreads();
   fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tO = tmem + 256;      // S buffers use columns [0, 64*NB)
+  const uint32_t tO = tmem + TM_O;
 
   if (warp == 0 || warp == 10) {
     // ------------------------------------------------------ TMA producers
@@ -378,6 +428,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
       int j = (int)(t_begin % p.tpu);
       for (long long i = t_begin; i < t_end; ++i) {
         mbar_wait(isK ? EMPTYK(s) : EMPTYV(s), ph ^ 1);
+        TRACE(isK ? 0 : 1, (int)(i - t_begin));
         const int row = (int)(u * p.cap + (long long)j * KT);
         const uint32_t dst = ring + s * kTileBytes;
         const uint32_t fb = isK ? FULLK(s) : FULLV(s);
@@ -409,16 +460,24 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
           const int tc = tcount + k;
           const int b = tc % NB;
           mbar_wait(FULLK(ks), kph);
+          TRACE(2, tc);
           mbar_wait(SEMPTY(b), ((tc / NB) & 1) ^ 1);   // released by its previous use
           fence_after();
           const uint32_t kt = sbase + OFF_K + ks * kTileBytes;
-          const uint32_t tS = tmem + 64 * b;
+          const uint32_t tS = tmem + TM_S + 64 * b;
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk) {
-            const uint32_t qa = sbase + OFF_Q + (kk >> 2) * (MM * 128) + (kk & 3) * 32;
             const uint32_t ka = kt + (kk >> 2) * kBox + (kk & 3) * 32;
-            umma_f16(tS, sdesc(qa, 16, 1024), sdesc(ka, 16, 1024), IQK, kk > 0);
+            // A = Q from TMEM: 16 bf16 of K per step = 8 packed columns
+#ifdef BMC_TC_TRACE
+            if (blockIdx.x == 0 && tc < 256) g_tc_mma[0][tc][kk] = clk();
+#endif
+            umma_f16_ts(tS, tmem + TM_Q + kk * 8, sdesc(ka, 16, 1024), IQK, kk > 0);
           }
+          TRACE(3, tc);
+#ifdef BMC_TC_TRACE
+          if (blockIdx.x == 0 && tc < 256) g_tc_mma[0][tc][8] = clk();
+#endif
           umma_commit(SFULL(b));
           umma_commit(EMPTYK(ks));    // K stage reusable once Q.K^T completed
           if (++ks == KS) { ks = 0; kph ^= 1; }
@@ -444,20 +503,27 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
           const int tc = tcount + k;
           const int b = tc % NB;
           mbar_wait(PFULL(b), (tc / NB) & 1);
+          TRACE(4, tc);
           mbar_wait(FULLV(vs), vph);
+          TRACE(5, tc);
           fence_after();
           const uint32_t vt = sbase + OFF_V + vs * kTileBytes;
 #pragma unroll
           for (int hl = 0; hl < BMC_TC_HALVES; ++hl) {
-            const uint32_t pa0 = sbase + OFF_P + (2 * b + hl) * P_BYTES;
+            const uint32_t pa0 = tmem + TM_P + b * 64 + hl * 32;   // A = P from TMEM
 #pragma unroll
             for (int kk = 0; kk < KT / 16; ++kk) {
-              const uint32_t pa = pa0 + kk * 32;
               const uint32_t va = vt + kk * 2048;   // 16 keys = two 8-row groups
-              umma_f16(tO, sdesc(pa, 16, 1024), sdesc(va, kBox, 1024), IPV,
-                       (k > 0 || hl > 0 || kk > 0) ? 1u : 0u);
+#ifdef BMC_TC_TRACE
+              if (blockIdx.x == 0 && tc < 256) g_tc_mma[1][tc][hl * 4 + kk] = clk();
+#endif
+              umma_f16_ts(tO, pa0 + kk * 8, sdesc(va, kBox, 1024), IPV,
+                          (k > 0 || hl > 0 || kk > 0) ? 1u : 0u);
             }
           }
+#ifdef BMC_TC_TRACE
+          if (blockIdx.x == 0 && tc < 256) g_tc_mma[1][tc][8] = clk();
+#endif
           umma_commit(PEMPTY(b));     // P buffer b reusable, O updated
           umma_commit(EMPTYV(vs));    // V stage reusable
           if (++vs == VS) { vs = 0; vph ^= 1; }
@@ -491,13 +557,23 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
         mbar_wait(QDONE, qdph);
         qdph ^= 1;
       }
-      const __nv_bfloat16* qsrc = p.Q + ((size_t)b_ * p.H_q + (size_t)g_ * p.G) * p.t * D;
-      for (int x = stid; x < p.M * (D / 8); x += 256) {
-        const int r = x / (D / 8), c = x % (D / 8);
-        const uint4 v = *reinterpret_cast<const uint4*>(qsrc + (size_t)r * D + c * 8);
-        *reinterpret_cast<uint4*>(smem + OFF_Q + (c >> 3) * (MM * 128) + sw128(r, c & 7)) = v;
+      // each thread stores the half (64 dims = 32 packed columns) of its row
+      {
+        const __nv_bfloat16* qrow =
+            p.Q + (((size_t)b_ * p.H_q + (size_t)g_ * p.G) * p.t + (active ? row : 0)) * D +
+            half * 64;
+        uint32_t w[32];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const uint4 v = active ? *reinterpret_cast<const uint4*>(qrow + c * 8)
+                                 : make_uint4(0, 0, 0, 0);
+          w[4 * c] = v.x; w[4 * c + 1] = v.y; w[4 * c + 2] = v.z; w[4 * c + 3] = v.w;
+        }
+        tmem_st16(tmem + TM_Q + half * 32 + lane_addr, w);
+        tmem_st16(tmem + TM_Q + half * 32 + 16 + lane_addr, w + 16);
+        tmem_wait_st();
       }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      fence_before();
       mbar_arrive(QFULL);
       // chain (reading R7): keys [0, valid_b + tau); token tree:
       // the committed keys plus the node's ancestors and itself
@@ -511,7 +587,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
         const int tc = tcount + k;          // this CTA's tile counter
         const int bb = tc % NB;
         const long long key0 = (long long)(j0 + k) * KT + half * 32;
+        if (stid == 0) TRACE(6, tc);
         mbar_wait(SFULL(bb), (tc / NB) & 1);
+        if (stid == 0) TRACE(7, tc);
+        TRACE_W(0, tc);
         fence_after();
         float sv[32];
         tmem_ld32(tmem + 64 * bb + half * 32 + lane_addr, sv);
@@ -541,10 +620,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
         float* xk = xch + ((tcount + k) & 1) * 256;
         xk[half * 128 + row] = mt;
         pair_sync();
+        if (stid == 0) TRACE(8, tc);
+        TRACE_W(1, tc);
         mt = fmaxf(mt, xk[(half ^ 1) * 128 + row]) * p.qscale;
         // P buffer bb was last read by the PV of tile tc - NB: the c-th
         // completion of PEMPTY(bb) belongs to the c-th tile using bb
         if (tc >= NB) mbar_wait(PEMPTY(bb), ((tc / NB) - 1) & 1);
+        if (stid == 0) TRACE(9, tc);
+        TRACE_W(2, tc);
         // lazy rescale: keep the old max unless the new one exceeds it by > 8
         // (both threads of a row take the same decision from the same values)
         bool rescale = false;
@@ -573,9 +656,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
           }
           fence_before();
         }
-        // P = exp2(s*qscale - m_use) split into bf16 hi + lo, UMMA layout
-        uint8_t* phi = smem + OFF_P + (2 * bb) * P_BYTES;
-        uint8_t* plo = phi + P_BYTES;
+        // P = exp2(s*qscale - m_use) split into bf16 hi + lo, stored packed in
+        // TMEM as the A operand of P.V (this thread: 32 keys = 16 columns)
+        uint32_t hw16[16], lw16[16];
         if (active) {
           const bool none = (m_use == -INFINITY);
           const float nm = -m_use;
@@ -597,14 +680,25 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
               hw[e] = *reinterpret_cast<const uint32_t*>(&h2);
               lw[e] = *reinterpret_cast<const uint32_t*>(&l2);
             }
-            const int ck = half * 4 + c8;
-            *reinterpret_cast<uint4*>(phi + sw128(row, ck)) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-            *reinterpret_cast<uint4*>(plo + sw128(row, ck)) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              hw16[c8 * 4 + e] = hw[e];
+              lw16[c8 * 4 + e] = lw[e];
+            }
           }
           l += (ts2a.x + ts2b.x) + (ts2a.y + ts2b.y);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) hw16[e] = lw16[e] = 0u;
         }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        const uint32_t tp = tmem + TM_P + bb * 64 + half * 16 + lane_addr;
+        tmem_st16(tp, hw16);
+        tmem_st16(tp + 32, lw16);
+        tmem_wait_st();
+        fence_before();
         mbar_arrive(PFULL(bb));
+        if (stid == 0) TRACE(10, tc);
+        TRACE_W(3, tc);
       }
       // ---- epilogue of this item: O (TMEM) -> output or partial record
       float* xl = xch + ((tcount + n) & 1) * 256;   // the parity no tile reads now
@@ -670,6 +764,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
   fence_before();
   __syncthreads();
   fence_after();
+#ifdef BMC_TC_TRACE
+  if (threadIdx.x == 0) { g_tc_cta[blockIdx.x][2] = clk(); g_tc_cta[blockIdx.x][3] = gtime(); }
+#endif
   if (warp == 1) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }
@@ -711,6 +808,15 @@ static cudaError_t make_map(CUtensorMap* m, const void* base, long long rows) {
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
+
+#ifdef BMC_TC_TRACE
+extern "C" int bmc_tc_trace(long long* out) {   // 16 x 256 clock64 values of CTA 0
+  if (cudaMemcpyFromSymbol(out, tc::g_tc_trace, sizeof(long long) * 16 * 256) != cudaSuccess) return -1;
+  if (cudaMemcpyFromSymbol(out + 16 * 256, tc::g_tc_mma, sizeof(long long) * 2 * 256 * 9) != cudaSuccess) return -1;
+  if (cudaMemcpyFromSymbol(out + 16 * 256 + 2 * 256 * 9, tc::g_tc_sm, sizeof(long long) * 8 * 256 * 4) != cudaSuccess) return -1;
+  return cudaMemcpyFromSymbol(out + 16 * 256 + 2 * 256 * 9 + 8 * 256 * 4, tc::g_tc_cta, sizeof(long long) * 160 * 4) == cudaSuccess ? 0 : -1;
+}
+#endif
 
 bool attn_tc_supported(int D, int dtype, int M) {
   return D == 128 && dtype == BMC_BF16 && M >= 1 && M <= tc::MM && encode_fn() != nullptr;
