@@ -1,0 +1,679 @@
+// attn_tck.cu -- GQA / speculative-verify attention on the 5th-generation
+// tensor cores with the KEYS on the TMEM lanes, sm_100a, bf16 cache, D = 128.
+//
+// Same computation as attn_decode.cu and attn_tc.cu (mask
+// P:L846-853, GQA P:L834-844, SD query block P:L444-448, token trees
+// P:L863-866): for a (batch b, kv head g) unit, its M = G*t query rows
+// attend the unit's cap key rows; row tau = m % t sees keys [0, valid_b + tau)
+// (chain) or the committed keys plus its node's ancestors (tree).
+//
+// Why this orientation: attn_tc.cu puts the M query rows on the TMEM lanes
+// (S = Q K^T, MMA M = 128 rows).  A TMEM lane quadrant q is reachable only
+// from warps with warp % 4 == q, which is also the SM sub-partition, so for
+// M <= 32 every exp2 / convert of the softmax lands on one SMSP: ~1000 cycles
+// per 64-key tile, the kernel's measured bottleneck (profiles/
+// r01_tc_trace_findings.txt).  Here the 128 keys of a tile are the MMA M:
+//     S^T[b] (TMEM, 128 key lanes x N cols fp32) = K_tile . Q^T
+//            M=128 (keys) x N (queries, M padded to 16 or 32) x K=128 (dims),
+//            A = K tile (K-major SW128), B = Q (K-major SW128, smem);
+//     O^T    (TMEM, 128 dim lanes x 2N cols fp32) += V_tile^T . [P_hi; P_lo]^T
+//            M=128 (dims) x 2N x K=128 (keys), A = V tile (MN-major SW128),
+//            B = P^T hi rows then lo rows (K-major SW128, smem),
+// so every lane of every softmax warp carries one key and a thread's work per
+// tile is the N/2 queries of its half, not 32 keys: the exp2 / pack work is
+// spread over all four SMSPs and shrinks by 128/N.
+//
+// Roles (384 threads, one persistent CTA per SM, stream-K tile split):
+//   warp 0 / 10: TMA producers of the K / V rings (2D tensor maps, boxes of
+//                64 dims x 128 keys, SWIZZLE_128B);
+//   warp 1:      TMEM allocator + S^T issuer;  warp 11: O^T issuer;
+//   warps 2-9:   softmax; warp w owns TMEM lane quadrant w % 4 (keys
+//                32*(w%4) .. +31 of each tile, dims 32*(w%4) .. of O^T) and
+//                query half (w - 2) / 4 (columns h*N/2 .. +N/2).
+// Online softmax with a lazy max (P:L274-276 restated as exp2 of
+// log2-scaled scores): a column's running max m only moves when a score
+// exceeds it by more than 8 (log2 units); the check is one barrier-reduction
+// (bar.red.or) per tile over the 4 warps of a half, and the column maxima are
+// reduced only when it fires.  P = 2^(s - m) is split into bf16 hi (upper 16
+// bits) + lo (rounded remainder): P = hi + lo to ~2^-16 relative, so the
+// tensor-core P.V keeps the bf16 path inside its 2e-3 budget.
+// Split units use the partial-record + last-CTA combine of combine.cuh.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "bmc_internal.h"
+#include "combine.cuh"
+#include "tc_common.cuh"
+
+namespace bmc {
+namespace tck {
+using namespace tcc;
+
+constexpr int D = 128;            // head dim (bf16)
+constexpr int KT = 128;           // keys per tile = MMA M of S^T
+constexpr int NB = 2;             // S^T / P^T buffers (tiles in flight)
+constexpr int kThreads = 384;
+constexpr uint32_t kTileBytes = KT * D * 2;   // 32 KiB per tensor per tile
+constexpr uint32_t kBox = 64 * 2 * KT;        // one 64-dim box of a tile: 16 KiB
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kRescale = 8.0f;
+
+template <int N>
+struct Cfg {
+  static_assert(N == 16 || N == 32, "query columns");
+  static constexpr int NH = N / 2;                          // columns per softmax half
+  static constexpr int KS = N <= 16 ? 3 : 2;                // K ring stages
+  static constexpr int VS = N <= 32 ? 3 : 2;                // V ring stages
+  static constexpr uint32_t OFF_K = 0;
+  static constexpr uint32_t OFF_V = OFF_K + KS * kTileBytes;
+  static constexpr uint32_t OFF_Q = OFF_V + VS * kTileBytes;   // [2 dim atoms][N][128 B]
+  static constexpr uint32_t kQAtom = N * 128;
+  static constexpr uint32_t OFF_P = OFF_Q + 2 * kQAtom;        // [NB][2 key atoms][2N][128 B]
+  static constexpr uint32_t kPAtom = 2 * N * 128;
+  static constexpr uint32_t kPBytes = 2 * kPAtom;
+  static constexpr uint32_t OFF_BAR = OFF_P + NB * kPBytes;
+  static constexpr uint32_t OFF_RED = OFF_BAR + 512;           // [2 halves][4 quadrants][NH] f32
+  static constexpr uint32_t OFF_SUM = OFF_RED + 2 * 4 * NH * 4;
+  static constexpr uint32_t kSmem = OFF_SUM + 2 * 4 * NH * 4 + 16;
+  static_assert(kSmem <= 232448, "shared memory");
+  static_assert(kQAtom % 1024 == 0 && kPAtom % 1024 == 0, "SW128 atoms");
+  static_assert(NB * kPBytes >= (4 + 2) * N * 4, "combine scratch in the P area");
+  // TMEM columns: S^T[b] at b*N, O^T (hi N cols, lo N cols) at NB*N
+  static constexpr uint32_t TM_O = NB * N;
+  static_assert(NB * N + 2 * N <= 256, "TMEM columns");
+};
+
+#ifdef BMC_TC_TRACE
+// Debug timeline (CTA 0): per tile clock64 at each wait / issue point; per CTA entry / exit.
+__device__ long long g_tck_trace[16][256];
+__device__ long long g_tck_cta[160][4];
+__device__ __forceinline__ long long clk() {
+  long long c;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+  return c;
+}
+__device__ __forceinline__ long long gtime() {
+  long long c;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(c));
+  return c;
+}
+#define TRACE(ev, i) do { if (blockIdx.x == 0 && (i) < 256) g_tck_trace[ev][i] = clk(); } while (0)
+#else
+#define TRACE(ev, i) do { } while (0)
+#endif
+
+struct Params {
+  CUtensorMap tmK;   // [U*cap rows][128] bf16, box 64 x 128, SWIZZLE_128B
+  CUtensorMap tmV;
+  const __nv_bfloat16* Q;   // [B][H_q][t][D]
+  float* O;                 // [B][H_q][t][D]
+  const uint8_t* Knew;      // pending appended row [B][H_kv][D] (n_app == 1)
+  const uint8_t* Vnew;
+  const uint8_t* Kd;        // pending drafts [B][H_kv][kd_stride][D]
+  const uint8_t* Vd;
+  uint8_t* Kc;              // cache base (pending rows are stored here)
+  uint8_t* Vc;
+  int n_app, n_draft, kd_stride;
+  float* ws;
+  int* counters;
+  long long cap;
+  long long total_tiles;
+  int tpu, U, H_kv, H_q, G, t, M, ctas;
+  float qscale;
+  int tree;
+  uint32_t anc[32];
+  int valid[BMC_MAX_B];
+};
+
+__device__ __forceinline__ void softmax_sync() {   // the 8 softmax warps
+  asm volatile("bar.sync 1, 256;" ::: "memory");
+}
+__device__ __forceinline__ void half_sync(int h) {  // the 4 warps of one query half
+  asm volatile("bar.sync %0, 128;" ::"r"(2 + h) : "memory");
+}
+// OR of `pred` over the 4 warps of query half h (a barrier with reduction)
+__device__ __forceinline__ bool half_any(int h, bool pred) {
+  uint32_t r;
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t"
+      "setp.ne.u32 p, %2, 0;\n\t"
+      "bar.red.or.pred q, %1, 128, p;\n\t"
+      "selp.u32 %0, 1, 0, q;\n\t}"
+      : "=r"(r)
+      : "r"(2 + h), "r"((uint32_t)pred)
+      : "memory");
+  return r != 0;
+}
+__device__ __forceinline__ void sts_u16(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"((unsigned short)v) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// NC consecutive fp32 TMEM columns of this warp's lane quadrant (NC % 8 == 0)
+template <int NC>
+__device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, float* v) {
+#pragma unroll
+  for (int c = 0; c < NC; c += 8) {
+    uint32_t* r = reinterpret_cast<uint32_t*>(v + c);
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7])
+        : "r"(taddr + c));
+  }
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+template <int NC>
+__device__ __forceinline__ void tmem_st_cols(uint32_t taddr, const float* v) {
+#pragma unroll
+  for (int c = 0; c < NC; c += 8) {
+    const uint32_t* r = reinterpret_cast<const uint32_t*>(v + c);
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr + c),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+        : "memory");
+  }
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ float warp_max(float x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, o));
+  return x;
+}
+__device__ __forceinline__ float warp_sum(float x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+
+template <int N>
+__global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_constant__ Params p) {
+  using C = Cfg<N>;
+  constexpr int NH = C::NH;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const uint32_t sbase = su32(smem);
+  if (sbase & 1023u) __trap();
+#ifdef BMC_TC_TRACE
+  if (threadIdx.x == 0) { g_tck_cta[blockIdx.x][0] = clk(); g_tck_cta[blockIdx.x][1] = gtime(); }
+#endif
+  const uint32_t bar0 = sbase + C::OFF_BAR;
+  auto FULLK = [&](int s) { return bar0 + 8u * s; };
+  auto EMPTYK = [&](int s) { return bar0 + 8u * (4 + s); };
+  auto FULLV = [&](int s) { return bar0 + 8u * (8 + s); };
+  auto EMPTYV = [&](int s) { return bar0 + 8u * (12 + s); };
+  auto SFULL = [&](int b) { return bar0 + 8u * (16 + b); };    // S^T MMA -> softmax
+  auto SEMPTY = [&](int b) { return bar0 + 8u * (18 + b); };   // softmax read S^T[b]
+  auto PFULL = [&](int b) { return bar0 + 8u * (20 + b); };    // P^T[b] in smem
+  auto PEMPTY = [&](int b) { return bar0 + 8u * (22 + b); };   // O^T MMA read P^T[b]
+  const uint32_t QFULL = bar0 + 8u * 24;
+  const uint32_t ODONE = bar0 + 8u * 25;
+  const uint32_t QDONE = bar0 + 8u * 26;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::OFF_BAR + 8 * 28);
+  int* sm_flag = reinterpret_cast<int*>(smem + C::OFF_BAR + 8 * 29);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const long long NT = p.total_tiles;
+  const long long t_begin = tile_begin(blockIdx.x, NT, p.ctas);
+  const long long t_end = tile_begin(blockIdx.x + 1, NT, p.ctas);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::KS; ++s) {
+      mbar_init(FULLK(s), 1);
+      mbar_init(EMPTYK(s), 1);
+    }
+    for (int s = 0; s < C::VS; ++s) {
+      mbar_init(FULLV(s), 1);
+      mbar_init(EMPTYV(s), 1);
+    }
+    for (int b = 0; b < NB; ++b) {
+      mbar_init(SFULL(b), 1);
+      mbar_init(SEMPTY(b), 256);
+      mbar_init(PFULL(b), 256);
+      mbar_init(PEMPTY(b), 1);
+    }
+    mbar_init(QFULL, 256);
+    mbar_init(ODONE, 1);
+    mbar_init(QDONE, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
+                     su32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  // fused KV-cache update: the pending appended / drafted rows that
+  // fall into this CTA's tiles are stored before its TMA loads read them
+  if (p.n_app || p.n_draft) {
+    constexpr int CHR = D * 2 / 16;
+    const int per_unit = (p.n_app + p.n_draft) * 2 * CHR;
+    const long long u0 = t_begin / p.tpu, u1 = (t_end - 1) / p.tpu;
+    for (long long x = threadIdx.x; x < (u1 - u0 + 1) * per_unit; x += kThreads) {
+      const long long uu = u0 + x / per_unit;
+      const int y = (int)(x % per_unit);
+      const int ck = y % CHR, tensor = (y / CHR) & 1, ri = y / (2 * CHR);
+      const int vb = p.valid[(int)(uu / p.H_kv)];
+      int row;
+      const uint8_t* src;
+      if (p.n_app && ri == 0) {
+        row = vb - 1;
+        src = (tensor ? p.Vnew : p.Knew) + (size_t)uu * (D * 2);
+      } else {
+        const int di = ri - p.n_app;
+        row = vb + di;
+        src = (tensor ? p.Vd : p.Kd) + ((size_t)uu * p.kd_stride + di) * (D * 2);
+      }
+      const long long tile = uu * p.tpu + row / KT;
+      if (tile < t_begin || tile >= t_end) continue;
+      const uint4 v = *reinterpret_cast<const uint4*>(src + ck * 16);
+      *reinterpret_cast<uint4*>((tensor ? p.Vc : p.Kc) + ((size_t)uu * p.cap + row) * (D * 2) +
+                                ck * 16) = v;
+    }
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 || warp == 10) {
+    // ------------------------------------------------------ TMA producers
+    if (lane == 0) {
+      const bool isK = warp == 0;
+      const CUtensorMap* tm = isK ? &p.tmK : &p.tmV;
+      const int NS = isK ? C::KS : C::VS;
+      const uint32_t ring = sbase + (isK ? C::OFF_K : C::OFF_V);
+      const uint64_t pol = evict_first_policy();
+      int s = 0;
+      uint32_t ph = 0;
+      long long u = t_begin / p.tpu;
+      int j = (int)(t_begin % p.tpu);
+      for (long long i = t_begin; i < t_end; ++i) {
+        mbar_wait(isK ? EMPTYK(s) : EMPTYV(s), ph ^ 1);
+        TRACE(isK ? 0 : 1, (int)(i - t_begin));
+        const int row = (int)(u * p.cap + (long long)j * KT);
+        const uint32_t dst = ring + s * kTileBytes;
+        const uint32_t fb = isK ? FULLK(s) : FULLV(s);
+        mbar_expect_tx(fb, kTileBytes);
+        tma_load_2d(dst, tm, 0, row, fb, pol);
+        tma_load_2d(dst + kBox, tm, 64, row, fb, pol);
+        if (++j == p.tpu) { j = 0; ++u; }
+        if (++s == NS) { s = 0; ph ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------ S^T = K Q^T issuer
+    if (lane == 0) {
+      constexpr uint32_t IQK = idesc_bf16(KT, N, 0, 0);
+      const uint32_t qs = sbase + C::OFF_Q;
+      int ks = 0;
+      uint32_t kph = 0, qph = 0;
+      long long i = t_begin;
+      int tcount = 0;
+      while (i < t_end) {
+        const long long u = i / p.tpu;
+        const long long iend = min(t_end, (u + 1) * p.tpu);
+        mbar_wait(QFULL, qph);
+        qph ^= 1;
+        fence_after();
+        const int n = (int)(iend - i);
+        for (int k = 0; k < n; ++k) {
+          const int tc = tcount + k;
+          const int b = tc % NB;
+          mbar_wait(FULLK(ks), kph);
+          TRACE(2, tc);
+          mbar_wait(SEMPTY(b), ((tc / NB) & 1) ^ 1);
+          TRACE(3, tc);
+          fence_after();
+          const uint32_t kt = sbase + C::OFF_K + ks * kTileBytes;
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t koff = (kk >> 2) * kBox + (kk & 3) * 32;
+            const uint32_t qoff = (kk >> 2) * C::kQAtom + (kk & 3) * 32;
+            umma_f16(tmem + b * N, sdesc(kt + koff, 16, 1024), sdesc(qs + qoff, 16, 1024), IQK,
+                     kk > 0);
+          }
+          TRACE(4, tc);
+          umma_commit(SFULL(b));
+          umma_commit(EMPTYK(ks));
+          if (++ks == C::KS) { ks = 0; kph ^= 1; }
+        }
+        umma_commit(QDONE);
+        tcount += n;
+        i = iend;
+      }
+    }
+  } else if (warp == 11) {
+    // ------------------------------------------------------ O^T += V^T P^T issuer
+    if (lane == 0) {
+      constexpr uint32_t IPV = idesc_bf16(D, 2 * N, 1, 0);   // A = V tile, MN-major
+      int vs = 0;
+      uint32_t vph = 0;
+      long long i = t_begin;
+      int tcount = 0;
+      while (i < t_end) {
+        const long long u = i / p.tpu;
+        const long long iend = min(t_end, (u + 1) * p.tpu);
+        const int n = (int)(iend - i);
+        for (int k = 0; k < n; ++k) {
+          const int tc = tcount + k;
+          const int b = tc % NB;
+          mbar_wait(PFULL(b), (tc / NB) & 1);
+          TRACE(5, tc);
+          mbar_wait(FULLV(vs), vph);
+          TRACE(6, tc);
+          fence_after();
+          const uint32_t vt = sbase + C::OFF_V + vs * kTileBytes;
+          const uint32_t pb = sbase + C::OFF_P + b * C::kPBytes;
+#pragma unroll
+          for (int kk = 0; kk < KT / 16; ++kk) {
+            const uint32_t poff = (kk >> 2) * C::kPAtom + (kk & 3) * 32;
+            umma_f16(tmem + C::TM_O, sdesc(vt + kk * 2048, kBox, 1024), sdesc(pb + poff, 16, 1024),
+                     IPV, (k > 0 || kk > 0) ? 1u : 0u);
+          }
+          TRACE(7, tc);
+          umma_commit(PEMPTY(b));
+          umma_commit(EMPTYV(vs));
+          if (++vs == C::VS) { vs = 0; vph ^= 1; }
+        }
+        umma_commit(ODONE);
+        tcount += n;
+        i = iend;
+      }
+    }
+  } else {
+    // ------------------------------------------------ softmax + epilogue
+    const int h = (warp - 2) >> 2;        // query half: columns h*NH .. +NH
+    const int q = warp & 3;               // TMEM lane quadrant: keys / dims 32q .. +31
+    const int kl = q * 32 + lane;         // this thread's key (in a tile) / dim (in O^T)
+    const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
+    const int stid = threadIdx.x - 64;
+    float* red = reinterpret_cast<float*>(smem + C::OFF_RED) + h * 4 * NH;   // [4][NH]
+    float* sums = reinterpret_cast<float*>(smem + C::OFF_SUM) + h * 4 * NH;  // [4][NH]
+    // P^T store address of key kl: key atom kl/64, 16-byte chunk (kl%64)/8 (swizzled by row)
+    const uint32_t pkey = (uint32_t)(kl >> 6) * C::kPAtom + (uint32_t)(kl & 7) * 2;
+    const uint32_t pchunk = (uint32_t)((kl & 63) >> 3);
+    uint32_t oph = 0, qdph = 0;
+    long long i = t_begin;
+    int tcount = 0;
+    bool first_item = true;
+    while (i < t_end) {
+      const long long u = i / p.tpu;
+      const long long iend = min(t_end, (u + 1) * p.tpu);
+      const int b_ = (int)(u / p.H_kv), g_ = (int)(u % p.H_kv);
+      const int j0 = (int)(i % p.tpu);
+      const size_t qrow0 = ((size_t)b_ * p.H_q + (size_t)g_ * p.G) * p.t;   // first query row
+      if (!first_item) {
+        mbar_wait(QDONE, qdph);
+        qdph ^= 1;
+      }
+      // Q rows (zero beyond M) into the K-major SW128 B operand
+      for (int x = stid; x < N * 16; x += 256) {
+        const int m = x >> 4, c = x & 15;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (m < p.M) v = *reinterpret_cast<const uint4*>(p.Q + (qrow0 + m) * D + c * 8);
+        const uint32_t off = (uint32_t)(c >> 3) * C::kQAtom + (uint32_t)m * 128 +
+                             ((((uint32_t)c & 7u) ^ ((uint32_t)m & 7u)) << 4);
+        *reinterpret_cast<uint4*>(smem + C::OFF_Q + off) = v;
+      }
+      fence_proxy_smem();
+      mbar_arrive(QFULL);
+      const int vb_ = p.valid[b_];
+      const int mcols = p.M - h * NH;    // active query columns of this half
+      float m_use[NH], l[NH];
+#pragma unroll
+      for (int c = 0; c < NH; ++c) {
+        m_use[c] = -INFINITY;
+        l[c] = 0.f;
+      }
+      const int n = (int)(iend - i);
+      for (int k = 0; k < n; ++k) {
+        const int tc = tcount + k;
+        const int bb = tc % NB;
+        const long long kidx = (long long)(j0 + k) * KT + kl;   // this thread's key row
+        if (stid == 0) TRACE(8, tc);
+        mbar_wait(SFULL(bb), (tc / NB) & 1);
+        if (stid == 0) TRACE(9, tc);
+        fence_after();
+        float x[NH];
+        tmem_ld_cols<NH>(tmem + bb * N + h * NH + lane_addr, x);
+        fence_before();
+        mbar_arrive(SEMPTY(bb));
+        // mask (chain: keys < valid_b + tau; tree: committed keys + ancestors)
+        // and log2 scaling; columns >= M are padding.  Only the tiles that
+        // reach past the committed rows need the per-column rule.
+        bool need = false;
+        if ((long long)(j0 + k + 1) * KT <= vb_) {
+#pragma unroll
+          for (int c = 0; c < NH; ++c) {
+            x[c] = c < mcols ? x[c] * p.qscale : -INFINITY;
+            need |= x[c] > m_use[c] + kRescale;
+          }
+        } else {
+          const long long js = kidx - vb_;
+#pragma unroll
+          for (int c = 0; c < NH; ++c) {
+            bool vis = c < mcols;
+            if (vis) {
+              const int tau = (h * NH + c) % p.t;
+              vis = kidx < (long long)vb_ + (p.tree ? 0 : tau) ||
+                    (p.tree && tau > 0 && js >= 0 && js < 32 && ((p.anc[tau - 1] >> js) & 1u));
+            }
+            x[c] = vis ? x[c] * p.qscale : -INFINITY;
+            need |= x[c] > m_use[c] + kRescale;
+          }
+        }
+        const bool any_ = half_any(h, need);
+        if (stid == 0) TRACE(10, tc);
+        if (any_) {
+          // column maxima of this tile over the half's 4 warps
+#pragma unroll
+          for (int c = 0; c < NH; ++c) {
+            const float wm = warp_max(x[c]);
+            if (lane == 0) red[q * NH + c] = wm;
+          }
+          half_sync(h);
+          bool resc = false;
+          float alpha[NH];
+#pragma unroll
+          for (int c = 0; c < NH; ++c) {
+            const float mt =
+                fmaxf(fmaxf(red[c], red[NH + c]), fmaxf(red[2 * NH + c], red[3 * NH + c]));
+            alpha[c] = 1.f;
+            if (mt > m_use[c] + kRescale) {
+              alpha[c] = (m_use[c] == -INFINITY) ? 0.f : fast_exp2(m_use[c] - mt);
+              m_use[c] = mt;
+              l[c] *= alpha[c];
+              resc |= (alpha[c] != 1.f);
+            }
+          }
+          // O^T columns of this half (rows = dims of this quadrant) are
+          // rescaled once the previous tile's O^T MMAs have completed
+          if (resc && k > 0) {
+            const int tp = tc - 1;
+            mbar_wait(PEMPTY(tp % NB), (tp / NB) & 1);
+            fence_after();
+#pragma unroll
+            for (int hl = 0; hl < 2; ++hl) {
+              float ov[NH];
+              const uint32_t ta = tmem + C::TM_O + hl * N + h * NH + lane_addr;
+              tmem_ld_cols<NH>(ta, ov);
+#pragma unroll
+              for (int c = 0; c < NH; ++c) ov[c] *= alpha[c];
+              tmem_st_cols<NH>(ta, ov);
+            }
+            fence_before();
+          }
+        }
+        // P^T[bb] was last read by the O^T MMAs of tile tc - NB
+        if (stid == 0) TRACE(11, tc);
+        if (tc >= NB) mbar_wait(PEMPTY(bb), ((tc / NB) - 1) & 1);
+        if (stid == 0) TRACE(12, tc);
+        const uint32_t pbase = sbase + C::OFF_P + bb * C::kPBytes + pkey;
+#pragma unroll
+        for (int c = 0; c < NH; ++c) {
+          // a column still at m = -inf has seen only masked keys (x = -inf): P = 0
+          const float pv = fast_exp2(x[c] - (m_use[c] == -INFINITY ? 0.f : m_use[c]));
+          l[c] += pv;
+          const uint32_t bits = __float_as_uint(pv);
+          const float hi = __uint_as_float(bits & 0xffff0000u);
+          const uint32_t lo = (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(pv - hi));
+          const uint32_t rh = (uint32_t)(h * NH + c), rl = rh + N;   // P^T rows: hi, lo
+          sts_u16(pbase + rh * 128 + ((pchunk ^ (rh & 7u)) << 4), bits >> 16);
+          sts_u16(pbase + rl * 128 + ((pchunk ^ (rl & 7u)) << 4), lo);
+        }
+        fence_proxy_smem();
+        mbar_arrive(PFULL(bb));
+        if (stid == 0) TRACE(13, tc);
+      }
+      // ---- epilogue of this item: column sums, O^T (TMEM) -> output / record
+#pragma unroll
+      for (int c = 0; c < NH; ++c) {
+        const float ws_ = warp_sum(l[c]);
+        if (lane == 0) sums[q * NH + c] = ws_;
+      }
+      mbar_wait(ODONE, oph);
+      oph ^= 1;
+      fence_after();
+      half_sync(h);
+      const long long ufirst = u * p.tpu, ulast = ufirst + p.tpu - 1;
+      const int c_lo = cta_of_tile(ufirst, NT, p.ctas);
+      const int c_hi = cta_of_tile(ulast, NT, p.ctas);
+      const int nseg = c_hi - c_lo + 1;
+      const size_t rec = rec_floats(p.M, D);
+      float* my = p.ws + ((size_t)blockIdx.x * 2 + (first_item ? 0 : 1)) * rec;
+      float o_hi[NH], o_lo[NH];
+      tmem_ld_cols<NH>(tmem + C::TM_O + h * NH + lane_addr, o_hi);
+      tmem_ld_cols<NH>(tmem + C::TM_O + N + h * NH + lane_addr, o_lo);
+#pragma unroll
+      for (int c = 0; c < NH; ++c) {
+        const int m = h * NH + c;
+        if (m < p.M) {
+          const float L = (sums[c] + sums[NH + c]) + (sums[2 * NH + c] + sums[3 * NH + c]);
+          const float o = o_hi[c] + o_lo[c];
+          if (nseg == 1) {
+            p.O[(qrow0 + m) * D + kl] = o / L;
+          } else {
+            my[(size_t)m * D + kl] = o;
+            if (kl == 0) {
+              my[(size_t)p.M * D + m] = m_use[c];
+              my[(size_t)p.M * D + p.M + m] = L;
+            }
+          }
+        }
+      }
+      fence_before();
+      if (nseg > 1) {
+        __threadfence();
+        softmax_sync();
+        if (stid == 0) {
+          const int old = atomicAdd(&p.counters[u], 1);
+          *sm_flag = (old == nseg - 1);
+        }
+        softmax_sync();
+        if (*sm_flag) {
+          __threadfence();
+          // scratch: the P^T buffers (every O^T MMA of this item has completed)
+          combine_unit<4>(p.ws, rec, c_lo, c_hi, ufirst, NT, p.ctas, p.M, D, p.O + qrow0 * D,
+                          reinterpret_cast<float*>(smem + C::OFF_P), stid, 256,
+                          [] { softmax_sync(); });
+          if (stid == 0) p.counters[u] = 0;
+        }
+      }
+      softmax_sync();   // sums / flag reuse by the next item
+      tcount += n;
+      first_item = false;
+      i = iend;
+    }
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+#ifdef BMC_TC_TRACE
+  if (threadIdx.x == 0) { g_tck_cta[blockIdx.x][2] = clk(); g_tck_cta[blockIdx.x][3] = gtime(); }
+#endif
+  if (warp == 1) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+  }
+}
+
+}  // namespace tck
+
+// ------------------------------------------------------------------ host
+
+#ifdef BMC_TC_TRACE
+extern "C" int bmc_tck_trace(long long* out) {   // [16][256] tile events, then [160][4] CTAs
+  if (cudaMemcpyFromSymbol(out, tck::g_tck_trace, sizeof(long long) * 16 * 256) != cudaSuccess)
+    return -1;
+  return cudaMemcpyFromSymbol(out + 16 * 256, tck::g_tck_cta, sizeof(long long) * 160 * 4) ==
+                 cudaSuccess ? 0 : -1;
+}
+#endif
+
+bool attn_tck_supported(int D, int dtype, int M) {
+  return D == 128 && dtype == BMC_BF16 && M >= 1 && M <= 32 && encode_fn() != nullptr;
+}
+
+template <int N>
+static cudaError_t launch_n(const tck::Params& p, int ctas, cudaStream_t s) {
+  static int attr_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev != dev) {
+    cudaError_t e = cudaFuncSetAttribute(tck::attn_tck_kernel<N>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)tck::Cfg<N>::kSmem);
+    if (e != cudaSuccess) return e;
+    attr_dev = dev;
+  }
+  tck::attn_tck_kernel<N><<<ctas, tck::kThreads, tck::Cfg<N>::kSmem, s>>>(p);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_attn_tck(const AttnStepArgs& a, int num_sms, cudaStream_t s) {
+  const AttnLayer& h = a.layers[0];
+  tck::Params p;
+  const long long U = (long long)a.B * a.H_kv;
+  cudaError_t e = make_map(&p.tmK, h.K, U * h.cap, tck::KT);
+  if (e == cudaSuccess) e = make_map(&p.tmV, h.V, U * h.cap, tck::KT);
+  if (e != cudaSuccess) return e;
+  p.Q = (const __nv_bfloat16*)h.Q;
+  p.O = h.O;
+  p.Knew = (const uint8_t*)h.Knew;
+  p.Vnew = (const uint8_t*)h.Vnew;
+  p.Kd = (const uint8_t*)h.Kd;
+  p.Vd = (const uint8_t*)h.Vd;
+  p.Kc = (uint8_t*)h.K;
+  p.Vc = (uint8_t*)h.V;
+  p.n_app = h.n_app;
+  p.n_draft = h.n_draft;
+  p.kd_stride = h.kd_stride;
+  p.ws = h.ws;
+  p.counters = h.counters;
+  p.cap = h.cap;
+  p.tpu = (int)(((h.scan > 0 ? h.scan : h.cap) + tck::KT - 1) / tck::KT);
+  p.U = (int)U;
+  p.total_tiles = U * p.tpu;
+  p.H_kv = a.H_kv;
+  p.H_q = a.H_q;
+  p.G = a.H_q / a.H_kv;
+  p.t = a.t;
+  p.M = p.G * a.t;
+  p.qscale = tck::kLog2e / sqrtf((float)tck::D);
+  p.tree = a.tree;
+  for (int i = 0; i < 32; ++i) p.anc[i] = a.anc[i];
+  for (int b = 0; b < a.B; ++b) p.valid[b] = a.valid[b];
+  int ctas = a.ctas > 0 ? a.ctas : num_sms;
+  if (ctas > p.total_tiles) ctas = (int)p.total_tiles;
+  p.ctas = ctas;
+  if (p.total_tiles == 0) return cudaSuccess;
+  if (p.M <= 16) return launch_n<16>(p, ctas, s);
+  return launch_n<32>(p, ctas, s);
+}
+
+}  // namespace bmc

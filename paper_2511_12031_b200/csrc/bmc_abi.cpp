@@ -491,8 +491,11 @@ int bmc_sdpa(bmc_t h, const void* Q, int n_valid, float* O) {
   // tensor cores when M = G*t makes a real tile (north_star item 4); the
   // crossover measured on B200 is M = 3..4 (tcgen05 1.4x faster at M=4,
   // 2.1x at M=5), CUDA cores keep M <= 2 (6.2-6.4 TB/s at M=1)
-  const bool use_tc = h->attn_path == 2 ||
+  const bool use_tc = h->attn_path >= 2 ||
                       (h->attn_path == 0 && M > kTcMinM && bmc::attn_tc_supported(h->D, h->dt, M));
+  // keys on the TMEM lanes for M <= 64 (attn_tck.cu), queries on the lanes
+  // above that or when forced (path 3)
+  const bool use_tck = use_tc && h->attn_path != 3 && bmc::attn_tck_supported(h->D, h->dt, M);
   if (use_tc) {
     if (!bmc::attn_tc_supported(h->D, h->dt, M))
       return fail(BMC_ERR_UNSUPPORTED, "tcgen05 path needs bf16, D=128, G*t<=128");
@@ -507,7 +510,10 @@ int bmc_sdpa(bmc_t h, const void* Q, int n_valid, float* O) {
   a.layers = &layer;
   if (use_tc) {
     a.ctas = std::min(h->attn_ctas, h->num_sms);
-    CK(h, bmc::launch_attn_tc(a, h->num_sms, h->stream), "attn_tc");
+    if (use_tck)
+      CK(h, bmc::launch_attn_tck(a, h->num_sms, h->stream), "attn_tck");
+    else
+      CK(h, bmc::launch_attn_tc(a, h->num_sms, h->stream), "attn_tc");
   } else {
     CK(h, bmc::launch_attn_step(a, h->num_sms, h->stream), "attn_step");
   }
@@ -562,7 +568,7 @@ int bmc_decode_step(const bmc_t* hs, int L, const void* const* K, const void* co
     if (ptr_kind(Q[l]) != 0 || ptr_kind(O[l]) != 0) fused = false;
   // GQA groups large enough for the tensor cores take the (per-layer) tcgen05 kernel
   const bmc_t h0 = hs[0];
-  if (h0->attn_path != 1 && (h0->attn_path == 2 || h0->H_q / h0->H_kv > kTcMinM) &&
+  if (h0->attn_path != 1 && (h0->attn_path >= 2 || h0->H_q / h0->H_kv > kTcMinM) &&
       bmc::attn_tc_supported(h0->D, h0->dt, h0->H_q / h0->H_kv))
     fused = false;
   if (!fused) {
@@ -865,7 +871,7 @@ int bmc_set_option(bmc_t h, int key, long long value) {
       h->attn_ctas = (int)value;
       return 0;
     case BMC_OPT_ATTN_PATH:
-      if (value < 0 || value > 2) return fail(BMC_ERR_ARG, "path");
+      if (value < 0 || value > 3) return fail(BMC_ERR_ARG, "path");
       h->attn_path = (int)value;
       return 0;
     case BMC_OPT_ARENA:

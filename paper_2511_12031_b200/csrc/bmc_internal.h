@@ -92,6 +92,10 @@ cudaError_t launch_attn_step(const AttnStepArgs& a, int num_sms, cudaStream_t s)
 // writes the layer's pending rows into the cache itself, like attn_step.
 bool attn_tc_supported(int D, int dtype, int M);
 cudaError_t launch_attn_tc(const AttnStepArgs& a, int num_sms, cudaStream_t s);
+// tcgen05 attention with the keys on the TMEM lanes (attn_tck.cu; bf16,
+// D = 128, M = G*t <= 64): the default tensor-core kernel for small M.
+bool attn_tck_supported(int D, int dtype, int M);
+cudaError_t launch_attn_tck(const AttnStepArgs& a, int num_sms, cudaStream_t s);
 
 void count_launch();
 unsigned long long launch_count();

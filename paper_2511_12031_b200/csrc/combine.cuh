@@ -30,18 +30,36 @@ __device__ __forceinline__ const float* cmb_record(const float* ws, int c, long 
   return ws + ((size_t)c * 2 + (tb >= ufirst ? 0 : 1)) * rec;
 }
 
-// Per-row merge weights' normalisers: mu (max) and 1/L for row r.
+// Per-row merge weights' normalisers: mu (max) and 1/L for row r.  The
+// records' scalars are loaded 8 segments at a time so a merge costs ~2 L2
+// round trips per 8 segments instead of 2 per segment.
 __device__ __forceinline__ void cmb_row_stats(const float* ws, size_t rec, int c_lo, int c_hi,
                                               long long ufirst, long long NT, int C, int M,
                                               int D, int r, float* mu_out, float* invl_out) {
-  float mu = -INFINITY;
-  for (int c = c_lo; c <= c_hi; ++c)
-    mu = fmaxf(mu, __ldcg(cmb_record(ws, c, ufirst, NT, C, rec) + (size_t)M * D + r));
-  float L = 0.f;
-  for (int c = c_lo; c <= c_hi; ++c) {
-    const float* rr = cmb_record(ws, c, ufirst, NT, C, rec);
-    const float mk = __ldcg(rr + (size_t)M * D + r);
-    if (mk != -INFINITY) L += __ldcg(rr + (size_t)M * D + M + r) * cmb_exp2(mk - mu);
+  constexpr int BT = 8;
+  float mu = -INFINITY, L = 0.f;
+  for (int c0 = c_lo; c0 <= c_hi; c0 += BT) {
+    float mv[BT], lv[BT];
+#pragma unroll
+    for (int s = 0; s < BT; ++s) {
+      mv[s] = -INFINITY;
+      lv[s] = 0.f;
+      if (c0 + s <= c_hi) {
+        const float* rr = cmb_record(ws, c0 + s, ufirst, NT, C, rec) + (size_t)M * D + r;
+        mv[s] = __ldcg(rr);
+        lv[s] = __ldcg(rr + M);
+      }
+    }
+    float mb = mv[0];
+#pragma unroll
+    for (int s = 1; s < BT; ++s) mb = fmaxf(mb, mv[s]);
+    if (mb > mu) {                       // rescale the running sum to the new max
+      L = (mu == -INFINITY) ? 0.f : L * cmb_exp2(mu - mb);
+      mu = mb;
+    }
+#pragma unroll
+    for (int s = 0; s < BT; ++s)
+      if (mv[s] != -INFINITY) L += lv[s] * cmb_exp2(mv[s] - mu);
   }
   *mu_out = mu;
   *invl_out = 1.f / L;

@@ -177,15 +177,18 @@ def test_launch_count_increments():
     p.close()
 
 
+@pytest.mark.parametrize("path", [2, 3])
 @pytest.mark.parametrize("H_kv,H_q,k,ctas", [(2, 2, 0, 0), (2, 8, 0, 0), (2, 16, 0, 0),
                                              (1, 8, 8, 0), (2, 16, 8, 5), (1, 16, 7, 0),
-                                             (2, 2, 4, 7), (3, 3, 4, 11)])
-def test_tcgen05_verify_path(H_kv, H_q, k, ctas):
-    """The tensor-core verify kernel (forced with BMC_OPT_ATTN_PATH=2) against
-    the oracle: M = G*(1+k_adm) from 1 to 128 query rows per KV head, ragged
-    caps (r=24 does not divide the 64-key tile), split units (ctas=5)."""
+                                             (2, 2, 4, 7), (3, 3, 4, 11), (1, 8, 3, 0),
+                                             (2, 8, 4, 9), (1, 16, 3, 6), (2, 4, 12, 0)])
+def test_tcgen05_verify_path(path, H_kv, H_q, k, ctas):
+    """The tensor-core kernels (BMC_OPT_ATTN_PATH=2: keys on the TMEM lanes
+    for M <= 64, 3: queries on the lanes) against the oracle: M = G*(1+k_adm)
+    from 1 to 128 query rows per KV head (M = 1, 4, 5, 8, 32, 40, 52, 64, 72,
+    128), ragged caps (r=24 divides neither tile), split units (ctas > 0)."""
     p = Pair(2, H_kv, H_q, 128, 24, 300, dtype="bf16", seed=23, ctas=ctas)
-    p.gpu.set_option(bmc.BMC_OPT_ATTN_PATH, 2)
+    p.gpu.set_option(bmc.BMC_OPT_ATTN_PATH, path)
     for _ in range(3):
         p.append()
     p.sdpa()
@@ -201,11 +204,12 @@ def test_tcgen05_verify_path(H_kv, H_q, k, ctas):
     p.close()
 
 
-def test_tcgen05_peaky_long():
-    """Near one-hot rows through the tensor-core path: P is split into
+@pytest.mark.parametrize("path", [2, 3])
+def test_tcgen05_peaky_long(path):
+    """Near one-hot rows through the tensor-core paths: P is split into
     bf16 hi + lo so its rounding stays far inside the 2e-3 budget."""
     p = Pair(2, 2, 16, 128, 64, 1500, dtype="bf16", seed=29, variant="peaky")
-    p.gpu.set_option(bmc.BMC_OPT_ATTN_PATH, 2)
+    p.gpu.set_option(bmc.BMC_OPT_ATTN_PATH, path)
     _decode(p, 1500, check_every=61)
     p.close()
 
@@ -243,7 +247,8 @@ def _random_path(rng, parent, k_adm):
 
 
 @pytest.mark.parametrize("path,H_kv,H_q,k", [(1, 2, 2, 6), (2, 2, 2, 6), (2, 2, 8, 12),
-                                             (1, 1, 4, 26), (2, 1, 4, 26)])
+                                             (1, 1, 4, 26), (2, 1, 4, 26), (3, 2, 8, 12),
+                                             (3, 1, 4, 26)])
 def test_token_tree_speculation(path, H_kv, H_q, k):
     """Token-tree speculation: nodes in BFS order in the padded
     rows, ancestor-rule mask in both attention kernels (CUDA cores: path 1,

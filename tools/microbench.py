@@ -134,8 +134,9 @@ def main():
         # verify shapes: 70B (G=8, t=1+k), L3-8B GQA (G=4), 7B-SD (t=5): CUDA cores vs tcgen05
         out["verify"] = []
         for (B, Hk, Hq, cap, t) in [(8, 8, 64, 8192, 9), (8, 8, 64, 8192, 1),
-                                    (64, 8, 32, 4096, 1), (32, 32, 32, 2048, 5)]:
-            for pa in (1, 2):
+                                    (64, 8, 32, 4096, 1), (32, 32, 32, 2048, 5),
+                                    (8, 8, 64, 8192, 4), (8, 8, 64, 8192, 8)]:
+            for pa in (1, 2, 3):
                 print("config", B, Hk, Hq, cap, t, pa, file=sys.stderr, flush=True)
                 out["verify"].append(attn_at(B, Hk, Hq, 128, cap, t=t, path=pa, reps=20,
                                              layers=4))
