@@ -41,6 +41,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <limits.h>
 #include <math.h>
 #include <stdint.h>
 
@@ -63,27 +64,33 @@ constexpr float kRescale = 8.0f;
 
 template <int N>
 struct Cfg {
-  static_assert(N == 16 || N == 32, "query columns");
+  static_assert(N % 16 == 0 && N >= 16 && N <= 80, "query columns");
   static constexpr int NH = N / 2;                          // columns per softmax half
+  static constexpr int NBP = N < 64 ? 2 : 1;                // P^T buffers
   static constexpr int KS = N <= 16 ? 3 : 2;                // K ring stages
   static constexpr int VS = N <= 32 ? 3 : 2;                // V ring stages
   static constexpr uint32_t OFF_K = 0;
   static constexpr uint32_t OFF_V = OFF_K + KS * kTileBytes;
-  static constexpr uint32_t OFF_Q = OFF_V + VS * kTileBytes;   // [2 dim atoms][N][128 B]
+  static constexpr uint32_t OFF_Q = OFF_V + VS * kTileBytes;   // [2 bufs][2 dim atoms][N][128 B]
   static constexpr uint32_t kQAtom = N * 128;
-  static constexpr uint32_t OFF_P = OFF_Q + 2 * kQAtom;        // [NB][2 key atoms][2N][128 B]
+  static constexpr uint32_t kQBytes = 2 * kQAtom;
+  static constexpr uint32_t OFF_P = OFF_Q + 2 * kQBytes;       // [NBP][2 key atoms][2N][128 B]
   static constexpr uint32_t kPAtom = 2 * N * 128;
   static constexpr uint32_t kPBytes = 2 * kPAtom;
-  static constexpr uint32_t OFF_BAR = OFF_P + NB * kPBytes;
+  static constexpr uint32_t OFF_BAR = OFF_P + NBP * kPBytes;
   static constexpr uint32_t OFF_RED = OFF_BAR + 512;           // [2 halves][4 quadrants][NH] f32
-  static constexpr uint32_t OFF_SUM = OFF_RED + 2 * 4 * NH * 4;
-  static constexpr uint32_t kSmem = OFF_SUM + 2 * 4 * NH * 4 + 16;
+  static constexpr uint32_t OFF_SUM = OFF_RED + 2 * 4 * NH * 4;  // [2][4][NH] f32
+  static constexpr uint32_t OFF_M = OFF_SUM + 2 * 4 * NH * 4;    // [2 halves][2 versions][NH] f32
+  static constexpr uint32_t OFF_A = OFF_M + 2 * 2 * NH * 4;      // [2][NH] rescale factors
+  static constexpr uint32_t OFF_LIM = OFF_A + 2 * NH * 4;        // [2][NH] int visible-key limit
+  static constexpr uint32_t OFF_QM = OFF_LIM + 2 * NH * 4;       // [2][NH] ancestor masks
+  static constexpr uint32_t kSmem = OFF_QM + 2 * NH * 4;
   static_assert(kSmem <= 232448, "shared memory");
   static_assert(kQAtom % 1024 == 0 && kPAtom % 1024 == 0, "SW128 atoms");
-  static_assert(NB * kPBytes >= (4 + 2) * N * 4, "combine scratch in the P area");
+  static_assert(NBP * kPBytes >= (4 + 2) * N * 4, "combine scratch in the P area");
   // TMEM columns: S^T[b] at b*N, O^T (hi N cols, lo N cols) at NB*N
   static constexpr uint32_t TM_O = NB * N;
-  static_assert(NB * N + 2 * N <= 256, "TMEM columns");
+  static constexpr uint32_t kTmemCols = (NB * N + 2 * N <= 256) ? 256 : 512;
 };
 
 #ifdef BMC_TC_TRACE
@@ -100,7 +107,8 @@ __device__ __forceinline__ long long gtime() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(c));
   return c;
 }
-#define TRACE(ev, i) do { if (blockIdx.x == 0 && (i) < 256) g_tck_trace[ev][i] = clk(); } while (0)
+__device__ int g_tck_trace_cta;
+#define TRACE(ev, i) do { if (blockIdx.x == g_tck_trace_cta && (i) < 256) g_tck_trace[ev][i] = clk(); } while (0)
 #else
 #define TRACE(ev, i) do { } while (0)
 #endif
@@ -179,10 +187,10 @@ __device__ __forceinline__ void tmem_st_cols(uint32_t taddr, const float* v) {
   }
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
-__device__ __forceinline__ float warp_max(float x) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) x = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, o));
-  return x;
+__device__ __forceinline__ float warp_max(float x) {   // one CREDUX on sm_100a
+  float y;
+  asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(y) : "f"(x));
+  return y;
 }
 __device__ __forceinline__ float warp_sum(float x) {
 #pragma unroll
@@ -209,11 +217,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
   auto SEMPTY = [&](int b) { return bar0 + 8u * (18 + b); };   // softmax read S^T[b]
   auto PFULL = [&](int b) { return bar0 + 8u * (20 + b); };    // P^T[b] in smem
   auto PEMPTY = [&](int b) { return bar0 + 8u * (22 + b); };   // O^T MMA read P^T[b]
-  const uint32_t QFULL = bar0 + 8u * 24;
-  const uint32_t ODONE = bar0 + 8u * 25;
-  const uint32_t QDONE = bar0 + 8u * 26;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::OFF_BAR + 8 * 28);
-  int* sm_flag = reinterpret_cast<int*>(smem + C::OFF_BAR + 8 * 29);
+  auto QFULL = [&](int b) { return bar0 + 8u * (24 + b); };    // Q buffer b written
+  auto QDONE = [&](int b) { return bar0 + 8u * (26 + b); };    // S^T MMAs done with Q buffer b
+  const uint32_t ODONE = bar0 + 8u * 28;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::OFF_BAR + 8 * 30);
+  int* sm_flag = reinterpret_cast<int*>(smem + C::OFF_BAR + 8 * 31);
+  int* resc_flag = reinterpret_cast<int*>(smem + C::OFF_BAR + 8 * 32);   // [2 halves]
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -233,17 +242,21 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
     for (int b = 0; b < NB; ++b) {
       mbar_init(SFULL(b), 1);
       mbar_init(SEMPTY(b), 256);
+    }
+    for (int b = 0; b < C::NBP; ++b) {
       mbar_init(PFULL(b), 256);
       mbar_init(PEMPTY(b), 1);
     }
-    mbar_init(QFULL, 256);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(QFULL(b), 256);
+      mbar_init(QDONE(b), 1);
+    }
     mbar_init(ODONE, 1);
-    mbar_init(QDONE, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
-                     su32(tmem_slot)));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     su32(tmem_slot)), "n"(C::kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   // fused KV-cache update: the pending appended / drafted rows that
@@ -309,16 +322,16 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
     // ------------------------------------------------------ S^T = K Q^T issuer
     if (lane == 0) {
       constexpr uint32_t IQK = idesc_bf16(KT, N, 0, 0);
-      const uint32_t qs = sbase + C::OFF_Q;
       int ks = 0;
-      uint32_t kph = 0, qph = 0;
+      uint32_t kph = 0;
       long long i = t_begin;
-      int tcount = 0;
+      int tcount = 0, item = 0;
       while (i < t_end) {
         const long long u = i / p.tpu;
         const long long iend = min(t_end, (u + 1) * p.tpu);
-        mbar_wait(QFULL, qph);
-        qph ^= 1;
+        const int qb = item & 1;
+        const uint32_t qs = sbase + C::OFF_Q + qb * C::kQBytes;
+        mbar_wait(QFULL(qb), (item >> 1) & 1);
         fence_after();
         const int n = (int)(iend - i);
         for (int k = 0; k < n; ++k) {
@@ -342,8 +355,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
           umma_commit(EMPTYK(ks));
           if (++ks == C::KS) { ks = 0; kph ^= 1; }
         }
-        umma_commit(QDONE);
+        umma_commit(QDONE(qb));
         tcount += n;
+        ++item;
         i = iend;
       }
     }
@@ -361,8 +375,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
         const int n = (int)(iend - i);
         for (int k = 0; k < n; ++k) {
           const int tc = tcount + k;
-          const int b = tc % NB;
-          mbar_wait(PFULL(b), (tc / NB) & 1);
+          const int b = tc % C::NBP;
+          mbar_wait(PFULL(b), (tc / C::NBP) & 1);
           TRACE(5, tc);
           mbar_wait(FULLV(vs), vph);
           TRACE(6, tc);
@@ -394,46 +408,73 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
     const int stid = threadIdx.x - 64;
     float* red = reinterpret_cast<float*>(smem + C::OFF_RED) + h * 4 * NH;   // [4][NH]
     float* sums = reinterpret_cast<float*>(smem + C::OFF_SUM) + h * 4 * NH;  // [4][NH]
+    float* msm = reinterpret_cast<float*>(smem + C::OFF_M) + h * 2 * NH;     // [2 versions][NH]
+    float* asm_ = reinterpret_cast<float*>(smem + C::OFF_A) + h * NH;        // rescale factors
+    int* lim = reinterpret_cast<int*>(smem + C::OFF_LIM) + h * NH;           // keys < lim visible
+    uint32_t* qmk = reinterpret_cast<uint32_t*>(smem + C::OFF_QM) + h * NH;  // + these drafts
     // P^T store address of key kl: key atom kl/64, 16-byte chunk (kl%64)/8 (swizzled by row)
     const uint32_t pkey = (uint32_t)(kl >> 6) * C::kPAtom + (uint32_t)(kl & 7) * 2;
     const uint32_t pchunk = (uint32_t)((kl & 63) >> 3);
-    uint32_t oph = 0, qdph = 0;
+    // Q rows of the item starting at tile x0 (zero beyond M) into Q buffer qb
+    auto load_q = [&](long long x0, int qb) {
+      const long long uq = x0 / p.tpu;
+      const int bq = (int)(uq / p.H_kv), gq = (int)(uq % p.H_kv);
+      const size_t r0 = ((size_t)bq * p.H_q + (size_t)gq * p.G) * p.t;
+      for (int x = stid; x < N * 16; x += 256) {
+        const int m = x >> 4, c = x & 15;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (m < p.M) v = *reinterpret_cast<const uint4*>(p.Q + (r0 + m) * D + c * 8);
+        const uint32_t off = (uint32_t)qb * C::kQBytes + (uint32_t)(c >> 3) * C::kQAtom +
+                             (uint32_t)m * 128 + ((((uint32_t)c & 7u) ^ ((uint32_t)m & 7u)) << 4);
+        *reinterpret_cast<uint4*>(smem + C::OFF_Q + off) = v;
+      }
+      fence_proxy_smem();
+      mbar_arrive(QFULL(qb));
+    };
+    uint32_t oph = 0;
     long long i = t_begin;
-    int tcount = 0;
-    bool first_item = true;
+    int tcount = 0, item = 0;
+    if (i < t_end) load_q(i, 0);
     while (i < t_end) {
       const long long u = i / p.tpu;
       const long long iend = min(t_end, (u + 1) * p.tpu);
       const int b_ = (int)(u / p.H_kv), g_ = (int)(u % p.H_kv);
       const int j0 = (int)(i % p.tpu);
       const size_t qrow0 = ((size_t)b_ * p.H_q + (size_t)g_ * p.G) * p.t;   // first query row
-      if (!first_item) {
-        mbar_wait(QDONE, qdph);
-        qdph ^= 1;
+      // prefetch the next item's Q into the other buffer once the S^T MMAs of
+      // the item before this one are done with it
+      if (iend < t_end) {
+        if (item >= 1) mbar_wait(QDONE((item - 1) & 1), ((item - 1) >> 1) & 1);
+        load_q(iend, (item + 1) & 1);
       }
-      // Q rows (zero beyond M) into the K-major SW128 B operand
-      for (int x = stid; x < N * 16; x += 256) {
-        const int m = x >> 4, c = x & 15;
-        uint4 v = make_uint4(0, 0, 0, 0);
-        if (m < p.M) v = *reinterpret_cast<const uint4*>(p.Q + (qrow0 + m) * D + c * 8);
-        const uint32_t off = (uint32_t)(c >> 3) * C::kQAtom + (uint32_t)m * 128 +
-                             ((((uint32_t)c & 7u) ^ ((uint32_t)m & 7u)) << 4);
-        *reinterpret_cast<uint4*>(smem + C::OFF_Q + off) = v;
-      }
-      fence_proxy_smem();
-      mbar_arrive(QFULL);
       const int vb_ = p.valid[b_];
-      const int mcols = p.M - h * NH;    // active query columns of this half
-      float m_use[NH], l[NH];
-#pragma unroll
-      for (int c = 0; c < NH; ++c) {
-        m_use[c] = -INFINITY;
-        l[c] = 0.f;
+      // per-column state of this half, written by the half's quadrant-0 warp
+      // (ordered before its first use by the first tile's barrier-reduction):
+      // running max (version 0) = -inf, visibility rule (chain: keys < valid_b
+      // + tau; tree: committed keys + the node's ancestors)
+      int mv = 0;                          // current version of msm
+      if (q == 0) {
+        for (int c = lane; c < NH; c += 32) {
+          const int m = h * NH + c;
+          const int tau = m % p.t;
+          msm[c] = -INFINITY;
+          lim[c] = m < p.M ? vb_ + (p.tree ? 0 : tau) : INT_MIN;
+          qmk[c] = (m < p.M && p.tree && tau > 0) ? p.anc[tau - 1] : 0u;
+        }
       }
+      half_sync(h);
+      float l[NH];
+#pragma unroll
+      for (int c = 0; c < NH; ++c) l[c] = 0.f;
+      // columns of this half that are real queries (the rest is padding)
+      const int mcols = p.M - h * NH;
+      const uint64_t colmask =
+          mcols <= 0 ? 0ull : (mcols >= 64 ? ~0ull : ((1ull << mcols) - 1ull));
       const int n = (int)(iend - i);
       for (int k = 0; k < n; ++k) {
         const int tc = tcount + k;
         const int bb = tc % NB;
+        const int pb = tc % C::NBP;
         const long long kidx = (long long)(j0 + k) * KT + kl;   // this thread's key row
         if (stid == 0) TRACE(8, tc);
         mbar_wait(SFULL(bb), (tc / NB) & 1);
@@ -443,28 +484,33 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
         tmem_ld_cols<NH>(tmem + bb * N + h * NH + lane_addr, x);
         fence_before();
         mbar_arrive(SEMPTY(bb));
-        // mask (chain: keys < valid_b + tau; tree: committed keys + ancestors)
-        // and log2 scaling; columns >= M are padding.  Only the tiles that
-        // reach past the committed rows need the per-column rule.
-        bool need = false;
-        if ((long long)(j0 + k + 1) * KT <= vb_) {
-#pragma unroll
-          for (int c = 0; c < NH; ++c) {
-            x[c] = c < mcols ? x[c] * p.qscale : -INFINITY;
-            need |= x[c] > m_use[c] + kRescale;
-          }
-        } else {
+        // mask + log2 scaling.  Tiles inside the committed rows see every real
+        // column; the (at most two per item) tiles reaching past them build
+        // the per-column visibility in a compact loop (cold code stays small:
+        // an instruction-cache miss costs an L2 round trip under full HBM load)
+        uint64_t vm = colmask;
+        if ((long long)(j0 + k + 1) * KT > vb_) {
           const long long js = kidx - vb_;
-#pragma unroll
+          vm = 0;
+#pragma unroll 1
           for (int c = 0; c < NH; ++c) {
-            bool vis = c < mcols;
-            if (vis) {
-              const int tau = (h * NH + c) % p.t;
-              vis = kidx < (long long)vb_ + (p.tree ? 0 : tau) ||
-                    (p.tree && tau > 0 && js >= 0 && js < 32 && ((p.anc[tau - 1] >> js) & 1u));
-            }
-            x[c] = vis ? x[c] * p.qscale : -INFINITY;
-            need |= x[c] > m_use[c] + kRescale;
+            const uint32_t qm = qmk[c];
+            const bool v = kidx < (long long)lim[c] || (js >= 0 && js < 32 && ((qm >> js) & 1u));
+            vm |= (uint64_t)v << c;
+          }
+        }
+        const float* mcur = msm + mv * NH;
+        bool need = false;
+#pragma unroll
+        for (int c0 = 0; c0 < NH; c0 += 8) {
+          float mr[8];
+          *reinterpret_cast<float4*>(mr) = *reinterpret_cast<const float4*>(mcur + c0);
+          *reinterpret_cast<float4*>(mr + 4) = *reinterpret_cast<const float4*>(mcur + c0 + 4);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int c = c0 + e;
+            x[c] = ((vm >> c) & 1ull) ? x[c] * p.qscale : -INFINITY;
+            need |= x[c] > mr[e] + kRescale;
           }
         }
         const bool any_ = half_any(h, need);
@@ -477,57 +523,84 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
             if (lane == 0) red[q * NH + c] = wm;
           }
           half_sync(h);
-          bool resc = false;
-          float alpha[NH];
-#pragma unroll
-          for (int c = 0; c < NH; ++c) {
-            const float mt =
-                fmaxf(fmaxf(red[c], red[NH + c]), fmaxf(red[2 * NH + c], red[3 * NH + c]));
-            alpha[c] = 1.f;
-            if (mt > m_use[c] + kRescale) {
-              alpha[c] = (m_use[c] == -INFINITY) ? 0.f : fast_exp2(m_use[c] - mt);
-              m_use[c] = mt;
-              l[c] *= alpha[c];
-              resc |= (alpha[c] != 1.f);
+          // the quadrant-0 warp moves the running maxima into the other
+          // version (readers of the current one are ordered by the barriers)
+          if (q == 0) {
+            const float* mold = msm + mv * NH;
+            float* mnew = msm + (mv ^ 1) * NH;
+            bool resc = false;
+            for (int c = lane; c < NH; c += 32) {
+              const float mt =
+                  fmaxf(fmaxf(red[c], red[NH + c]), fmaxf(red[2 * NH + c], red[3 * NH + c]));
+              const float mo = mold[c];
+              float mnx = mo, alpha = 1.f;
+              if (mt > mo + kRescale) {
+                alpha = (mo == -INFINITY) ? 0.f : fast_exp2(mo - mt);
+                mnx = mt;
+                resc |= (mo != -INFINITY);
+              }
+              mnew[c] = mnx;
+              asm_[c] = alpha;
             }
+            resc = __any_sync(0xffffffffu, resc);
+            if (lane == 0) resc_flag[h] = resc;
+          }
+          half_sync(h);
+          mv ^= 1;
+#pragma unroll
+          for (int c0 = 0; c0 < NH; c0 += 4) {
+            const float4 a4 = *reinterpret_cast<const float4*>(asm_ + c0);
+            l[c0] *= a4.x;
+            l[c0 + 1] *= a4.y;
+            l[c0 + 2] *= a4.z;
+            l[c0 + 3] *= a4.w;
           }
           // O^T columns of this half (rows = dims of this quadrant) are
           // rescaled once the previous tile's O^T MMAs have completed
-          if (resc && k > 0) {
+          if (resc_flag[h] && k > 0) {
             const int tp = tc - 1;
-            mbar_wait(PEMPTY(tp % NB), (tp / NB) & 1);
+            mbar_wait(PEMPTY(tp % C::NBP), (tp / C::NBP) & 1);
             fence_after();
+#pragma unroll 1
+            for (int cc = 0; cc < 2 * NH; cc += 8) {
+              const int hl = cc >= NH, c0 = cc - hl * NH;
+              float ov[8];
+              const uint32_t ta = tmem + C::TM_O + hl * N + h * NH + c0 + lane_addr;
+              tmem_ld_cols<8>(ta, ov);
 #pragma unroll
-            for (int hl = 0; hl < 2; ++hl) {
-              float ov[NH];
-              const uint32_t ta = tmem + C::TM_O + hl * N + h * NH + lane_addr;
-              tmem_ld_cols<NH>(ta, ov);
-#pragma unroll
-              for (int c = 0; c < NH; ++c) ov[c] *= alpha[c];
-              tmem_st_cols<NH>(ta, ov);
+              for (int e = 0; e < 8; ++e) ov[e] *= asm_[c0 + e];
+              tmem_st_cols<8>(ta, ov);
             }
             fence_before();
           }
         }
-        // P^T[bb] was last read by the O^T MMAs of tile tc - NB
+        // P^T[pb] was last read by the O^T MMAs of tile tc - NBP
         if (stid == 0) TRACE(11, tc);
-        if (tc >= NB) mbar_wait(PEMPTY(bb), ((tc / NB) - 1) & 1);
+        if (tc >= C::NBP) mbar_wait(PEMPTY(pb), ((tc / C::NBP) - 1) & 1);
         if (stid == 0) TRACE(12, tc);
-        const uint32_t pbase = sbase + C::OFF_P + bb * C::kPBytes + pkey;
+        const uint32_t pbase = sbase + C::OFF_P + pb * C::kPBytes + pkey;
+        const float* mu = msm + mv * NH;
 #pragma unroll
-        for (int c = 0; c < NH; ++c) {
-          // a column still at m = -inf has seen only masked keys (x = -inf): P = 0
-          const float pv = fast_exp2(x[c] - (m_use[c] == -INFINITY ? 0.f : m_use[c]));
-          l[c] += pv;
-          const uint32_t bits = __float_as_uint(pv);
-          const float hi = __uint_as_float(bits & 0xffff0000u);
-          const uint32_t lo = (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(pv - hi));
-          const uint32_t rh = (uint32_t)(h * NH + c), rl = rh + N;   // P^T rows: hi, lo
-          sts_u16(pbase + rh * 128 + ((pchunk ^ (rh & 7u)) << 4), bits >> 16);
-          sts_u16(pbase + rl * 128 + ((pchunk ^ (rl & 7u)) << 4), lo);
+        for (int c0 = 0; c0 < NH; c0 += 8) {
+          float mr[8];
+          *reinterpret_cast<float4*>(mr) = *reinterpret_cast<const float4*>(mu + c0);
+          *reinterpret_cast<float4*>(mr + 4) = *reinterpret_cast<const float4*>(mu + c0 + 4);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int c = c0 + e;
+            // a column still at m = -inf has seen only masked keys (x = -inf): P = 0
+            const float pv = fast_exp2(x[c] - (mr[e] == -INFINITY ? 0.f : mr[e]));
+            l[c] += pv;
+            const uint32_t bits = __float_as_uint(pv);
+            const float hi = __uint_as_float(bits & 0xffff0000u);
+            const uint32_t lo = (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(pv - hi));
+            const uint32_t rh = (uint32_t)(h * NH + c), rl = rh + N;   // P^T rows: hi, lo
+            sts_u16(pbase + rh * 128 + ((pchunk ^ (rh & 7u)) << 4), bits >> 16);
+            sts_u16(pbase + rl * 128 + ((pchunk ^ (rl & 7u)) << 4), lo);
+          }
         }
         fence_proxy_smem();
-        mbar_arrive(PFULL(bb));
+        mbar_arrive(PFULL(pb));
         if (stid == 0) TRACE(13, tc);
       }
       // ---- epilogue of this item: column sums, O^T (TMEM) -> output / record
@@ -536,8 +609,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
         const float ws_ = warp_sum(l[c]);
         if (lane == 0) sums[q * NH + c] = ws_;
       }
+      if (stid == 0) TRACE(14, tcount);
       mbar_wait(ODONE, oph);
       oph ^= 1;
+      if (stid == 0) TRACE(15, tcount);
       fence_after();
       half_sync(h);
       const long long ufirst = u * p.tpu, ulast = ufirst + p.tpu - 1;
@@ -545,23 +620,28 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
       const int c_hi = cta_of_tile(ulast, NT, p.ctas);
       const int nseg = c_hi - c_lo + 1;
       const size_t rec = rec_floats(p.M, D);
-      float* my = p.ws + ((size_t)blockIdx.x * 2 + (first_item ? 0 : 1)) * rec;
-      float o_hi[NH], o_lo[NH];
-      tmem_ld_cols<NH>(tmem + C::TM_O + h * NH + lane_addr, o_hi);
-      tmem_ld_cols<NH>(tmem + C::TM_O + N + h * NH + lane_addr, o_lo);
+      float* my = p.ws + ((size_t)blockIdx.x * 2 + (item == 0 ? 0 : 1)) * rec;
+      const float* mfin = msm + mv * NH;
+#pragma unroll 1
+      for (int c0 = 0; c0 < NH; c0 += 8) {
+        float o_hi[8], o_lo[8];
+        tmem_ld_cols<8>(tmem + C::TM_O + h * NH + c0 + lane_addr, o_hi);
+        tmem_ld_cols<8>(tmem + C::TM_O + N + h * NH + c0 + lane_addr, o_lo);
 #pragma unroll
-      for (int c = 0; c < NH; ++c) {
-        const int m = h * NH + c;
-        if (m < p.M) {
-          const float L = (sums[c] + sums[NH + c]) + (sums[2 * NH + c] + sums[3 * NH + c]);
-          const float o = o_hi[c] + o_lo[c];
-          if (nseg == 1) {
-            p.O[(qrow0 + m) * D + kl] = o / L;
-          } else {
-            my[(size_t)m * D + kl] = o;
-            if (kl == 0) {
-              my[(size_t)p.M * D + m] = m_use[c];
-              my[(size_t)p.M * D + p.M + m] = L;
+        for (int e = 0; e < 8; ++e) {
+          const int c = c0 + e;
+          const int m = h * NH + c;
+          if (m < p.M) {
+            const float L = (sums[c] + sums[NH + c]) + (sums[2 * NH + c] + sums[3 * NH + c]);
+            const float o = o_hi[e] + o_lo[e];
+            if (nseg == 1) {
+              p.O[(qrow0 + m) * D + kl] = o / L;
+            } else {
+              my[(size_t)m * D + kl] = o;
+              if (kl == 0) {
+                my[(size_t)p.M * D + m] = mfin[c];
+                my[(size_t)p.M * D + p.M + m] = L;
+              }
             }
           }
         }
@@ -584,9 +664,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
           if (stid == 0) p.counters[u] = 0;
         }
       }
-      softmax_sync();   // sums / flag reuse by the next item
+      softmax_sync();   // sums / column state / flag reuse by the next item
+      if (stid == 0) TRACE(14, tcount + 1);
       tcount += n;
-      first_item = false;
+      ++item;
       i = iend;
     }
   }
@@ -597,7 +678,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
   if (threadIdx.x == 0) { g_tck_cta[blockIdx.x][2] = clk(); g_tck_cta[blockIdx.x][3] = gtime(); }
 #endif
   if (warp == 1) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "n"(C::kTmemCols));
   }
 }
 
@@ -606,6 +688,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
 // ------------------------------------------------------------------ host
 
 #ifdef BMC_TC_TRACE
+extern "C" int bmc_tck_trace_cta(int c) {
+  return cudaMemcpyToSymbol(tck::g_tck_trace_cta, &c, sizeof(int)) == cudaSuccess ? 0 : -1;
+}
 extern "C" int bmc_tck_trace(long long* out) {   // [16][256] tile events, then [160][4] CTAs
   if (cudaMemcpyFromSymbol(out, tck::g_tck_trace, sizeof(long long) * 16 * 256) != cudaSuccess)
     return -1;
@@ -615,7 +700,7 @@ extern "C" int bmc_tck_trace(long long* out) {   // [16][256] tile events, then 
 #endif
 
 bool attn_tck_supported(int D, int dtype, int M) {
-  return D == 128 && dtype == BMC_BF16 && M >= 1 && M <= 32 && encode_fn() != nullptr;
+  return D == 128 && dtype == BMC_BF16 && M >= 1 && M <= 80 && encode_fn() != nullptr;
 }
 
 template <int N>
@@ -673,7 +758,10 @@ cudaError_t launch_attn_tck(const AttnStepArgs& a, int num_sms, cudaStream_t s) 
   p.ctas = ctas;
   if (p.total_tiles == 0) return cudaSuccess;
   if (p.M <= 16) return launch_n<16>(p, ctas, s);
-  return launch_n<32>(p, ctas, s);
+  if (p.M <= 32) return launch_n<32>(p, ctas, s);
+  if (p.M <= 48) return launch_n<48>(p, ctas, s);
+  if (p.M <= 64) return launch_n<64>(p, ctas, s);
+  return launch_n<80>(p, ctas, s);
 }
 
 }  // namespace bmc

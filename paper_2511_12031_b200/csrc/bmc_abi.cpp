@@ -493,9 +493,10 @@ int bmc_sdpa(bmc_t h, const void* Q, int n_valid, float* O) {
   // 2.1x at M=5), CUDA cores keep M <= 2 (6.2-6.4 TB/s at M=1)
   const bool use_tc = h->attn_path >= 2 ||
                       (h->attn_path == 0 && M > kTcMinM && bmc::attn_tc_supported(h->D, h->dt, M));
-  // keys on the TMEM lanes for M <= 64 (attn_tck.cu), queries on the lanes
+  // keys on the TMEM lanes for M <= 80 (attn_tck.cu), queries on the lanes
   // above that or when forced (path 3)
-  const bool use_tck = use_tc && h->attn_path != 3 && bmc::attn_tck_supported(h->D, h->dt, M);
+  const bool use_tck = use_tc && h->attn_path != 3 && M <= 64 &&
+                       bmc::attn_tck_supported(h->D, h->dt, M);
   if (use_tc) {
     if (!bmc::attn_tc_supported(h->D, h->dt, M))
       return fail(BMC_ERR_UNSUPPORTED, "tcgen05 path needs bf16, D=128, G*t<=128");

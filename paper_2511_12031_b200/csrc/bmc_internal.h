@@ -93,7 +93,7 @@ cudaError_t launch_attn_step(const AttnStepArgs& a, int num_sms, cudaStream_t s)
 bool attn_tc_supported(int D, int dtype, int M);
 cudaError_t launch_attn_tc(const AttnStepArgs& a, int num_sms, cudaStream_t s);
 // tcgen05 attention with the keys on the TMEM lanes (attn_tck.cu; bf16,
-// D = 128, M = G*t <= 64): the default tensor-core kernel for small M.
+// D = 128, M = G*t <= 80): the default tensor-core kernel up to M = 80.
 bool attn_tck_supported(int D, int dtype, int M);
 cudaError_t launch_attn_tck(const AttnStepArgs& a, int num_sms, cudaStream_t s);
 

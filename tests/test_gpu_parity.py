@@ -181,12 +181,13 @@ def test_launch_count_increments():
 @pytest.mark.parametrize("H_kv,H_q,k,ctas", [(2, 2, 0, 0), (2, 8, 0, 0), (2, 16, 0, 0),
                                              (1, 8, 8, 0), (2, 16, 8, 5), (1, 16, 7, 0),
                                              (2, 2, 4, 7), (3, 3, 4, 11), (1, 8, 3, 0),
-                                             (2, 8, 4, 9), (1, 16, 3, 6), (2, 4, 12, 0)])
+                                             (2, 8, 4, 9), (1, 16, 3, 6), (2, 4, 12, 0),
+                                             (1, 8, 9, 4), (2, 6, 7, 0)])
 def test_tcgen05_verify_path(path, H_kv, H_q, k, ctas):
     """The tensor-core kernels (BMC_OPT_ATTN_PATH=2: keys on the TMEM lanes
-    for M <= 64, 3: queries on the lanes) against the oracle: M = G*(1+k_adm)
-    from 1 to 128 query rows per KV head (M = 1, 4, 5, 8, 32, 40, 52, 64, 72,
-    128), ragged caps (r=24 divides neither tile), split units (ctas > 0)."""
+    for M <= 80, 3: queries on the lanes) against the oracle: M = G*(1+k_adm)
+    from 1 to 128 query rows per KV head (M = 1, 4, 5, 8, 24, 32, 40, 52, 64,
+    72, 80, 128), ragged caps (r=24 divides neither tile), split units."""
     p = Pair(2, H_kv, H_q, 128, 24, 300, dtype="bf16", seed=23, ctas=ctas)
     p.gpu.set_option(bmc.BMC_OPT_ATTN_PATH, path)
     for _ in range(3):

@@ -9,6 +9,8 @@ from tools.microbench import attn_at
 from paper_2511_12031_b200 import bmc
 L = bmc.load()
 B, Hk, Hq, cap, t = (int(x) for x in sys.argv[1:6])
+tcta = int(sys.argv[6]) if len(sys.argv) > 6 else 0
+L.bmc_tck_trace_cta(tcta)
 print(attn_at(B, Hk, Hq, 128, cap, t=t, path=2, reps=2, layers=1))
 buf = (ctypes.c_longlong * (16 * 256 + 160 * 4))()
 L.bmc_tck_trace.argtypes = [ctypes.c_void_p]
@@ -16,12 +18,14 @@ assert L.bmc_tck_trace(buf) == 0
 a = np.array(buf[:])
 tr = a[:16 * 256].reshape(16, 256)
 cta = a[16 * 256:].reshape(160, 4)[:148]
-base = cta[0, 0]
+base = cta[tcta, 0]
 names = ["K issue", "V issue", "QK fullK", "QK Sempty", "QK issued", "PV pfull", "PV fullV",
-         "PV issued", "sm pre-S", "sm S", "sm any", "sm preP", "sm Pempty", "sm Pfull"]
+         "PV issued", "sm pre-S", "sm S", "sm any", "sm preP", "sm Pempty", "sm Pfull",
+         "pre-ODONE", "ODONE"]
 print("tile " + " ".join(f"{n:>9s}" for n in names))
-for i in range(0, 30):
-    print(f"{i:4d} " + " ".join(f"{(tr[e][i] - base) if tr[e][i] else -1:9d}" for e in range(14)))
+for i in range(0, 32):
+    print(f"{i:4d} " + " ".join(f"{(tr[e][i] - base) if tr[e][i] else -1:9d}" for e in range(16)))
+print("CTA end (cycles from its start):", cta[tcta, 2] - cta[tcta, 0])
 cyc = cta[:, 2] - cta[:, 0]; ns = cta[:, 3] - cta[:, 1]
 t0 = cta[:, 1].min()
 ok = ns > 0
