@@ -493,10 +493,12 @@ int bmc_sdpa(bmc_t h, const void* Q, int n_valid, float* O) {
   // 2.1x at M=5), CUDA cores keep M <= 2 (6.2-6.4 TB/s at M=1)
   const bool use_tc = h->attn_path >= 2 ||
                       (h->attn_path == 0 && M > kTcMinM && bmc::attn_tc_supported(h->D, h->dt, M));
-  // keys on the TMEM lanes for M <= 80 (attn_tck.cu), queries on the lanes
-  // above that or when forced (path 3)
-  const bool use_tck = use_tc && h->attn_path != 3 && M <= 64 &&
-                       bmc::attn_tck_supported(h->D, h->dt, M);
+  // keys on the TMEM lanes (attn_tck.cu) for M <= 64 or when forced (path 4),
+  // queries on the lanes above that or when forced (path 3)
+  const bool use_tck = use_tc && h->attn_path != 3 &&
+                       (h->attn_path == 4 || M <= 64) && bmc::attn_tck_supported(h->D, h->dt, M);
+  if (h->attn_path == 4 && !use_tck)
+    return fail(BMC_ERR_UNSUPPORTED, "keys-on-lanes tcgen05 path needs bf16, D=128, G*t<=80");
   if (use_tc) {
     if (!bmc::attn_tc_supported(h->D, h->dt, M))
       return fail(BMC_ERR_UNSUPPORTED, "tcgen05 path needs bf16, D=128, G*t<=128");
@@ -872,7 +874,7 @@ int bmc_set_option(bmc_t h, int key, long long value) {
       h->attn_ctas = (int)value;
       return 0;
     case BMC_OPT_ATTN_PATH:
-      if (value < 0 || value > 3) return fail(BMC_ERR_ARG, "path");
+      if (value < 0 || value > 4) return fail(BMC_ERR_ARG, "path");
       h->attn_path = (int)value;
       return 0;
     case BMC_OPT_ARENA:
