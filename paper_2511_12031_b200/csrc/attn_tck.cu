@@ -45,6 +45,8 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <unordered_map>
+
 #include "bmc_internal.h"
 #include "combine.cuh"
 #include "tc_common.cuh"
@@ -113,8 +115,9 @@ __device__ int g_tck_trace_cta;
 #define TRACE(ev, i) do { } while (0)
 #endif
 
-struct Params {
-  CUtensorMap tmK;   // [U*cap rows][128] bf16, box 64 x 128, SWIZZLE_128B
+// One layer of a launch (a decode step fuses up to 32 layers of one shape)
+struct LayerP {
+  CUtensorMap tmK;          // [U*cap rows][128] bf16, box 64 x 128, SWIZZLE_128B
   CUtensorMap tmV;
   const __nv_bfloat16* Q;   // [B][H_q][t][D]
   float* O;                 // [B][H_q][t][D]
@@ -124,11 +127,16 @@ struct Params {
   const uint8_t* Vd;
   uint8_t* Kc;              // cache base (pending rows are stored here)
   uint8_t* Vc;
+  float* ws;                // split-K partial records of this layer
+  int* counters;            // [U]
+};
+template <int MAXL>
+struct Params {
+  LayerP lay[MAXL];
+  int L;
   int n_app, n_draft, kd_stride;
-  float* ws;
-  int* counters;
-  long long cap;
-  long long total_tiles;
+  long long cap;            // rows per unit (every layer of a launch)
+  long long total_tiles;    // L * U * tpu
   int tpu, U, H_kv, H_q, G, t, M, ctas;
   float qscale;
   int tree;
@@ -198,8 +206,8 @@ __device__ __forceinline__ float warp_sum(float x) {
   return x;
 }
 
-template <int N>
-__global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_constant__ Params p) {
+template <int N, int MAXL>
+__global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_constant__ Params<MAXL> p) {
   using C = Cfg<N>;
   constexpr int NH = C::NH;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -266,7 +274,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
     const int per_unit = (p.n_app + p.n_draft) * 2 * CHR;
     const long long u0 = t_begin / p.tpu, u1 = (t_end - 1) / p.tpu;
     for (long long x = threadIdx.x; x < (u1 - u0 + 1) * per_unit; x += kThreads) {
-      const long long uu = u0 + x / per_unit;
+      const long long gu = u0 + x / per_unit;          // global unit: layer * U + unit
+      const LayerP& ly = p.lay[MAXL == 1 ? 0 : (int)(gu / p.U)];
+      const long long uu = gu % p.U;
       const int y = (int)(x % per_unit);
       const int ck = y % CHR, tensor = (y / CHR) & 1, ri = y / (2 * CHR);
       const int vb = p.valid[(int)(uu / p.H_kv)];
@@ -274,16 +284,16 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
       const uint8_t* src;
       if (p.n_app && ri == 0) {
         row = vb - 1;
-        src = (tensor ? p.Vnew : p.Knew) + (size_t)uu * (D * 2);
+        src = (tensor ? ly.Vnew : ly.Knew) + (size_t)uu * (D * 2);
       } else {
         const int di = ri - p.n_app;
         row = vb + di;
-        src = (tensor ? p.Vd : p.Kd) + ((size_t)uu * p.kd_stride + di) * (D * 2);
+        src = (tensor ? ly.Vd : ly.Kd) + ((size_t)uu * p.kd_stride + di) * (D * 2);
       }
-      const long long tile = uu * p.tpu + row / KT;
+      const long long tile = gu * p.tpu + row / KT;
       if (tile < t_begin || tile >= t_end) continue;
       const uint4 v = *reinterpret_cast<const uint4*>(src + ck * 16);
-      *reinterpret_cast<uint4*>((tensor ? p.Vc : p.Kc) + ((size_t)uu * p.cap + row) * (D * 2) +
+      *reinterpret_cast<uint4*>((tensor ? ly.Vc : ly.Kc) + ((size_t)uu * p.cap + row) * (D * 2) +
                                 ck * 16) = v;
     }
     asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -297,24 +307,25 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
     // ------------------------------------------------------ TMA producers
     if (lane == 0) {
       const bool isK = warp == 0;
-      const CUtensorMap* tm = isK ? &p.tmK : &p.tmV;
       const int NS = isK ? C::KS : C::VS;
       const uint32_t ring = sbase + (isK ? C::OFF_K : C::OFF_V);
       const uint64_t pol = evict_first_policy();
       int s = 0;
       uint32_t ph = 0;
-      long long u = t_begin / p.tpu;
+      long long gu = t_begin / p.tpu;               // global unit
       int j = (int)(t_begin % p.tpu);
       for (long long i = t_begin; i < t_end; ++i) {
         mbar_wait(isK ? EMPTYK(s) : EMPTYV(s), ph ^ 1);
         TRACE(isK ? 0 : 1, (int)(i - t_begin));
-        const int row = (int)(u * p.cap + (long long)j * KT);
+        const LayerP& ly = p.lay[MAXL == 1 ? 0 : (int)(gu / p.U)];
+        const CUtensorMap* tm = isK ? &ly.tmK : &ly.tmV;
+        const int row = (int)((gu % p.U) * p.cap + (long long)j * KT);
         const uint32_t dst = ring + s * kTileBytes;
         const uint32_t fb = isK ? FULLK(s) : FULLV(s);
         mbar_expect_tx(fb, kTileBytes);
         tma_load_2d(dst, tm, 0, row, fb, pol);
         tma_load_2d(dst + kBox, tm, 64, row, fb, pol);
-        if (++j == p.tpu) { j = 0; ++u; }
+        if (++j == p.tpu) { j = 0; ++gu; }
         if (++s == NS) { s = 0; ph ^= 1; }
       }
     }
@@ -327,8 +338,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
       long long i = t_begin;
       int tcount = 0, item = 0;
       while (i < t_end) {
-        const long long u = i / p.tpu;
-        const long long iend = min(t_end, (u + 1) * p.tpu);
+        const long long gu = i / p.tpu;
+        const long long iend = min(t_end, (gu + 1) * p.tpu);
         const int qb = item & 1;
         const uint32_t qs = sbase + C::OFF_Q + qb * C::kQBytes;
         mbar_wait(QFULL(qb), (item >> 1) & 1);
@@ -417,13 +428,15 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
     const uint32_t pchunk = (uint32_t)((kl & 63) >> 3);
     // Q rows of the item starting at tile x0 (zero beyond M) into Q buffer qb
     auto load_q = [&](long long x0, int qb) {
-      const long long uq = x0 / p.tpu;
+      const long long guq = x0 / p.tpu;
+      const __nv_bfloat16* Qs = p.lay[MAXL == 1 ? 0 : (int)(guq / p.U)].Q;
+      const long long uq = guq % p.U;
       const int bq = (int)(uq / p.H_kv), gq = (int)(uq % p.H_kv);
       const size_t r0 = ((size_t)bq * p.H_q + (size_t)gq * p.G) * p.t;
       for (int x = stid; x < N * 16; x += 256) {
         const int m = x >> 4, c = x & 15;
         uint4 v = make_uint4(0, 0, 0, 0);
-        if (m < p.M) v = *reinterpret_cast<const uint4*>(p.Q + (r0 + m) * D + c * 8);
+        if (m < p.M) v = *reinterpret_cast<const uint4*>(Qs + (r0 + m) * D + c * 8);
         const uint32_t off = (uint32_t)qb * C::kQBytes + (uint32_t)(c >> 3) * C::kQAtom +
                              (uint32_t)m * 128 + ((((uint32_t)c & 7u) ^ ((uint32_t)m & 7u)) << 4);
         *reinterpret_cast<uint4*>(smem + C::OFF_Q + off) = v;
@@ -436,8 +449,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
     int tcount = 0, item = 0;
     if (i < t_end) load_q(i, 0);
     while (i < t_end) {
-      const long long u = i / p.tpu;
-      const long long iend = min(t_end, (u + 1) * p.tpu);
+      const long long gu = i / p.tpu;                // global unit: layer * U + unit
+      const long long iend = min(t_end, (gu + 1) * p.tpu);
+      const LayerP& ly = p.lay[MAXL == 1 ? 0 : (int)(gu / p.U)];
+      const long long u = gu % p.U;
       const int b_ = (int)(u / p.H_kv), g_ = (int)(u % p.H_kv);
       const int j0 = (int)(i % p.tpu);
       const size_t qrow0 = ((size_t)b_ * p.H_q + (size_t)g_ * p.G) * p.t;   // first query row
@@ -615,12 +630,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
       if (stid == 0) TRACE(15, tcount);
       fence_after();
       half_sync(h);
-      const long long ufirst = u * p.tpu, ulast = ufirst + p.tpu - 1;
+      const long long ufirst = gu * p.tpu, ulast = ufirst + p.tpu - 1;
       const int c_lo = cta_of_tile(ufirst, NT, p.ctas);
       const int c_hi = cta_of_tile(ulast, NT, p.ctas);
       const int nseg = c_hi - c_lo + 1;
       const size_t rec = rec_floats(p.M, D);
-      float* my = p.ws + ((size_t)blockIdx.x * 2 + (item == 0 ? 0 : 1)) * rec;
+      float* my = ly.ws + ((size_t)blockIdx.x * 2 + (item == 0 ? 0 : 1)) * rec;
       const float* mfin = msm + mv * NH;
 #pragma unroll 1
       for (int c0 = 0; c0 < NH; c0 += 8) {
@@ -635,7 +650,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
             const float L = (sums[c] + sums[NH + c]) + (sums[2 * NH + c] + sums[3 * NH + c]);
             const float o = o_hi[e] + o_lo[e];
             if (nseg == 1) {
-              p.O[(qrow0 + m) * D + kl] = o / L;
+              ly.O[(qrow0 + m) * D + kl] = o / L;
             } else {
               my[(size_t)m * D + kl] = o;
               if (kl == 0) {
@@ -651,17 +666,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
         __threadfence();
         softmax_sync();
         if (stid == 0) {
-          const int old = atomicAdd(&p.counters[u], 1);
+          const int old = atomicAdd(&ly.counters[u], 1);
           *sm_flag = (old == nseg - 1);
         }
         softmax_sync();
         if (*sm_flag) {
           __threadfence();
           // scratch: the P^T buffers (every O^T MMA of this item has completed)
-          combine_unit<4>(p.ws, rec, c_lo, c_hi, ufirst, NT, p.ctas, p.M, D, p.O + qrow0 * D,
+          combine_unit<4>(ly.ws, rec, c_lo, c_hi, ufirst, NT, p.ctas, p.M, D, ly.O + qrow0 * D,
                           reinterpret_cast<float*>(smem + C::OFF_P), stid, 256,
                           [] { softmax_sync(); });
-          if (stid == 0) p.counters[u] = 0;
+          if (stid == 0) ly.counters[u] = 0;
         }
       }
       softmax_sync();   // sums / column state / flag reuse by the next item
@@ -703,47 +718,84 @@ bool attn_tck_supported(int D, int dtype, int M) {
   return D == 128 && dtype == BMC_BF16 && M >= 1 && M <= 80 && encode_fn() != nullptr;
 }
 
-template <int N>
-static cudaError_t launch_n(const tck::Params& p, int ctas, cudaStream_t s) {
+template <int N, int MAXL>
+static cudaError_t launch_n(const tck::Params<MAXL>& p, int ctas, cudaStream_t s) {
   static int attr_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);
   if (attr_dev != dev) {
-    cudaError_t e = cudaFuncSetAttribute(tck::attn_tck_kernel<N>,
+    cudaError_t e = cudaFuncSetAttribute(tck::attn_tck_kernel<N, MAXL>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)tck::Cfg<N>::kSmem);
     if (e != cudaSuccess) return e;
     attr_dev = dev;
   }
-  tck::attn_tck_kernel<N><<<ctas, tck::kThreads, tck::Cfg<N>::kSmem, s>>>(p);
+  tck::attn_tck_kernel<N, MAXL><<<ctas, tck::kThreads, tck::Cfg<N>::kSmem, s>>>(p);
   count_launch();
   return cudaGetLastError();
 }
 
-cudaError_t launch_attn_tck(const AttnStepArgs& a, int num_sms, cudaStream_t s) {
-  const AttnLayer& h = a.layers[0];
-  tck::Params p;
-  const long long U = (long long)a.B * a.H_kv;
-  cudaError_t e = make_map(&p.tmK, h.K, U * h.cap, tck::KT);
-  if (e == cudaSuccess) e = make_map(&p.tmV, h.V, U * h.cap, tck::KT);
+// Tensor maps are pure functions of (base, rows): cache them so a fused
+// 32-layer step does not re-encode 64 maps on the host every token.
+static cudaError_t cached_map(CUtensorMap* m, const void* base, long long rows) {
+  struct Key {
+    const void* base;
+    long long rows;
+    bool operator==(const Key& o) const { return base == o.base && rows == o.rows; }
+  };
+  struct Hash {
+    size_t operator()(const Key& k) const {
+      return std::hash<const void*>()(k.base) ^ (std::hash<long long>()(k.rows) * 31);
+    }
+  };
+  static thread_local std::unordered_map<Key, CUtensorMap, Hash> cache;
+  const Key k{base, rows};
+  auto it = cache.find(k);
+  if (it != cache.end()) {
+    *m = it->second;
+    return cudaSuccess;
+  }
+  cudaError_t e = make_map(m, base, rows, tck::KT);
   if (e != cudaSuccess) return e;
-  p.Q = (const __nv_bfloat16*)h.Q;
-  p.O = h.O;
-  p.Knew = (const uint8_t*)h.Knew;
-  p.Vnew = (const uint8_t*)h.Vnew;
-  p.Kd = (const uint8_t*)h.Kd;
-  p.Vd = (const uint8_t*)h.Vd;
-  p.Kc = (uint8_t*)h.K;
-  p.Vc = (uint8_t*)h.V;
-  p.n_app = h.n_app;
-  p.n_draft = h.n_draft;
-  p.kd_stride = h.kd_stride;
-  p.ws = h.ws;
-  p.counters = h.counters;
-  p.cap = h.cap;
-  p.tpu = (int)(((h.scan > 0 ? h.scan : h.cap) + tck::KT - 1) / tck::KT);
+  if (cache.size() > 4096) cache.clear();
+  cache.emplace(k, *m);
+  return cudaSuccess;
+}
+
+template <int MAXL>
+static cudaError_t launch_layers(const AttnStepArgs& a, int l0, int nl, int num_sms,
+                                 cudaStream_t s) {
+  tck::Params<MAXL> p;
+  const AttnLayer& h0 = a.layers[l0];
+  const long long U = (long long)a.B * a.H_kv;
+  for (int l = 0; l < nl; ++l) {
+    const AttnLayer& h = a.layers[l0 + l];
+    if (h.cap != h0.cap || h.scan != h0.scan || h.n_app != h0.n_app ||
+        h.n_draft != h0.n_draft || h.kd_stride != h0.kd_stride)
+      return cudaErrorInvalidValue;   // the caller launches such layers one by one
+    tck::LayerP& ly = p.lay[l];
+    cudaError_t e = cached_map(&ly.tmK, h.K, U * h.cap);
+    if (e == cudaSuccess) e = cached_map(&ly.tmV, h.V, U * h.cap);
+    if (e != cudaSuccess) return e;
+    ly.Q = (const __nv_bfloat16*)h.Q;
+    ly.O = h.O;
+    ly.Knew = (const uint8_t*)h.Knew;
+    ly.Vnew = (const uint8_t*)h.Vnew;
+    ly.Kd = (const uint8_t*)h.Kd;
+    ly.Vd = (const uint8_t*)h.Vd;
+    ly.Kc = (uint8_t*)h.K;
+    ly.Vc = (uint8_t*)h.V;
+    ly.ws = h.ws;
+    ly.counters = h.counters;
+  }
+  p.L = nl;
+  p.n_app = h0.n_app;
+  p.n_draft = h0.n_draft;
+  p.kd_stride = h0.kd_stride;
+  p.cap = h0.cap;
+  p.tpu = (int)(((h0.scan > 0 ? h0.scan : h0.cap) + tck::KT - 1) / tck::KT);
   p.U = (int)U;
-  p.total_tiles = U * p.tpu;
+  p.total_tiles = (long long)nl * U * p.tpu;
   p.H_kv = a.H_kv;
   p.H_q = a.H_q;
   p.G = a.H_q / a.H_kv;
@@ -757,11 +809,27 @@ cudaError_t launch_attn_tck(const AttnStepArgs& a, int num_sms, cudaStream_t s) 
   if (ctas > p.total_tiles) ctas = (int)p.total_tiles;
   p.ctas = ctas;
   if (p.total_tiles == 0) return cudaSuccess;
-  if (p.M <= 16) return launch_n<16>(p, ctas, s);
-  if (p.M <= 32) return launch_n<32>(p, ctas, s);
-  if (p.M <= 48) return launch_n<48>(p, ctas, s);
-  if (p.M <= 64) return launch_n<64>(p, ctas, s);
-  return launch_n<80>(p, ctas, s);
+  if constexpr (MAXL > 1) {   // multi-layer launches: the GQA decode step, M = G <= 32
+    if (p.M <= 16) return launch_n<16, MAXL>(p, ctas, s);
+    if (p.M <= 32) return launch_n<32, MAXL>(p, ctas, s);
+    return cudaErrorInvalidValue;
+  } else {
+    if (p.M <= 16) return launch_n<16, 1>(p, ctas, s);
+    if (p.M <= 32) return launch_n<32, 1>(p, ctas, s);
+    if (p.M <= 48) return launch_n<48, 1>(p, ctas, s);
+    if (p.M <= 64) return launch_n<64, 1>(p, ctas, s);
+    return launch_n<80, 1>(p, ctas, s);
+  }
+}
+
+cudaError_t launch_attn_tck(const AttnStepArgs& a, int num_sms, cudaStream_t s) {
+  if (a.L == 1) return launch_layers<1>(a, 0, 1, num_sms, s);
+  for (int l0 = 0; l0 < a.L; l0 += kMaxLayersPerLaunch) {
+    const int nl = a.L - l0 < kMaxLayersPerLaunch ? a.L - l0 : kMaxLayersPerLaunch;
+    cudaError_t e = launch_layers<kMaxLayersPerLaunch>(a, l0, nl, num_sms, s);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 }  // namespace bmc

@@ -569,11 +569,16 @@ int bmc_decode_step(const bmc_t* hs, int L, const void* const* K, const void* co
   }
   for (int l = 0; l < L; ++l)
     if (ptr_kind(Q[l]) != 0 || ptr_kind(O[l]) != 0) fused = false;
-  // GQA groups large enough for the tensor cores take the (per-layer) tcgen05 kernel
+  // GQA groups large enough for the tensor cores take the tcgen05 kernel: the
+  // keys-on-lanes kernel fuses the layers (G <= 32), the other runs per layer
   const bmc_t h0 = hs[0];
-  if (h0->attn_path != 1 && (h0->attn_path >= 2 || h0->H_q / h0->H_kv > kTcMinM) &&
-      bmc::attn_tc_supported(h0->D, h0->dt, h0->H_q / h0->H_kv))
-    fused = false;
+  const int G = h0->H_q / h0->H_kv;
+  const bool tc = h0->attn_path != 1 && (h0->attn_path >= 2 || G > kTcMinM) &&
+                  bmc::attn_tc_supported(h0->D, h0->dt, G);
+  const bool tck = tc && h0->attn_path != 3 && G <= 32 && bmc::attn_tck_supported(h0->D, h0->dt, G);
+  for (int l = 1; l < L && tck; ++l)
+    if (hs[l]->attn_path != h0->attn_path) fused = false;
+  if (tc && !tck) fused = false;
   if (!fused) {
     for (int l = 0; l < L; ++l) {
       int rc = bmc_append(hs[l], K[l], V[l]);
@@ -587,13 +592,36 @@ int bmc_decode_step(const bmc_t* hs, int L, const void* const* K, const void* co
   for (int l = 0; l < L; ++l) {
     int rc = append_impl(hs[l], K[l], V[l]);
     if (rc) return rc;
+    if (tck) {
+      rc = ensure_workspace(hs[l], G);
+      if (rc) return rc;
+    }
     fill_layer(hs[l], Q[l], O[l], &layers[l]);
   }
   bmc::AttnStepArgs a;
   fill_args(hs[0], 1, &a);
   a.L = L;
   a.layers = layers.data();
-  CK(hs[0], bmc::launch_attn_step(a, hs[0]->num_sms, hs[0]->stream), "attn_step");
+  if (tck) {
+    // one launch per 32 layers when every layer has the same capacity (the
+    // usual case: one r, one step sequence); else one launch per layer
+    bool same = true;
+    for (int l = 1; l < L; ++l)
+      if (layers[l].cap != layers[0].cap || layers[l].scan != layers[0].scan) same = false;
+    a.ctas = std::min(h0->attn_ctas, h0->num_sms);
+    if (same) {
+      CK(h0, bmc::launch_attn_tck(a, h0->num_sms, h0->stream), "attn_tck");
+    } else {
+      for (int l = 0; l < L; ++l) {
+        bmc::AttnStepArgs a1 = a;
+        a1.L = 1;
+        a1.layers = &layers[l];
+        CK(h0, bmc::launch_attn_tck(a1, h0->num_sms, h0->stream), "attn_tck");
+      }
+    }
+  } else {
+    CK(hs[0], bmc::launch_attn_step(a, hs[0]->num_sms, hs[0]->stream), "attn_step");
+  }
   for (int l = 0; l < L; ++l) {
     hs[l]->n_app = hs[l]->n_draft = 0;
     account_sdpa(hs[l], 1);

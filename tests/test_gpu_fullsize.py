@@ -64,7 +64,8 @@ def _run_decode_fullsize(B, H_kv, H_q, D, N, r, L, sample_steps, sample_units, s
     # BASELINE configs[1]: Llama-2-7B shape, B=16, context 4096, r = 64 (bench default)
     dict(B=16, H_kv=32, H_q=32, D=128, N=4096, r=64, L=2),
     # BASELINE configs[3] per GPU: Llama-3-8B GQA (32 q / 8 kv heads), B=64, context 8192
-    dict(B=64, H_kv=8, H_q=32, D=128, N=8192, r=128, L=1),
+    # (two layers: the fused multi-layer tcgen05 launch of the GQA decode step)
+    dict(B=64, H_kv=8, H_q=32, D=128, N=8192, r=128, L=2),
 ])
 def test_fullsize_decode(cfg):
     B, H_kv, H_q, D, N, r, L = (cfg[k] for k in ("B", "H_kv", "H_q", "D", "N", "r", "L"))
@@ -169,17 +170,19 @@ def test_fullsize_speculative_7b():
     c.close()
 
 
-def test_decode_step_matches_per_layer_calls():
+@pytest.mark.parametrize("H_q,path_b", [(4, 1), (8, 0)])
+def test_decode_step_matches_per_layer_calls(H_q, path_b):
     """bmc_decode_step (fused multi-layer launch, >32 layers -> 2 launches)
     matches per-layer append + sdpa calls: caches and ledgers bit-identical,
     outputs equal up to the split-K summation order (the CTA partition of the
-    tile stream differs)."""
-    B, H_kv, H_q, D, N, r, L = 2, 2, 8, 128, 200, 24, 40
+    tile stream differs).  G = 2: CUDA-core step kernel; G = 4: the
+    keys-on-lanes tcgen05 kernel, fused over layers, vs its per-layer launches."""
+    B, H_kv, D, N, r, L = 2, 2, 128, 200, 24, 40
     dev = torch.device("cuda")
     a = [bmc.KVCache(B, H_kv, H_q, D, r, N, dtype="bf16") for _ in range(L)]
     b = [bmc.KVCache(B, H_kv, H_q, D, r, N, dtype="bf16") for _ in range(L)]
-    for x in b:      # same CUDA-core algorithm as the fused multi-layer launch
-        x.set_option(bmc.BMC_OPT_ATTN_PATH, 1)
+    for x in b:      # same algorithm as the fused multi-layer launch
+        x.set_option(bmc.BMC_OPT_ATTN_PATH, path_b)
     plan = bmc.StepPlan(a)
     g = torch.Generator(device=dev)
     g.manual_seed(3)
