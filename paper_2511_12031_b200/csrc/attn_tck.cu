@@ -82,8 +82,9 @@ struct Cfg {
   static constexpr uint32_t OFF_BAR = OFF_P + NBP * kPBytes;
   static constexpr uint32_t OFF_RED = OFF_BAR + 512;           // [2 halves][4 quadrants][NH] f32
   static constexpr uint32_t OFF_SUM = OFF_RED + 2 * 4 * NH * 4;  // [2][4][NH] f32
-  static constexpr uint32_t OFF_M = OFF_SUM + 2 * 4 * NH * 4;    // [2 halves][2 versions][NH] f32
-  static constexpr uint32_t OFF_A = OFF_M + 2 * 2 * NH * 4;      // [2][NH] rescale factors
+  // running maxima: [2 halves][2 versions][m, m-or-0, m+8][NH] f32
+  static constexpr uint32_t OFF_M = OFF_SUM + 2 * 4 * NH * 4;
+  static constexpr uint32_t OFF_A = OFF_M + 2 * 2 * 3 * NH * 4;  // [2][NH] rescale factors
   static constexpr uint32_t OFF_LIM = OFF_A + 2 * NH * 4;        // [2][NH] int visible-key limit
   static constexpr uint32_t OFF_QM = OFF_LIM + 2 * NH * 4;       // [2][NH] ancestor masks
   static constexpr uint32_t kSmem = OFF_QM + 2 * NH * 4;
@@ -419,7 +420,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
     const int stid = threadIdx.x - 64;
     float* red = reinterpret_cast<float*>(smem + C::OFF_RED) + h * 4 * NH;   // [4][NH]
     float* sums = reinterpret_cast<float*>(smem + C::OFF_SUM) + h * 4 * NH;  // [4][NH]
-    float* msm = reinterpret_cast<float*>(smem + C::OFF_M) + h * 2 * NH;     // [2 versions][NH]
+    // per version: m (true running max), m or 0 (exponent offset), m + 8 (threshold)
+    float* msm = reinterpret_cast<float*>(smem + C::OFF_M) + h * 2 * 3 * NH;
     float* asm_ = reinterpret_cast<float*>(smem + C::OFF_A) + h * NH;        // rescale factors
     int* lim = reinterpret_cast<int*>(smem + C::OFF_LIM) + h * NH;           // keys < lim visible
     uint32_t* qmk = reinterpret_cast<uint32_t*>(smem + C::OFF_QM) + h * NH;  // + these drafts
@@ -473,18 +475,16 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
           const int m = h * NH + c;
           const int tau = m % p.t;
           msm[c] = -INFINITY;
+          msm[NH + c] = 0.f;
+          msm[2 * NH + c] = -INFINITY;
           lim[c] = m < p.M ? vb_ + (p.tree ? 0 : tau) : INT_MIN;
           qmk[c] = (m < p.M && p.tree && tau > 0) ? p.anc[tau - 1] : 0u;
         }
       }
       half_sync(h);
-      float l[NH];
+      float2 l2[NH / 2];                   // this key lane's partial row sums
 #pragma unroll
-      for (int c = 0; c < NH; ++c) l[c] = 0.f;
-      // columns of this half that are real queries (the rest is padding)
-      const int mcols = p.M - h * NH;
-      const uint64_t colmask =
-          mcols <= 0 ? 0ull : (mcols >= 64 ? ~0ull : ((1ull << mcols) - 1ull));
+      for (int c = 0; c < NH / 2; ++c) l2[c] = make_float2(0.f, 0.f);
       const int n = (int)(iend - i);
       for (int k = 0; k < n; ++k) {
         const int tc = tcount + k;
@@ -499,34 +499,39 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
         tmem_ld_cols<NH>(tmem + bb * N + h * NH + lane_addr, x);
         fence_before();
         mbar_arrive(SEMPTY(bb));
-        // mask + log2 scaling.  Tiles inside the committed rows see every real
-        // column; the (at most two per item) tiles reaching past them build
+        // log2 scaling and mask.  Tiles inside the committed rows need no mask
+        // (padding columns have Q = 0: finite scores in outputs nobody
+        // reads); the (at most two per item) tiles reaching past them build
         // the per-column visibility in a compact loop (cold code stays small:
         // an instruction-cache miss costs an L2 round trip under full HBM load)
-        uint64_t vm = colmask;
+        const float2 qs2 = make_float2(p.qscale, p.qscale);
+#pragma unroll
+        for (int c = 0; c < NH; c += 2) {
+          const float2 y = __fmul2_rn(make_float2(x[c], x[c + 1]), qs2);
+          x[c] = y.x;
+          x[c + 1] = y.y;
+        }
         if ((long long)(j0 + k + 1) * KT > vb_) {
           const long long js = kidx - vb_;
-          vm = 0;
+          uint64_t vm = 0;
 #pragma unroll 1
           for (int c = 0; c < NH; ++c) {
             const uint32_t qm = qmk[c];
             const bool v = kidx < (long long)lim[c] || (js >= 0 && js < 32 && ((qm >> js) & 1u));
             vm |= (uint64_t)v << c;
           }
+#pragma unroll
+          for (int c = 0; c < NH; ++c) x[c] = ((vm >> c) & 1ull) ? x[c] : -INFINITY;
         }
-        const float* mcur = msm + mv * NH;
+        const float* mthr = msm + mv * 3 * NH + 2 * NH;
         bool need = false;
 #pragma unroll
         for (int c0 = 0; c0 < NH; c0 += 8) {
           float mr[8];
-          *reinterpret_cast<float4*>(mr) = *reinterpret_cast<const float4*>(mcur + c0);
-          *reinterpret_cast<float4*>(mr + 4) = *reinterpret_cast<const float4*>(mcur + c0 + 4);
+          *reinterpret_cast<float4*>(mr) = *reinterpret_cast<const float4*>(mthr + c0);
+          *reinterpret_cast<float4*>(mr + 4) = *reinterpret_cast<const float4*>(mthr + c0 + 4);
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const int c = c0 + e;
-            x[c] = ((vm >> c) & 1ull) ? x[c] * p.qscale : -INFINITY;
-            need |= x[c] > mr[e] + kRescale;
-          }
+          for (int e = 0; e < 8; ++e) need |= x[c0 + e] > mr[e];
         }
         const bool any_ = half_any(h, need);
         if (stid == 0) TRACE(10, tc);
@@ -541,8 +546,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
           // the quadrant-0 warp moves the running maxima into the other
           // version (readers of the current one are ordered by the barriers)
           if (q == 0) {
-            const float* mold = msm + mv * NH;
-            float* mnew = msm + (mv ^ 1) * NH;
+            const float* mold = msm + mv * 3 * NH;
+            float* mnew = msm + (mv ^ 1) * 3 * NH;
             bool resc = false;
             for (int c = lane; c < NH; c += 32) {
               const float mt =
@@ -555,6 +560,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
                 resc |= (mo != -INFINITY);
               }
               mnew[c] = mnx;
+              mnew[NH + c] = mnx == -INFINITY ? 0.f : mnx;
+              mnew[2 * NH + c] = mnx + kRescale;
               asm_[c] = alpha;
             }
             resc = __any_sync(0xffffffffu, resc);
@@ -565,10 +572,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
 #pragma unroll
           for (int c0 = 0; c0 < NH; c0 += 4) {
             const float4 a4 = *reinterpret_cast<const float4*>(asm_ + c0);
-            l[c0] *= a4.x;
-            l[c0 + 1] *= a4.y;
-            l[c0 + 2] *= a4.z;
-            l[c0 + 3] *= a4.w;
+            l2[c0 / 2] = __fmul2_rn(l2[c0 / 2], make_float2(a4.x, a4.y));
+            l2[c0 / 2 + 1] = __fmul2_rn(l2[c0 / 2 + 1], make_float2(a4.z, a4.w));
           }
           // O^T columns of this half (rows = dims of this quadrant) are
           // rescaled once the previous tile's O^T MMAs have completed
@@ -594,24 +599,28 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
         if (tc >= C::NBP) mbar_wait(PEMPTY(pb), ((tc / C::NBP) - 1) & 1);
         if (stid == 0) TRACE(12, tc);
         const uint32_t pbase = sbase + C::OFF_P + pb * C::kPBytes + pkey;
-        const float* mu = msm + mv * NH;
+        const float* msf = msm + mv * 3 * NH + NH;   // m, or 0 while m = -inf (then x = -inf)
 #pragma unroll
         for (int c0 = 0; c0 < NH; c0 += 8) {
           float mr[8];
-          *reinterpret_cast<float4*>(mr) = *reinterpret_cast<const float4*>(mu + c0);
-          *reinterpret_cast<float4*>(mr + 4) = *reinterpret_cast<const float4*>(mu + c0 + 4);
+          *reinterpret_cast<float4*>(mr) = *reinterpret_cast<const float4*>(msf + c0);
+          *reinterpret_cast<float4*>(mr + 4) = *reinterpret_cast<const float4*>(msf + c0 + 4);
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
+          for (int e = 0; e < 8; e += 2) {
             const int c = c0 + e;
-            // a column still at m = -inf has seen only masked keys (x = -inf): P = 0
-            const float pv = fast_exp2(x[c] - (mr[e] == -INFINITY ? 0.f : mr[e]));
-            l[c] += pv;
-            const uint32_t bits = __float_as_uint(pv);
-            const float hi = __uint_as_float(bits & 0xffff0000u);
-            const uint32_t lo = (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(pv - hi));
-            const uint32_t rh = (uint32_t)(h * NH + c), rl = rh + N;   // P^T rows: hi, lo
-            sts_u16(pbase + rh * 128 + ((pchunk ^ (rh & 7u)) << 4), bits >> 16);
-            sts_u16(pbase + rl * 128 + ((pchunk ^ (rl & 7u)) << 4), lo);
+            const float2 d = __fadd2_rn(make_float2(x[c], x[c + 1]), make_float2(-mr[e], -mr[e + 1]));
+            const float2 pv = make_float2(fast_exp2(d.x), fast_exp2(d.y));
+            l2[c / 2] = __fadd2_rn(l2[c / 2], pv);
+#pragma unroll
+            for (int z = 0; z < 2; ++z) {
+              const float pz = z ? pv.y : pv.x;
+              const uint32_t bits = __float_as_uint(pz);
+              const float hi = __uint_as_float(bits & 0xffff0000u);
+              const uint32_t lo = (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(pz - hi));
+              const uint32_t rh = (uint32_t)(h * NH + c + z), rl = rh + N;   // P^T rows: hi, lo
+              sts_u16(pbase + rh * 128 + ((pchunk ^ (rh & 7u)) << 4), bits >> 16);
+              sts_u16(pbase + rl * 128 + ((pchunk ^ (rl & 7u)) << 4), lo);
+            }
           }
         }
         fence_proxy_smem();
@@ -621,7 +630,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
       // ---- epilogue of this item: column sums, O^T (TMEM) -> output / record
 #pragma unroll
       for (int c = 0; c < NH; ++c) {
-        const float ws_ = warp_sum(l[c]);
+        const float ws_ = warp_sum((c & 1) ? l2[c / 2].y : l2[c / 2].x);
         if (lane == 0) sums[q * NH + c] = ws_;
       }
       if (stid == 0) TRACE(14, tcount);
@@ -636,7 +645,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
       const int nseg = c_hi - c_lo + 1;
       const size_t rec = rec_floats(p.M, D);
       float* my = ly.ws + ((size_t)blockIdx.x * 2 + (item == 0 ? 0 : 1)) * rec;
-      const float* mfin = msm + mv * NH;
+      const float* mfin = msm + mv * 3 * NH;
 #pragma unroll 1
       for (int c0 = 0; c0 < NH; c0 += 8) {
         float o_hi[8], o_lo[8];

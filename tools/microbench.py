@@ -136,7 +136,7 @@ def main():
         for (B, Hk, Hq, cap, t) in [(8, 8, 64, 8192, 9), (8, 8, 64, 8192, 1),
                                     (64, 8, 32, 4096, 1), (32, 32, 32, 2048, 5),
                                     (8, 8, 64, 8192, 4), (8, 8, 64, 8192, 8)]:
-            for pa in (1, 2, 3):
+            for pa in ((2, 3, 4) if (Hq // Hk) * t > 64 else (1, 2, 3)):
                 print("config", B, Hk, Hq, cap, t, pa, file=sys.stderr, flush=True)
                 out["verify"].append(attn_at(B, Hk, Hq, 128, cap, t=t, path=pa, reps=20,
                                              layers=4))
