@@ -186,7 +186,7 @@ int bmc_sync(bmc_t h);
 /* Tuning / test options (key, value).  Keys:
      1 BMC_OPT_ATTN_CTAS      CTAs of the attention kernel (0 = auto)
      2 BMC_OPT_ATTN_PATH      0 auto, 1 CUDA-core split-K, 2 tcgen05 (keys on
-                              the TMEM lanes for G*t <= 64, else queries on
+                              the TMEM lanes for G*t <= 80, else queries on
                               the lanes), 3 tcgen05 with queries on the lanes,
                               4 tcgen05 with keys on the lanes (G*t <= 80)
      3 BMC_OPT_ARENA          0 VMM ping-pong slots, 1 stream-ordered pool

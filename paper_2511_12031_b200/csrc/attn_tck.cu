@@ -514,7 +514,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
         if ((long long)(j0 + k + 1) * KT > vb_) {
           const long long js = kidx - vb_;
           uint64_t vm = 0;
-#pragma unroll 1
+#pragma unroll 8
           for (int c = 0; c < NH; ++c) {
             const uint32_t qm = qmk[c];
             const bool v = kidx < (long long)lim[c] || (js >= 0 && js < 32 && ((qm >> js) & 1u));

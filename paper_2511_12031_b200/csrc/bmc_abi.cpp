@@ -493,10 +493,10 @@ int bmc_sdpa(bmc_t h, const void* Q, int n_valid, float* O) {
   // 2.1x at M=5), CUDA cores keep M <= 2 (6.2-6.4 TB/s at M=1)
   const bool use_tc = h->attn_path >= 2 ||
                       (h->attn_path == 0 && M > kTcMinM && bmc::attn_tc_supported(h->D, h->dt, M));
-  // keys on the TMEM lanes (attn_tck.cu) for M <= 64 or when forced (path 4),
-  // queries on the lanes above that or when forced (path 3)
+  // keys on the TMEM lanes (attn_tck.cu) for M <= 80, queries on the lanes
+  // above that or when forced (path 3); path 4 insists on keys on the lanes
   const bool use_tck = use_tc && h->attn_path != 3 &&
-                       (h->attn_path == 4 || M <= 64) && bmc::attn_tck_supported(h->D, h->dt, M);
+                       bmc::attn_tck_supported(h->D, h->dt, M);
   if (h->attn_path == 4 && !use_tck)
     return fail(BMC_ERR_UNSUPPORTED, "keys-on-lanes tcgen05 path needs bf16, D=128, G*t<=80");
   if (use_tc) {

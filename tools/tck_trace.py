@@ -11,7 +11,7 @@ L = bmc.load()
 B, Hk, Hq, cap, t = (int(x) for x in sys.argv[1:6])
 tcta = int(sys.argv[6]) if len(sys.argv) > 6 else 0
 L.bmc_tck_trace_cta(tcta)
-print(attn_at(B, Hk, Hq, 128, cap, t=t, path=2, reps=2, layers=1))
+print(attn_at(B, Hk, Hq, 128, cap, t=t, path=4, reps=2, layers=1))
 buf = (ctypes.c_longlong * (16 * 256 + 160 * 4))()
 L.bmc_tck_trace.argtypes = [ctypes.c_void_p]
 assert L.bmc_tck_trace(buf) == 0
