@@ -65,6 +65,7 @@ def lib():
         vp, ip, i = ctypes.c_void_p, ctypes.POINTER(ctypes.c_int), ctypes.c_int
         L.oracle_create.argtypes = [i, i, i, i, i, i, i, i, ctypes.POINTER(vp)]
         L.oracle_append.argtypes = [vp, vp, vp]
+        L.oracle_append_n.argtypes = [vp, vp, vp, i]
         L.oracle_spec_write.argtypes = [vp, vp, vp, i]
         L.oracle_sdpa.argtypes = [vp, vp, i, vp]
         L.oracle_commit.argtypes = [vp, i]
@@ -76,7 +77,7 @@ def lib():
         L.oracle_exact_sdpa.argtypes = [vp, vp, vp, i, i, vp]
         L.oracle_spec_write_tree.argtypes = [vp, vp, vp, i, ip]
         L.oracle_commit_path.argtypes = [vp, ip, ip, i]
-        for f in ("oracle_create", "oracle_append", "oracle_spec_write", "oracle_sdpa",
+        for f in ("oracle_create", "oracle_append", "oracle_append_n", "oracle_spec_write", "oracle_sdpa",
                   "oracle_commit", "oracle_commit_rows", "oracle_stats", "oracle_valid",
                   "oracle_read_cache", "oracle_destroy", "oracle_exact_sdpa",
                   "oracle_spec_write_tree", "oracle_commit_path"):
@@ -134,6 +135,14 @@ class Oracle:
         k, v = _raw(K, self.dtype), _raw(V, self.dtype)
         assert k.size == self.B * self.H_kv * self.D and v.size == k.size
         return self._check(lib().oracle_append(self._h, _ptr(k), _ptr(v)), "oracle_append")
+
+    def append_n(self, K, V, n: int):
+        """Bulk (prompt) append of n rows per unit, K/V [B][H_kv][n][D]."""
+        if n == 0:
+            return self._check(lib().oracle_append_n(self._h, None, None, 0), "append_n")
+        k, v = _raw(K, self.dtype), _raw(V, self.dtype)
+        assert k.size == self.B * self.H_kv * n * self.D and v.size == k.size
+        return self._check(lib().oracle_append_n(self._h, _ptr(k), _ptr(v), n), "oracle_append_n")
 
     def spec_write(self, Kd, Vd, k: int) -> int:
         if k == 0:

@@ -220,6 +220,39 @@ int oracle_append(oracle_t h, const void* K, const void* V) {
   }
 }
 
+/* ------------------------------------------------------------ bulk append */
+
+/* Bulk (prompt) append of n rows per unit, K/V laid out [B][H_kv][n][D].
+   Contents and valid lengths equal n single appends; the allocation ledger
+   follows the prompt-ingestion rule ("one chunk covering the whole
+   prompt (single alloc event), not token-by-token"; reading R19): at most
+   one reallocation, to the capacity n single appends would end at --
+   BMC: cap + r*ceil((mv + n - cap)/r) capped at N_max;
+   ITERATIVE: exactly mv + n; UPFRONT: none --
+   copying the mv rows that can hold data. */
+int oracle_append_n(oracle_t h, const void* K, const void* V, int n) {
+  if (!h || n < 0) return OR_ERR_ARG;
+  if (n == 0) return OR_OK;
+  if (!K || !V) return OR_ERR_ARG;
+  if (h->staged > 0) return OR_ERR_STATE;
+  int mv = max_valid(h);
+  if ((long)mv + n > h->N_max) return OR_ERR_CAPACITY;
+  long need = (long)mv + n;
+  int rc = OR_OK;
+  if (h->policy == ORACLE_POLICY_ITERATIVE) {
+    rc = reallocate(h, need, mv);
+  } else if (h->policy == ORACLE_POLICY_BMC && need > h->cap) {
+    long chunks = (need - h->cap + h->r - 1) / h->r;
+    long nc = h->cap + chunks * h->r;
+    if (nc > h->N_max) nc = h->N_max;
+    rc = reallocate(h, nc, mv);
+  }
+  if (rc) return rc;
+  for (int i = 0; i < n; ++i) write_row(h, (const unsigned char*)K, (const unsigned char*)V, n, i, i);
+  for (int b = 0; b < h->B; ++b) h->valid[b] += n;
+  return OR_OK;
+}
+
 /* ------------------------------------------------------------- spec_write */
 
 /* BMC / UPFRONT admission: "limit the number of speculated

@@ -50,6 +50,7 @@ typedef struct {
 int oracle_create(int B, int H_kv, int H_q, int D, int r, int N_max, int dtype,
                   int policy, oracle_t* out);
 int oracle_append(oracle_t h, const void* K, const void* V);          /* [B][H_kv][D] */
+int oracle_append_n(oracle_t h, const void* K, const void* V, int n);   /* [B][H_kv][n][D] bulk (prompt) append */
 int oracle_spec_write(oracle_t h, const void* Kd, const void* Vd, int k); /* [B][H_kv][k][D]; returns k_adm */
 int oracle_sdpa(oracle_t h, const void* Q, int n_valid, double* O);   /* Q [B][H_q][t][D], O fp64 */
 int oracle_commit(oracle_t h, int n_accepted);

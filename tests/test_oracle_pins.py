@@ -550,3 +550,99 @@ def test_tree_errors(oracle_mod):
     assert e.value.code == -1
     orc.commit_path([[0, 2]])
     assert list(orc.valid()) == [3]
+
+
+# ------------------------------------------------------- bulk (prompt) append
+
+def _prompt(seed, B, H_kv, D, n, dtype="bf16"):
+    """[B][H_kv][n][D] prompt rows from the per-step streams of steps 1..n."""
+    ks, vs = [], []
+    for t in range(1, n + 1):
+        x = synth.step_inputs(seed, 0, t, B=B, H_kv=H_kv, H_q=H_kv, D=D, dtype=dtype)
+        ks.append(x["k"])
+        vs.append(x["v"])
+    return torch.stack(ks, dim=2).contiguous(), torch.stack(vs, dim=2).contiguous()
+
+
+@pytest.mark.parametrize("policy,r", [(O.POLICY_BMC, 4), (O.POLICY_BMC, 16),
+                                      (O.POLICY_ITERATIVE, 1), (O.POLICY_UPFRONT, 40)])
+def test_append_n_equals_single_appends(oracle_mod, policy, r):
+    """A bulk append of n rows leaves the cache contents and lengths that n
+    single appends leave (P:L609 in-place writes; S:L104 prompt ingestion),
+    including after earlier decode rows; padded rows stay zero."""
+    B, H, D, N = 2, 3, 8, 40
+    a = O.Oracle(B, H, H, D, r, N, dtype=O.BF16, policy=policy)
+    b = O.Oracle(B, H, H, D, r, N, dtype=O.BF16, policy=policy)
+    K1, V1 = _prompt(5, B, H, D, 13)
+    K2, V2 = _prompt(6, B, H, D, 9)
+    a.append_n(K1, V1, 13)
+    a.append_n(K2, V2, 9)
+    for K, V, n in ((K1, V1, 13), (K2, V2, 9)):
+        for i in range(n):
+            b.append(K[:, :, i].contiguous(), V[:, :, i].contiguous())
+    assert list(a.valid()) == list(b.valid()) == [22, 22]
+    Ka, Va = a.read_cache()
+    Kb, Vb = b.read_cache()
+    assert np.array_equal(Ka[:, :22], Kb[:, :22]) and np.array_equal(Va[:, :22], Vb[:, :22])
+    assert not Ka[:, 22:].any() and not Va[:, 22:].any()
+    assert a.stats()["append_written_bytes"] == b.stats()["append_written_bytes"]
+
+
+@pytest.mark.parametrize("P", [1, 15, 16, 17, 100, 128])
+def test_prefill_ledger_closed_form(oracle_mod, P):
+    """Prompt ingestion is one allocation: from an empty BMC cache
+    with r=16 a prompt of P rows ends at cap = r*ceil(P/r) (min r, max N_max)
+    after one growth beyond the first chunk, copying nothing; ITERATIVE
+    allocates exactly P rows; UPFRONT allocates nothing more."""
+    B, H, D, N, r = 1, 2, 4, 128, 16
+    K, V = _prompt(7, B, H, D, P, dtype="f32")
+    U, rb = B * H, D * 4
+    bm = O.Oracle(B, H, H, D, r, N, dtype=O.F32, policy=O.POLICY_BMC)
+    bm.append_n(K, V, P)
+    s = bm.stats()
+    cap = min(N, max(r, r * math.ceil(P / r)))
+    assert s["capacity"] == cap and s["valid_max"] == P
+    assert s["alloc_events"] == (1 if P <= r else 2)
+    assert s["copy_events"] == (0 if P <= r else 1) and s["copied_bytes"] == 0
+    assert s["init_written_bytes"] == 2 * U * rb * (r + (cap if P > r else 0))
+    it = O.Oracle(B, H, H, D, 1, N, dtype=O.F32, policy=O.POLICY_ITERATIVE)
+    it.append_n(K, V, P)
+    s = it.stats()
+    assert s["capacity"] == P and s["alloc_events"] == 1 and s["copied_bytes"] == 0
+    up = O.Oracle(B, H, H, D, N, N, dtype=O.F32, policy=O.POLICY_UPFRONT)
+    up.append_n(K, V, P)
+    assert up.stats()["alloc_events"] == 1 and up.stats()["capacity"] == N
+
+
+def test_prefill_then_decode_sdpa_is_exact(oracle_mod):
+    """After a bulk prompt the masked SDPA over the padded cache equals the
+    textbook SDPA over exactly the prompt rows."""
+    B, H, D, N, r, P = 1, 1, 8, 64, 16, 21
+    K, V = _prompt(8, B, H, D, P, dtype="f32")
+    orc = O.Oracle(B, H, H, D, r, N, dtype=O.F32, policy=O.POLICY_BMC)
+    orc.append_n(K, V, P)
+    q = synth.step_inputs(8, 0, P + 1, B=B, H_kv=H, H_q=H, D=D, dtype="f32")["q"]
+    got = orc.sdpa(q, P).reshape(D)
+    ref = O.exact_sdpa(q.numpy().reshape(D).astype(np.float64),
+                       K.numpy().reshape(P, D).astype(np.float64),
+                       V.numpy().reshape(P, D).astype(np.float64))
+    assert np.abs(got - ref).max() <= 1e-12
+
+
+def test_append_n_errors(oracle_mod):
+    """CAPACITY past N_max, STATE with staged drafts, n = 0 is a no-op."""
+    B, H, D, N = 1, 1, 4, 10
+    orc = O.Oracle(B, H, H, D, 4, N, dtype=O.F32, policy=O.POLICY_BMC)
+    K, V = _prompt(9, B, H, D, 11, dtype="f32")
+    with pytest.raises(O.OracleError) as e:
+        orc.append_n(K, V, 11)
+    assert e.value.code == -3
+    orc.append_n(K[:, :, :0], V[:, :, :0], 0)
+    assert orc.stats()["valid_max"] == 0
+    K3, V3 = _prompt(9, B, H, D, 3, dtype="f32")
+    orc.append_n(K3, V3, 3)
+    kd = torch.zeros(B, H, 1, D)
+    orc.spec_write(kd, kd, 1)
+    with pytest.raises(O.OracleError) as e:
+        orc.append_n(K3, V3, 3)
+    assert e.value.code == -2
