@@ -95,6 +95,18 @@ int bmc_create_ex(int B, int H_kv, int H_q, int D, int r, int N_max, bmc_dtype d
    staged, CAPACITY if max valid == N_max. */
 int bmc_append(bmc_t h, const void* K, const void* V);
 
+/* Bulk (prompt) append: n rows per unit, K and V [B][H_kv][n][D] in the
+   cache dtype (device or host pointers).  Contents and lengths equal n
+   bmc_append calls (P:L609 in-place writes); the allocation follows prompt
+   ingestion (reading R19): at most ONE reallocation, to the
+   capacity n appends would end at (BMC: cap + r*ceil((valid+n-cap)/r) capped
+   at N_max; ITERATIVE: valid + n; UPFRONT: none), copying the valid rows.
+   The rows are copied by a kernel this call enqueues (not deferred to the
+   next call), so K and V must stay valid until the stream passes it.
+   Errors: ARG (n < 0, null pointers), STATE (drafts staged), CAPACITY
+   (valid + n > N_max); n == 0 is a no-op. */
+int bmc_append_n(bmc_t h, const void* K, const void* V, int n);
+
 /* bmc_spec_write: place k chain-draft rows in the padded rows.
    K_draft, V_draft: [B][H_kv][k][D].  Admits k_adm = min(k, cap - max valid)
    drafts (BMC, UPFRONT: never grows) or min(k, N_max - max valid)

@@ -33,7 +33,8 @@ _TORCH_DT = {BMC_F32: torch.float32, BMC_BF16: torch.bfloat16}
 _NAMES = {0: "OK", -1: "ARG", -2: "STATE", -3: "CAPACITY", -4: "OOM", -5: "CUDA",
           -6: "UNSUPPORTED"}
 
-EXPORTS = ["bmc_create", "bmc_create_ex", "bmc_append", "bmc_spec_write", "bmc_sdpa",
+EXPORTS = ["bmc_create", "bmc_create_ex", "bmc_append", "bmc_append_n", "bmc_spec_write",
+           "bmc_sdpa",
            "bmc_commit", "bmc_commit_rows", "bmc_commit_path", "bmc_spec_write_tree",
            "bmc_decode_step", "bmc_destroy", "bmc_stats", "bmc_kv_view",
            "bmc_valid", "bmc_read_cache", "bmc_sync", "bmc_set_option", "bmc_launch_count", "bmc_last_error"]
@@ -71,6 +72,7 @@ def load(path: str = SO_PATH):
     L.bmc_create.argtypes = [i, i, i, i, i, i, ctypes.POINTER(vp)]
     L.bmc_create_ex.argtypes = [i, i, i, i, i, i, i, i, i, vp, ctypes.POINTER(vp)]
     L.bmc_append.argtypes = [vp, vp, vp]
+    L.bmc_append_n.argtypes = [vp, vp, vp, ctypes.c_int]
     L.bmc_spec_write.argtypes = [vp, vp, vp, i]
     L.bmc_sdpa.argtypes = [vp, vp, i, vp]
     L.bmc_commit.argtypes = [vp, i]
@@ -130,6 +132,10 @@ def bmc_create_ex(B, H_kv, H_q, D, r, N_max, dtype=BMC_BF16, policy=BMC_POLICY_B
 
 def bmc_append(h, K, V) -> int:
     return _check(load().bmc_append(h, _ptr(K), _ptr(V)), "bmc_append")
+
+
+def bmc_append_n(h, K, V, n: int) -> int:
+    return _check(load().bmc_append_n(h, _ptr(K), _ptr(V), n), "bmc_append_n")
 
 
 def bmc_spec_write(h, K_draft, V_draft, k: int) -> int:
@@ -252,6 +258,12 @@ class KVCache:
 
     def append(self, K, V):
         rc = bmc_append(self.h, K, V)
+        self._keep = (K, V)
+        return rc
+
+    def append_n(self, K, V, n):
+        """Bulk (prompt) append, K/V [B][H_kv][n][D]."""
+        rc = bmc_append_n(self.h, K, V, n)
         self._keep = (K, V)
         return rc
 

@@ -401,6 +401,41 @@ int bmc_append(bmc_t h, const void* K, const void* V) {
   return append_impl(h, K, V);
 }
 
+int bmc_append_n(bmc_t h, const void* K, const void* V, int n) {
+  int rc = enter(h);
+  if (rc) return rc;
+  if (n < 0) return fail(BMC_ERR_ARG, "n=%d < 0", n);
+  if (n == 0) return 0;
+  if (!K || !V) return fail(BMC_ERR_ARG, "K or V is null");
+  if (h->staged > 0) return fail(BMC_ERR_STATE, "append while %d drafts are staged", h->staged);
+  const int mv = max_valid(h);
+  if ((long long)mv + n > h->N_max)
+    return fail(BMC_ERR_CAPACITY, "%d + %d rows exceed N_max=%d", mv, n, h->N_max);
+  if (h->n_app || h->n_draft) rc = flush_pending(h);
+  if (rc) return rc;
+  // one allocation for the whole prompt, to the capacity n single
+  // appends would end at; the mv rows that can hold data are copied
+  const long long need = (long long)mv + n;
+  if (h->pol == BMC_POLICY_ITERATIVE) {
+    rc = reallocate(h, need, mv);
+  } else if (h->pol == BMC_POLICY_BMC && need > h->cap) {
+    const long long chunks = (need - h->cap + h->r - 1) / h->r;
+    rc = reallocate(h, std::min<long long>(h->cap + chunks * h->r, h->N_max), mv);
+  }
+  if (rc) return rc;
+  const size_t in_bytes = (size_t)h->U * n * h->row_bytes;
+  const void* ptrs[2] = {K, V};
+  const size_t sizes[2] = {in_bytes, in_bytes};
+  const void* dev[2];
+  rc = device_inputs(h, 0, ptrs, sizes, 2, dev);
+  if (rc) return rc;
+  rc = write_rows(h, dev[0], dev[1], n, n, 0);
+  if (rc) return rc;
+  h->st.append_written_bytes += 2LL * h->U * n * h->row_bytes;
+  for (auto& v : h->valid) v += n;
+  return 0;
+}
+
 int bmc_spec_write(bmc_t h, const void* K_draft, const void* V_draft, int k) {
   int rc = enter(h);
   if (rc) return rc;

@@ -56,6 +56,16 @@ class Pair:
         self.gpu.append(self._dev(x["k"]), self._dev(x["v"]))
         self.orc.append(x["k"], x["v"])
 
+    def append_n(self, n):
+        """Bulk (prompt) append of n rows (the draft stream's [B][H_kv][n][D] layout)."""
+        x = synth.step_inputs(self.seed, self.layer, self.step, B=self.B, H_kv=self.H_kv,
+                              H_q=self.H_q, D=self.D, dtype=self.dtype, k_draft=max(n, 1),
+                              want=("kd", "vd"), variant=self.variant)
+        self.step += 1
+        kd, vd = x["kd"][:, :, :n].contiguous(), x["vd"][:, :, :n].contiguous()
+        self.gpu.append_n(self._dev(kd), self._dev(vd), n)
+        self.orc.append_n(kd, vd, n)
+
     def spec_write(self, k):
         x = synth.step_inputs(self.seed, self.layer, self.step, B=self.B, H_kv=self.H_kv,
                               H_q=self.H_q, D=self.D, dtype=self.dtype, k_draft=k,

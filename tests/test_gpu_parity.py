@@ -289,3 +289,23 @@ def test_token_tree_paper_example_gpu():
         p.commit_path([pth])
     p.check_state()
     p.close()
+
+
+@pytest.mark.parametrize("policy,r,prompt", [("bmc", 16, 1), ("bmc", 16, 16), ("bmc", 16, 17),
+                                             ("bmc", 24, 130), ("iterative", 1, 45),
+                                             ("upfront", 300, 77)])
+@pytest.mark.parametrize("host_io", [False, True])
+def test_bulk_prefill_then_decode(policy, r, prompt, host_io):
+    """bmc_append_n (prompt ingestion, one allocation: S:L104, reading R19)
+    then decode and a second bulk append mid-stream: cache bytes, lengths and
+    ledger bit-exact vs the oracle, every output within 2e-3."""
+    p = Pair(2, 2, 8, 128, r, 300, dtype="bf16", policy=policy, seed=41, host_io=host_io)
+    p.append_n(prompt)
+    p.check_state()
+    for _ in range(20):
+        p.append()
+        p.sdpa()
+    p.append_n(33)
+    p.sdpa()
+    p.check_state()
+    p.close()

@@ -1,7 +1,9 @@
 """Small workload for compute-sanitizer (memcheck / racecheck / synccheck):
 the toy config through every kernel: growth copies, fused appends, the CUDA-
-core attention (single layer and multi-layer step), SD with rollback, and the
-tcgen05 verify kernel; outputs checked against the oracle."""
+core attention (single layer and multi-layer step), SD with rollback, both
+tcgen05 kernels (keys on the TMEM lanes incl. N=80, a token tree and the fused
+GQA decode step; queries on the lanes), the bulk append; outputs checked
+against the oracle."""
 import os
 import sys
 
@@ -31,6 +33,50 @@ for it in range(12):
     p.commit_rows(synth.acceptance(3, it, 2, k))
 p.check_state()
 p.close()
+# the queries-on-lanes tcgen05 kernel, split units
+p = Pair(2, 1, 4, 128, 16, 96, dtype="bf16", seed=4, ctas=5)
+p.gpu.set_option(bmc.BMC_OPT_ATTN_PATH, 3)
+for it in range(8):
+    p.append()
+    k = p.spec_write(3)
+    p.sdpa(n_valid=-1)
+    p.commit_rows(synth.acceptance(4, it, 2, k))
+p.check_state()
+p.close()
+# keys on the lanes at N = 80 (M = 8 * 9), bulk prompt first
+p = Pair(1, 1, 8, 128, 32, 200, dtype="bf16", seed=5, ctas=3)
+p.gpu.set_option(bmc.BMC_OPT_ATTN_PATH, 4)
+p.append_n(70)
+for it in range(6):
+    p.append()
+    k = p.spec_write(8)
+    p.sdpa(n_valid=-1)
+    p.commit_rows(synth.acceptance(5, it, 1, k))
+p.check_state()
+p.close()
+# token tree through the keys-on-lanes kernel
+p = Pair(2, 1, 4, 128, 32, 160, dtype="bf16", seed=6)
+p.gpu.set_option(bmc.BMC_OPT_ATTN_PATH, 2)
+for _ in range(3):
+    p.append()
+for it in range(5):
+    p.append()
+    k = p.spec_write_tree(6, [-1, 0, 0, 1, 1, 2])
+    p.sdpa(n_valid=-1)
+    p.commit_path([[0, 1, 3][: it % 4], [0, 2][: (it + 1) % 3]])
+p.check_state()
+p.close()
+# fused GQA decode step (G = 4, keys-on-lanes kernel over 3 layers)
+caches = [bmc.KVCache(2, 2, 8, 128, 16, 64, dtype="bf16") for _ in range(3)]
+plan = bmc.StepPlan(caches)
+ks = [torch.randn(2, 2, 128, device="cuda").to(torch.bfloat16) for _ in range(3)]
+qs = [torch.randn(2, 8, 1, 128, device="cuda").to(torch.bfloat16) for _ in range(3)]
+os_ = [torch.empty(2, 8, 1, 128, device="cuda") for _ in range(3)]
+for n in range(1, 40):
+    bmc.bmc_decode_step(plan, plan.ptrs(ks), plan.ptrs(ks), plan.ptrs(qs), plan.ptrs(os_), n)
+torch.cuda.synchronize()
+for c in caches:
+    c.close()
 # multi-layer step
 caches = [bmc.KVCache(1, 2, 2, 128, 8, 32, dtype="bf16") for _ in range(3)]
 plan = bmc.StepPlan(caches)
