@@ -254,27 +254,41 @@ class KVCache:
     # Rows passed to append / spec_write are read by the next call that
     # touches the cache (include/bmc.h): keep them referenced until then so the
     # torch caching allocator cannot hand their memory to another tensor first.
+    # Host tensors are copied on the handle's own copy streams (pinned) and
+    # may still be read after the call returns: they are held until sync().
     _keep = ()
+    _hold = None
+
+    def _hold_host(self, *xs):
+        hs = [x for x in xs if isinstance(x, torch.Tensor) and x.device.type == "cpu"]
+        if hs:
+            if self._hold is None:
+                self._hold = []
+            self._hold.extend(hs)
 
     def append(self, K, V):
         rc = bmc_append(self.h, K, V)
         self._keep = (K, V)
+        self._hold_host(K, V)
         return rc
 
     def append_n(self, K, V, n):
         """Bulk (prompt) append, K/V [B][H_kv][n][D]."""
         rc = bmc_append_n(self.h, K, V, n)
         self._keep = (K, V)
+        self._hold_host(K, V)
         return rc
 
     def spec_write(self, Kd, Vd, k):
         rc = bmc_spec_write(self.h, Kd, Vd, k)
         self._keep = self._keep + (Kd, Vd)
+        self._hold_host(Kd, Vd)
         return rc
 
     def spec_write_tree(self, Kd, Vd, k, parent):
         rc = bmc_spec_write_tree(self.h, Kd, Vd, k, parent)
         self._keep = self._keep + (Kd, Vd)
+        self._hold_host(Kd, Vd)
         return rc
 
     def commit_path(self, paths):
@@ -289,6 +303,7 @@ class KVCache:
                             device=Q.device if isinstance(Q, torch.Tensor) else "cuda")
         bmc_sdpa(self.h, Q, n_valid, O)
         self._keep = ()
+        self._hold_host(Q, O)
         return O
 
     def commit(self, n):
@@ -323,6 +338,7 @@ class KVCache:
     def sync(self):
         rc = bmc_sync(self.h)
         self._keep = ()
+        self._hold = None
         return rc
 
     def close(self):

@@ -66,7 +66,36 @@ struct bmc_ctx {
   int tree = 0;                  // staged rows form a token tree
   uint32_t anc[32] = {};         // bit j of anc[i]: node j is node i or its ancestor
   struct Pipe* pipe = nullptr;   // host-I/O pipeline of bmc_decode_step (first layer owns it)
+  struct HostIO* hio = nullptr;  // copy streams of the per-call API's pinned host arguments
 };
+
+// Pinned-host arguments of the per-call API (append, spec_write, sdpa) are
+// copied on the handle's own upload / download streams, ordered against the
+// compute stream with events, so the copies of layer l+1 overlap the kernel of
+// layer l (the per-layer speculative-decoding loop's end-to-end path).
+struct HostIO {
+  cudaStream_t up = nullptr, down = nullptr;
+  cudaEvent_t in_ready[3] = {}, in_free[3] = {}, alloc_done = nullptr;
+  bool in_used[3] = {false, false, false};
+  cudaEvent_t out_ready = nullptr, out_free = nullptr;
+  bool out_used = false;
+};
+
+static void hio_destroy(HostIO* x) {
+  if (!x) return;
+  if (x->up) cudaStreamSynchronize(x->up);
+  if (x->down) cudaStreamSynchronize(x->down);
+  for (int i = 0; i < 3; ++i) {
+    if (x->in_ready[i]) cudaEventDestroy(x->in_ready[i]);
+    if (x->in_free[i]) cudaEventDestroy(x->in_free[i]);
+  }
+  if (x->alloc_done) cudaEventDestroy(x->alloc_done);
+  if (x->out_ready) cudaEventDestroy(x->out_ready);
+  if (x->out_free) cudaEventDestroy(x->out_free);
+  if (x->up) cudaStreamDestroy(x->up);
+  if (x->down) cudaStreamDestroy(x->down);
+  delete x;
+}
 
 // Host-I/O pipeline of bmc_decode_step: two staging slots, a copy stream and
 // events, so that the host->device copy of step s+1 and the device->host copy
@@ -153,32 +182,83 @@ static int ensure_stage_in(bmc_t h, int slot, size_t bytes) {
 
 // Map caller inputs (device or host) to device pointers; host inputs are
 // copied into the handle's staging buffer `slot` on its stream.
+static int ensure_hio(bmc_t h) {
+  if (h->hio) return 0;
+  HostIO* x = new HostIO();
+  h->hio = x;
+  CK(h, cudaStreamCreateWithFlags(&x->up, cudaStreamNonBlocking), "upload stream");
+  CK(h, cudaStreamCreateWithFlags(&x->down, cudaStreamNonBlocking), "download stream");
+  for (int i = 0; i < 3; ++i) {
+    CK(h, cudaEventCreateWithFlags(&x->in_ready[i], cudaEventDisableTiming), "event");
+    CK(h, cudaEventCreateWithFlags(&x->in_free[i], cudaEventDisableTiming), "event");
+  }
+  CK(h, cudaEventCreateWithFlags(&x->alloc_done, cudaEventDisableTiming), "event");
+  CK(h, cudaEventCreateWithFlags(&x->out_ready, cudaEventDisableTiming), "event");
+  CK(h, cudaEventCreateWithFlags(&x->out_free, cudaEventDisableTiming), "event");
+  return 0;
+}
+
+// The staged inputs of every slot have been consumed by the kernels enqueued
+// on the compute stream so far (called after each launch that reads them).
+static int inputs_consumed(bmc_t h) {
+  if (!h->hio) return 0;
+  for (int i = 0; i < 3; ++i)
+    if (h->hio->in_used[i]) CK(h, cudaEventRecord(h->hio->in_free[i], h->stream), "event");
+  return 0;
+}
+
+// Device pointers for the op's inputs: device arguments are used in place,
+// host arguments are copied into staging slot `slot` -- pinned ones on the
+// upload stream (overlapping earlier kernels), pageable ones on the compute
+// stream.
 static int device_inputs(bmc_t h, int slot, const void** ptrs, const size_t* bytes, int n,
                          const void** dev) {
   size_t need = 0;
-  bool any_host = false;
-  bool dev_ptr[8];
+  bool any_host = false, all_pinned = true;
+  int kind[8];
   for (int i = 0; i < n; ++i) {
-    dev_ptr[i] = is_device_ptr(ptrs[i]);
-    if (!dev_ptr[i]) {
+    kind[i] = ptr_kind(ptrs[i]);
+    if (kind[i] != 0) {
       any_host = true;
+      if (kind[i] != 1) all_pinned = false;
       need += (bytes[i] + 255) / 256 * 256;
     }
   }
-  if (any_host) {
-    int rc = ensure_stage_in(h, slot, need);
+  if (!any_host) {
+    for (int i = 0; i < n; ++i) dev[i] = ptrs[i];
+    return 0;
+  }
+  const bool grew = h->stage_in_bytes[slot] < need;
+  int rc = ensure_stage_in(h, slot, need);
+  if (rc) return rc;
+  cudaStream_t cs = h->stream;
+  if (all_pinned) {
+    rc = ensure_hio(h);
     if (rc) return rc;
+    HostIO* x = h->hio;
+    cs = x->up;
+    if (grew) {   // the new slot was allocated on the compute stream
+      CK(h, cudaEventRecord(x->alloc_done, h->stream), "event");
+      CK(h, cudaStreamWaitEvent(cs, x->alloc_done, 0), "wait");
+    }
+    if (x->in_used[slot]) CK(h, cudaStreamWaitEvent(cs, x->in_free[slot], 0), "wait");
   }
   size_t off = 0;
   for (int i = 0; i < n; ++i) {
-    if (dev_ptr[i]) {
+    if (kind[i] == 0) {
       dev[i] = ptrs[i];
     } else {
       void* d = (char*)h->stage_in[slot] + off;
-      CK(h, cudaMemcpyAsync(d, ptrs[i], bytes[i], cudaMemcpyHostToDevice, h->stream), "H2D");
+      CK(h, cudaMemcpyAsync(d, ptrs[i], bytes[i], cudaMemcpyHostToDevice, cs), "H2D");
       dev[i] = d;
       off += (bytes[i] + 255) / 256 * 256;
     }
+  }
+  if (all_pinned) {
+    HostIO* x = h->hio;
+    CK(h, cudaEventRecord(x->in_ready[slot], cs), "event");
+    CK(h, cudaStreamWaitEvent(h->stream, x->in_ready[slot], 0), "wait");
+    x->in_used[slot] = true;
   }
   return 0;
 }
@@ -244,6 +324,7 @@ static int flush_pending(bmc_t h) {
   if (h->n_app) rc = write_rows(h, h->knew, h->vnew, 1, 1, -1);   // row valid_b - 1
   if (!rc && h->n_draft) rc = write_rows(h, h->kd, h->vd, h->kd_stride, h->n_draft, 0);
   h->n_app = h->n_draft = 0;
+  if (!rc) rc = inputs_consumed(h);
   return rc;
 }
 
@@ -430,6 +511,7 @@ int bmc_append_n(bmc_t h, const void* K, const void* V, int n) {
   rc = device_inputs(h, 0, ptrs, sizes, 2, dev);
   if (rc) return rc;
   rc = write_rows(h, dev[0], dev[1], n, n, 0);
+  if (!rc) rc = inputs_consumed(h);
   if (rc) return rc;
   h->st.append_written_bytes += 2LL * h->U * n * h->row_bytes;
   for (auto& v : h->valid) v += n;
@@ -513,6 +595,9 @@ int bmc_sdpa(bmc_t h, const void* Q, int n_valid, float* O) {
   const bool host_out = out_kind != 0;
   float* od = O;
   if (host_out) {
+    // the previous download from the staging output must have finished
+    if (h->hio && h->hio->out_used)
+      CK(h, cudaStreamWaitEvent(h->stream, h->hio->out_free, 0), "wait");
     if (h->stage_out_bytes < o_bytes) {
       if (h->stage_out) cudaFreeAsync(h->stage_out, h->stream);
       h->stage_out = nullptr;
@@ -557,9 +642,22 @@ int bmc_sdpa(bmc_t h, const void* Q, int n_valid, float* O) {
   }
   h->n_app = h->n_draft = 0;
   account_sdpa(h, t);
+  rc = inputs_consumed(h);
+  if (rc) return rc;
   if (host_out) {
-    CK(h, cudaMemcpyAsync(O, od, o_bytes, cudaMemcpyDeviceToHost, h->stream), "D2H");
-    if (out_kind == 2) CK(h, cudaStreamSynchronize(h->stream), "sync");
+    if (out_kind == 1) {   // pinned: download on the handle's download stream
+      rc = ensure_hio(h);
+      if (rc) return rc;
+      HostIO* x = h->hio;
+      CK(h, cudaEventRecord(x->out_ready, h->stream), "event");
+      CK(h, cudaStreamWaitEvent(x->down, x->out_ready, 0), "wait");
+      CK(h, cudaMemcpyAsync(O, od, o_bytes, cudaMemcpyDeviceToHost, x->down), "D2H");
+      CK(h, cudaEventRecord(x->out_free, x->down), "event");
+      x->out_used = true;
+    } else {
+      CK(h, cudaMemcpyAsync(O, od, o_bytes, cudaMemcpyDeviceToHost, h->stream), "D2H");
+      CK(h, cudaStreamSynchronize(h->stream), "sync");
+    }
   }
   return 0;
 }
@@ -660,6 +758,8 @@ int bmc_decode_step(const bmc_t* hs, int L, const void* const* K, const void* co
   for (int l = 0; l < L; ++l) {
     hs[l]->n_app = hs[l]->n_draft = 0;
     account_sdpa(hs[l], 1);
+    int rc = inputs_consumed(hs[l]);
+    if (rc) return rc;
   }
   return 0;
 }
@@ -854,6 +954,8 @@ int bmc_destroy(bmc_t h) {
   cudaStreamSynchronize(h->stream);
   pipe_destroy(h->pipe);
   h->pipe = nullptr;
+  hio_destroy(h->hio);
+  h->hio = nullptr;
   bmc::arena_release(h->arena, &h->kbuf, h->stream);
   bmc::arena_release(h->arena, &h->vbuf, h->stream);
   for (int i = 0; i < 3; ++i)
@@ -922,6 +1024,10 @@ int bmc_sync(bmc_t h) {
     if (rc) return rc;
   }
   CK(h, cudaStreamSynchronize(h->stream), "sync");
+  if (h->hio) {
+    CK(h, cudaStreamSynchronize(h->hio->up), "sync upload stream");
+    CK(h, cudaStreamSynchronize(h->hio->down), "sync download stream");
+  }
   if (h->pipe) {
     CK(h, cudaStreamSynchronize(h->pipe->copy), "sync copy stream");
     CK(h, cudaStreamSynchronize(h->pipe->down), "sync copy stream");

@@ -121,9 +121,12 @@ def test_sd_admission_and_allocs():
     p.close()
 
 
-def test_host_pointer_io():
-    """The end-to-end path: host inputs staged inside the call, host output."""
-    p = Pair(2, 2, 4, 128, 16, 110, dtype="bf16", seed=17, host_io=True)
+@pytest.mark.parametrize("host_io", [True, "pinned"])
+def test_host_pointer_io(host_io):
+    """The end-to-end path: host inputs staged inside the call (pageable: on
+    the compute stream; pinned: on the handle's upload stream, event-ordered),
+    host output (pinned: downloaded on the handle's download stream)."""
+    p = Pair(2, 2, 4, 128, 16, 110, dtype="bf16", seed=17, host_io=host_io)
     _decode(p, 100, check_every=7)
     p.append()
     p.spec_write(3)
@@ -309,3 +312,21 @@ def test_bulk_prefill_then_decode(policy, r, prompt, host_io):
     p.sdpa()
     p.check_state()
     p.close()
+
+
+def test_pinned_per_layer_loop_overlaps_correctly():
+    """Two layers driven call by call with pinned host buffers, as the
+    speculative bench loop does: every upload of layer l+1 may overlap layer
+    l's kernel, every download the next layer's; all outputs and caches
+    against the oracle."""
+    ps = [Pair(2, 2, 4, 128, 16, 140, dtype="bf16", seed=50 + l, layer=l, host_io="pinned")
+          for l in range(2)]
+    for it in range(40):
+        for p in ps:
+            p.append()
+            k = p.spec_write(3)
+            p.sdpa(n_valid=-1)
+            p.commit_rows(synth.acceptance(50, it, 2, k))
+    for p in ps:
+        p.check_state()
+        p.close()
