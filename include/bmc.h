@@ -95,6 +95,28 @@ int bmc_create_ex(int B, int H_kv, int H_q, int D, int r, int N_max, bmc_dtype d
    staged, CAPACITY if max valid == N_max. */
 int bmc_append(bmc_t h, const void* K, const void* V);
 
+/* The number of drafts an append followed by bmc_spec_write(k) would admit
+   now (P:L867-869 admission after a possible growth): the t - 1
+   of the next verify step.  Host-only, no device work.  Errors: STATE
+   (drafts staged), CAPACITY (cache full), ARG (k < 0). */
+int bmc_admissible(bmc_t h, int k);
+
+/* One speculative-decoding iteration of L layers:
+   for every layer bmc_append(K[l], V[l]) and bmc_spec_write(Kd[l], Vd[l], k),
+   then the verify SDPA of all layers -- one persistent launch per 32 layers
+   when the layers share shape, stream, lengths and capacity and the kernel
+   takes several layers (CUDA cores for M = G*t <= 2, the keys-on-lanes
+   tcgen05 kernel for M <= 80), else one launch per layer.  K, V
+   [B][H_kv][D], Kd, Vd [B][H_kv][k][D] (device or host, as bmc_append /
+   bmc_spec_write); Q[l] DEVICE [B][H_q][t][D] and O[l] DEVICE
+   [B][H_q][t][D] fp32 with t = 1 + bmc_admissible(hs[l], k) (every layer
+   admits the same number).  Returns k_adm >= 0, or an error before anything
+   is enqueued (ARG, STATE, CAPACITY).  Commit afterwards per layer with
+   bmc_commit / bmc_commit_rows. */
+int bmc_spec_step(const bmc_t* hs, int L, const void* const* K, const void* const* V,
+                  const void* const* Kd, const void* const* Vd, int k,
+                  const void* const* Q, float* const* O);
+
 /* Bulk (prompt) append: n rows per unit, K and V [B][H_kv][n][D] in the
    cache dtype (device or host pointers).  Contents and lengths equal n
    bmc_append calls (P:L609 in-place writes); the allocation follows prompt

@@ -34,7 +34,7 @@ _NAMES = {0: "OK", -1: "ARG", -2: "STATE", -3: "CAPACITY", -4: "OOM", -5: "CUDA"
           -6: "UNSUPPORTED"}
 
 EXPORTS = ["bmc_create", "bmc_create_ex", "bmc_append", "bmc_append_n", "bmc_spec_write",
-           "bmc_sdpa",
+           "bmc_sdpa", "bmc_admissible", "bmc_spec_step",
            "bmc_commit", "bmc_commit_rows", "bmc_commit_path", "bmc_spec_write_tree",
            "bmc_decode_step", "bmc_destroy", "bmc_stats", "bmc_kv_view",
            "bmc_valid", "bmc_read_cache", "bmc_sync", "bmc_set_option", "bmc_launch_count", "bmc_last_error"]
@@ -73,6 +73,8 @@ def load(path: str = SO_PATH):
     L.bmc_create_ex.argtypes = [i, i, i, i, i, i, i, i, i, vp, ctypes.POINTER(vp)]
     L.bmc_append.argtypes = [vp, vp, vp]
     L.bmc_append_n.argtypes = [vp, vp, vp, ctypes.c_int]
+    L.bmc_admissible.argtypes = [vp, ctypes.c_int]
+    L.bmc_spec_step.argtypes = [vp, ctypes.c_int, vp, vp, vp, vp, ctypes.c_int, vp, vp]
     L.bmc_spec_write.argtypes = [vp, vp, vp, i]
     L.bmc_sdpa.argtypes = [vp, vp, i, vp]
     L.bmc_commit.argtypes = [vp, i]
@@ -170,6 +172,16 @@ def bmc_decode_step(plan: StepPlan, K, V, Q, O, n_valid: int) -> int:
     """K, V, Q, O: ctypes pointer arrays from plan.ptrs(...)."""
     return _check(load().bmc_decode_step(plan.hs, plan.L, K, V, Q, O, n_valid),
                   "bmc_decode_step")
+
+
+def bmc_admissible(h, k: int) -> int:
+    return _check(load().bmc_admissible(h, k), "bmc_admissible")
+
+
+def bmc_spec_step(plan: StepPlan, K, V, Kd, Vd, k: int, Q, O) -> int:
+    """One speculative iteration over the plan's layers; returns k_adm.
+    K, V, Kd, Vd, Q, O: ctypes pointer arrays from plan.ptrs(...)."""
+    return _check(load().bmc_spec_step(plan.hs, plan.L, K, V, Kd, Vd, k, Q, O), "bmc_spec_step")
 
 
 def bmc_spec_write_tree(h, K_draft, V_draft, k: int, parent) -> int:

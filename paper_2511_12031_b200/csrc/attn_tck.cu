@@ -818,10 +818,12 @@ static cudaError_t launch_layers(const AttnStepArgs& a, int l0, int nl, int num_
   if (ctas > p.total_tiles) ctas = (int)p.total_tiles;
   p.ctas = ctas;
   if (p.total_tiles == 0) return cudaSuccess;
-  if constexpr (MAXL > 1) {   // multi-layer launches: the GQA decode step, M = G <= 32
+  if constexpr (MAXL > 1) {   // multi-layer launches: GQA decode and speculative steps
     if (p.M <= 16) return launch_n<16, MAXL>(p, ctas, s);
     if (p.M <= 32) return launch_n<32, MAXL>(p, ctas, s);
-    return cudaErrorInvalidValue;
+    if (p.M <= 48) return launch_n<48, MAXL>(p, ctas, s);
+    if (p.M <= 64) return launch_n<64, MAXL>(p, ctas, s);
+    return launch_n<80, MAXL>(p, ctas, s);
   } else {
     if (p.M <= 16) return launch_n<16, 1>(p, ctas, s);
     if (p.M <= 32) return launch_n<32, 1>(p, ctas, s);

@@ -574,39 +574,10 @@ int bmc_spec_write_tree(bmc_t h, const void* K_draft, const void* V_draft, int k
   return k_adm;
 }
 
-int bmc_sdpa(bmc_t h, const void* Q, int n_valid, float* O) {
-  int rc = enter(h);
-  if (rc) return rc;
-  if (!Q || !O) return fail(BMC_ERR_ARG, "Q or O is null");
-  if (n_valid == 0) return fail(BMC_ERR_ARG, "n_valid == 0");
-  if (n_valid != BMC_PER_ROW) {
-    for (int b = 0; b < h->B; ++b)
-      if (h->valid[b] != n_valid)
-        return fail(BMC_ERR_STATE, "n_valid=%d but row %d holds %d", n_valid, b, h->valid[b]);
-  }
-  if (min_valid(h) == 0) return fail(BMC_ERR_ARG, "a batch row has no committed token");
-  const int t = 1 + h->staged;
-  const size_t q_bytes = (size_t)h->B * h->H_q * t * h->row_bytes;
-  const size_t o_bytes = (size_t)h->B * h->H_q * t * h->D * sizeof(float);
-  const void* qd = nullptr;
-  rc = device_inputs(h, 2, &Q, &q_bytes, 1, &qd);
-  if (rc) return rc;
-  const int out_kind = ptr_kind(O);
-  const bool host_out = out_kind != 0;
-  float* od = O;
-  if (host_out) {
-    // the previous download from the staging output must have finished
-    if (h->hio && h->hio->out_used)
-      CK(h, cudaStreamWaitEvent(h->stream, h->hio->out_free, 0), "wait");
-    if (h->stage_out_bytes < o_bytes) {
-      if (h->stage_out) cudaFreeAsync(h->stage_out, h->stream);
-      h->stage_out = nullptr;
-      h->stage_out_bytes = 0;
-      CK(h, cudaMallocAsync((void**)&h->stage_out, o_bytes, h->stream), "stage_out");
-      h->stage_out_bytes = o_bytes;
-    }
-    od = h->stage_out;
-  }
+// The attention launch of one layer (t query rows per head): kernel choice
+// by M = G*t, workspace, the layer's pending rows consumed.
+static int launch_sdpa_layer(bmc_t h, const void* qd, float* od, int t) {
+  int rc = 0;
   const int M = (h->H_q / h->H_kv) * t;
   // tensor cores when M = G*t makes a real tile (north_star item 4); the
   // crossover measured on B200 is M = 3..4 (tcgen05 1.4x faster at M=4,
@@ -642,7 +613,43 @@ int bmc_sdpa(bmc_t h, const void* Q, int n_valid, float* O) {
   }
   h->n_app = h->n_draft = 0;
   account_sdpa(h, t);
-  rc = inputs_consumed(h);
+  return inputs_consumed(h);
+}
+
+int bmc_sdpa(bmc_t h, const void* Q, int n_valid, float* O) {
+  int rc = enter(h);
+  if (rc) return rc;
+  if (!Q || !O) return fail(BMC_ERR_ARG, "Q or O is null");
+  if (n_valid == 0) return fail(BMC_ERR_ARG, "n_valid == 0");
+  if (n_valid != BMC_PER_ROW) {
+    for (int b = 0; b < h->B; ++b)
+      if (h->valid[b] != n_valid)
+        return fail(BMC_ERR_STATE, "n_valid=%d but row %d holds %d", n_valid, b, h->valid[b]);
+  }
+  if (min_valid(h) == 0) return fail(BMC_ERR_ARG, "a batch row has no committed token");
+  const int t = 1 + h->staged;
+  const size_t q_bytes = (size_t)h->B * h->H_q * t * h->row_bytes;
+  const size_t o_bytes = (size_t)h->B * h->H_q * t * h->D * sizeof(float);
+  const void* qd = nullptr;
+  rc = device_inputs(h, 2, &Q, &q_bytes, 1, &qd);
+  if (rc) return rc;
+  const int out_kind = ptr_kind(O);
+  const bool host_out = out_kind != 0;
+  float* od = O;
+  if (host_out) {
+    // the previous download from the staging output must have finished
+    if (h->hio && h->hio->out_used)
+      CK(h, cudaStreamWaitEvent(h->stream, h->hio->out_free, 0), "wait");
+    if (h->stage_out_bytes < o_bytes) {
+      if (h->stage_out) cudaFreeAsync(h->stage_out, h->stream);
+      h->stage_out = nullptr;
+      h->stage_out_bytes = 0;
+      CK(h, cudaMallocAsync((void**)&h->stage_out, o_bytes, h->stream), "stage_out");
+      h->stage_out_bytes = o_bytes;
+    }
+    od = h->stage_out;
+  }
+  rc = launch_sdpa_layer(h, qd, od, t);
   if (rc) return rc;
   if (host_out) {
     if (out_kind == 1) {   // pinned: download on the handle's download stream
@@ -660,6 +667,102 @@ int bmc_sdpa(bmc_t h, const void* Q, int n_valid, float* O) {
     }
   }
   return 0;
+}
+
+int bmc_admissible(bmc_t h, int k) {
+  int rc = enter(h);
+  if (rc) return rc;
+  if (k < 0) return fail(BMC_ERR_ARG, "k=%d < 0", k);
+  if (h->staged > 0) return fail(BMC_ERR_STATE, "drafts already staged");
+  const long long mv = max_valid(h);
+  if (mv >= h->N_max) return fail(BMC_ERR_CAPACITY, "cache full (N_max=%d)", h->N_max);
+  // state after the append: growth when full, then admission
+  // into the free rows; ITERATIVE is limited by N_max only
+  const long long mv1 = mv + 1;
+  if (h->pol == BMC_POLICY_ITERATIVE) return (int)std::min<long long>(k, h->N_max - mv1);
+  long long cap = h->cap;
+  if (h->pol == BMC_POLICY_BMC && mv == h->cap) cap = std::min<long long>(h->cap + h->r, h->N_max);
+  return (int)std::min<long long>(k, cap - mv1);
+}
+
+int bmc_spec_step(const bmc_t* hs, int L, const void* const* K, const void* const* V,
+                  const void* const* Kd, const void* const* Vd, int k, const void* const* Q,
+                  float* const* O) {
+  if (!hs || L < 1 || !K || !V || !Q || !O || k < 0 || (k > 0 && (!Kd || !Vd)))
+    return fail(BMC_ERR_ARG, "null argument or k < 0");
+  // validate every layer before enqueueing anything; all layers must admit
+  // the same number of drafts (they share the step sequence)
+  int k_adm = -1;
+  for (int l = 0; l < L; ++l) {
+    const int a = bmc_admissible(hs[l], k);
+    if (a < 0) return a;
+    if (k_adm >= 0 && a != k_adm)
+      return fail(BMC_ERR_STATE, "layer %d admits %d drafts, layer 0 %d", l, a, k_adm);
+    k_adm = a;
+    if (!K[l] || !V[l] || !Q[l] || !O[l] || (k > 0 && (!Kd[l] || !Vd[l])))
+      return fail(BMC_ERR_ARG, "layer %d: null tensor", l);
+    if (ptr_kind(Q[l]) != 0 || ptr_kind(O[l]) != 0)
+      return fail(BMC_ERR_ARG, "layer %d: bmc_spec_step takes device Q and O", l);
+  }
+  const int t = 1 + k_adm;
+  for (int l = 0; l < L; ++l) {
+    int rc = append_impl(hs[l], K[l], V[l]);
+    if (rc) return rc;
+    if (k > 0) {
+      rc = bmc_spec_write(hs[l], Kd[l], Vd[l], k);
+      if (rc < 0) return rc;
+    }
+  }
+  // one launch for the layers when they share shape, stream, lengths and
+  // capacity and the kernel takes several layers (CUDA cores, or the
+  // keys-on-lanes tcgen05 kernel up to M = 80); else one launch per layer
+  const bmc_t h0 = hs[0];
+  bool fused = true;
+  for (int l = 1; l < L; ++l) {
+    const bmc_t a = hs[l];
+    if (a->B != h0->B || a->H_kv != h0->H_kv || a->H_q != h0->H_q || a->D != h0->D ||
+        a->dt != h0->dt || a->stream != h0->stream || a->device != h0->device ||
+        a->valid != h0->valid || a->cap != h0->cap || a->attn_path != h0->attn_path ||
+        a->skip_padding != h0->skip_padding)
+      fused = false;
+  }
+  const int M = (h0->H_q / h0->H_kv) * t;
+  const bool tc = h0->attn_path >= 2 ||
+                  (h0->attn_path == 0 && M > kTcMinM && bmc::attn_tc_supported(h0->D, h0->dt, M));
+  const bool tck = tc && h0->attn_path != 3 && bmc::attn_tck_supported(h0->D, h0->dt, M);
+  if (tc && !tck) fused = false;
+  if (!fused) {
+    for (int l = 0; l < L; ++l) {
+      int rc = launch_sdpa_layer(hs[l], Q[l], O[l], t);
+      if (rc) return rc;
+    }
+    return k_adm;
+  }
+  std::vector<bmc::AttnLayer> layers(L);
+  for (int l = 0; l < L; ++l) {
+    if (tck) {
+      int rc = ensure_workspace(hs[l], M);
+      if (rc) return rc;
+    }
+    fill_layer(hs[l], Q[l], O[l], &layers[l]);
+  }
+  bmc::AttnStepArgs a;
+  fill_args(h0, t, &a);
+  a.L = L;
+  a.layers = layers.data();
+  if (tck) {
+    a.ctas = std::min(h0->attn_ctas, h0->num_sms);
+    CK(h0, bmc::launch_attn_tck(a, h0->num_sms, h0->stream), "attn_tck");
+  } else {
+    CK(h0, bmc::launch_attn_step(a, h0->num_sms, h0->stream), "attn_step");
+  }
+  for (int l = 0; l < L; ++l) {
+    hs[l]->n_app = hs[l]->n_draft = 0;
+    account_sdpa(hs[l], t);
+    int rc = inputs_consumed(hs[l]);
+    if (rc) return rc;
+  }
+  return k_adm;
 }
 
 static int decode_step_host(const bmc_t* hs, int L, const void* const* K, const void* const* V,
@@ -703,12 +806,12 @@ int bmc_decode_step(const bmc_t* hs, int L, const void* const* K, const void* co
   for (int l = 0; l < L; ++l)
     if (ptr_kind(Q[l]) != 0 || ptr_kind(O[l]) != 0) fused = false;
   // GQA groups large enough for the tensor cores take the tcgen05 kernel: the
-  // keys-on-lanes kernel fuses the layers (G <= 32), the other runs per layer
+  // keys-on-lanes kernel fuses the layers (G <= 80), the other runs per layer
   const bmc_t h0 = hs[0];
   const int G = h0->H_q / h0->H_kv;
   const bool tc = h0->attn_path != 1 && (h0->attn_path >= 2 || G > kTcMinM) &&
                   bmc::attn_tc_supported(h0->D, h0->dt, G);
-  const bool tck = tc && h0->attn_path != 3 && G <= 32 && bmc::attn_tck_supported(h0->D, h0->dt, G);
+  const bool tck = tc && h0->attn_path != 3 && bmc::attn_tck_supported(h0->D, h0->dt, G);
   for (int l = 1; l < L && tck; ++l)
     if (hs[l]->attn_path != h0->attn_path) fused = false;
   if (tc && !tck) fused = false;

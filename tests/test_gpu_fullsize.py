@@ -241,3 +241,56 @@ def test_decode_step_host_io_pipeline():
         assert torch.equal(_bits(kx), _bits(ky)) and torch.equal(_bits(vx), _bits(vy))
     for x in a + b:
         x.close()
+
+
+@pytest.mark.parametrize("H_kv,H_q,k,L", [(2, 2, 1, 3), (2, 2, 4, 3), (2, 8, 3, 3),
+                                          (1, 8, 8, 3), (2, 4, 4, 34), (1, 16, 8, 2)])
+def test_spec_step_matches_per_layer_calls(H_kv, H_q, k, L):
+    """bmc_spec_step (append + spec_write of every layer, then one verify
+    launch per 32 layers: CUDA cores for M <= 2, keys-on-lanes tcgen05 up to
+    M = 80, per-layer launches above) matches per-layer append / spec_write /
+    sdpa calls: admissions, caches and ledgers identical, outputs equal up to
+    the split-K summation order; per-row commits in between."""
+    B, D, N, r = 2, 128, 160, 24
+    dev = torch.device("cuda")
+    a = [bmc.KVCache(B, H_kv, H_q, D, r, N, dtype="bf16") for _ in range(L)]
+    b = [bmc.KVCache(B, H_kv, H_q, D, r, N, dtype="bf16") for _ in range(L)]
+    plan = bmc.StepPlan(a)
+    g = torch.Generator(device=dev)
+    g.manual_seed(11)
+    it = 0
+    while max(a[0].valid()) < N - 1 - k:
+        kad = bmc.bmc_admissible(a[0].h, k)
+        t = 1 + kad
+        ks = [torch.randn(B, H_kv, D, generator=g, device=dev).to(torch.bfloat16) for _ in range(L)]
+        vs = [torch.randn(B, H_kv, D, generator=g, device=dev).to(torch.bfloat16) for _ in range(L)]
+        kd = [torch.randn(B, H_kv, k, D, generator=g, device=dev).to(torch.bfloat16)
+              for _ in range(L)]
+        vd = [torch.randn(B, H_kv, k, D, generator=g, device=dev).to(torch.bfloat16)
+              for _ in range(L)]
+        qs = [torch.randn(B, H_q, t, D, generator=g, device=dev).to(torch.bfloat16)
+              for _ in range(L)]
+        oa = [torch.empty(B, H_q, t, D, device=dev) for _ in range(L)]
+        got = bmc.bmc_spec_step(plan, plan.ptrs(ks), plan.ptrs(vs), plan.ptrs(kd), plan.ptrs(vd),
+                                k, plan.ptrs(qs), plan.ptrs(oa))
+        assert got == kad
+        ob = []
+        for l in range(L):
+            b[l].append(ks[l], vs[l])
+            assert b[l].spec_write(kd[l], vd[l], k) == kad
+            ob.append(b[l].sdpa(qs[l], -1))
+        torch.cuda.synchronize()
+        for l in range(L):
+            torch.testing.assert_close(oa[l], ob[l], rtol=0, atol=2e-5)
+        acc = [int((it * 7 + 3 * bb) % (kad + 1)) for bb in range(B)]
+        for l in range(L):
+            a[l].commit_rows(acc)
+            b[l].commit_rows(acc)
+        it += 1
+    for l in range(L):
+        ka, va = a[l].kv()
+        kb, vb = b[l].kv()
+        assert torch.equal(_bits(ka), _bits(kb)) and torch.equal(_bits(va), _bits(vb))
+        assert a[l].stats() == b[l].stats()
+    for x in a + b:
+        x.close()
