@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libbmc.so")
 SOURCES = ["cache_kernels.cu", "attn_decode.cu", "attn_tc.cu", "attn_tck.cu", "arena.cpp", "bmc_abi.cpp"]
-HEADERS = ["bmc_internal.h", os.path.join("..", "..", "include", "bmc.h")]
+HEADERS = ["bmc_internal.h", "combine.cuh", "tc_common.cuh", os.path.join("..", "..", "include", "bmc.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 

@@ -18,7 +18,9 @@
 //            A = K tile (K-major SW128), B = Q (K-major SW128, smem);
 //     O^T    (TMEM, 128 dim lanes x 2N cols fp32) += V_tile^T . [P_hi; P_lo]^T
 //            M=128 (dims) x 2N x K=128 (keys), A = V tile (MN-major SW128),
-//            B = P^T hi rows then lo rows (K-major SW128, smem),
+//            B = P^T hi columns then lo columns (MN-major SWIZZLE_32B, smem:
+//            a thread holds one key and N/2 consecutive queries, so its P
+//            values are contiguous and go out as 16-byte stores),
 // so every lane of every softmax warp carries one key and a thread's work per
 // tile is the N/2 queries of its half, not 32 keys: the exp2 / pack work is
 // spread over all four SMSPs and shrinks by 128/N.
@@ -76,9 +78,10 @@ struct Cfg {
   static constexpr uint32_t OFF_Q = OFF_V + VS * kTileBytes;   // [2 bufs][2 dim atoms][N][128 B]
   static constexpr uint32_t kQAtom = N * 128;
   static constexpr uint32_t kQBytes = 2 * kQAtom;
-  static constexpr uint32_t OFF_P = OFF_Q + 2 * kQBytes;       // [NBP][2 key atoms][2N][128 B]
-  static constexpr uint32_t kPAtom = 2 * N * 128;
-  static constexpr uint32_t kPBytes = 2 * kPAtom;
+  // P^T (MN-major SWIZZLE_32B): [NBP][2N/16 query blocks][128 keys][32 B]
+  static constexpr uint32_t OFF_P = OFF_Q + 2 * kQBytes;
+  static constexpr uint32_t kPBlock = KT * 32;                 // LBO: one 16-query block
+  static constexpr uint32_t kPBytes = 2 * N / 16 * kPBlock;
   static constexpr uint32_t OFF_BAR = OFF_P + NBP * kPBytes;
   static constexpr uint32_t OFF_RED = OFF_BAR + 512;           // [2 halves][4 quadrants][NH] f32
   static constexpr uint32_t OFF_SUM = OFF_RED + 2 * 4 * NH * 4;  // [2][4][NH] f32
@@ -89,7 +92,8 @@ struct Cfg {
   static constexpr uint32_t OFF_QM = OFF_LIM + 2 * NH * 4;       // [2][NH] ancestor masks
   static constexpr uint32_t kSmem = OFF_QM + 2 * NH * 4;
   static_assert(kSmem <= 232448, "shared memory");
-  static_assert(kQAtom % 1024 == 0 && kPAtom % 1024 == 0, "SW128 atoms");
+  static_assert(kQAtom % 1024 == 0 && kPBytes % 1024 == 0, "swizzle atoms");
+  static_assert(NH % 8 == 0, "16-byte P stores");
   static_assert(NBP * kPBytes >= (4 + 2) * N * 4, "combine scratch in the P area");
   // TMEM columns: S^T[b] at b*N, O^T (hi N cols, lo N cols) at NB*N
   static constexpr uint32_t TM_O = NB * N;
@@ -164,8 +168,11 @@ __device__ __forceinline__ bool half_any(int h, bool pred) {
       : "memory");
   return r != 0;
 }
-__device__ __forceinline__ void sts_u16(uint32_t addr, uint32_t v) {
-  asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"((unsigned short)v) : "memory");
+__device__ __forceinline__ void sts_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c,
+                                       uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),
+               "r"(d)
+               : "memory");
 }
 __device__ __forceinline__ void fence_proxy_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -376,7 +383,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
   } else if (warp == 11) {
     // ------------------------------------------------------ O^T += V^T P^T issuer
     if (lane == 0) {
-      constexpr uint32_t IPV = idesc_bf16(D, 2 * N, 1, 0);   // A = V tile, MN-major
+      constexpr uint32_t IPV = idesc_bf16(D, 2 * N, 1, 1);   // A = V tile, B = P^T: MN-major
       int vs = 0;
       uint32_t vph = 0;
       long long i = t_begin;
@@ -397,9 +404,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
           const uint32_t pb = sbase + C::OFF_P + b * C::kPBytes;
 #pragma unroll
           for (int kk = 0; kk < KT / 16; ++kk) {
-            const uint32_t poff = (kk >> 2) * C::kPAtom + (kk & 3) * 32;
-            umma_f16(tmem + C::TM_O, sdesc(vt + kk * 2048, kBox, 1024), sdesc(pb + poff, 16, 1024),
-                     IPV, (k > 0 || kk > 0) ? 1u : 0u);
+            // 16 keys = two 8-key groups of 256 B (SBO); 16-query blocks kPBlock apart (LBO)
+            umma_f16(tmem + C::TM_O, sdesc(vt + kk * 2048, kBox, 1024),
+                     sdesc_sw32(pb + kk * 512, C::kPBlock, 256), IPV, (k > 0 || kk > 0) ? 1u : 0u);
           }
           TRACE(7, tc);
           umma_commit(PEMPTY(b));
@@ -425,9 +432,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
     float* asm_ = reinterpret_cast<float*>(smem + C::OFF_A) + h * NH;        // rescale factors
     int* lim = reinterpret_cast<int*>(smem + C::OFF_LIM) + h * NH;           // keys < lim visible
     uint32_t* qmk = reinterpret_cast<uint32_t*>(smem + C::OFF_QM) + h * NH;  // + these drafts
-    // P^T store address of key kl: key atom kl/64, 16-byte chunk (kl%64)/8 (swizzled by row)
-    const uint32_t pkey = (uint32_t)(kl >> 6) * C::kPAtom + (uint32_t)(kl & 7) * 2;
-    const uint32_t pchunk = (uint32_t)((kl & 63) >> 3);
+    // P^T (MN-major SWIZZLE_32B) address of key kl's 8-query chunk e:
+    //   (e/2)*kPBlock + (kl/8)*256 + (kl%8)*32 + (((e&1) ^ bit2(kl)) << 4);
+    // the 8 lanes of a store phase cover all 32 banks
+    const uint32_t pkey = (uint32_t)(kl >> 3) * 256u + (uint32_t)(kl & 7) * 32u;
+    const uint32_t pswz = (uint32_t)(kl >> 2) & 1u;
+    auto paddr = [&](int e) -> uint32_t {
+      return (uint32_t)(e >> 1) * C::kPBlock + pkey + ((((uint32_t)e & 1u) ^ pswz) << 4);
+    };
     // Q rows of the item starting at tile x0 (zero beyond M) into Q buffer qb
     auto load_q = [&](long long x0, int qb) {
       const long long guq = x0 / p.tpu;
@@ -594,12 +606,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
             fence_before();
           }
         }
-        // P^T[pb] was last read by the O^T MMAs of tile tc - NBP
-        if (stid == 0) TRACE(11, tc);
-        if (tc >= C::NBP) mbar_wait(PEMPTY(pb), ((tc / C::NBP) - 1) & 1);
-        if (stid == 0) TRACE(12, tc);
-        const uint32_t pbase = sbase + C::OFF_P + pb * C::kPBytes + pkey;
+        // P = 2^(x - m) and its bf16 hi / lo halves, packed two queries per
+        // word, before waiting for the P^T buffer (overlaps the previous
+        // tile's O^T MMAs)
         const float* msf = msm + mv * 3 * NH + NH;   // m, or 0 while m = -inf (then x = -inf)
+        uint32_t phi[NH / 2], plo[NH / 2];
 #pragma unroll
         for (int c0 = 0; c0 < NH; c0 += 8) {
           float mr[8];
@@ -611,17 +622,25 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
             const float2 d = __fadd2_rn(make_float2(x[c], x[c + 1]), make_float2(-mr[e], -mr[e + 1]));
             const float2 pv = make_float2(fast_exp2(d.x), fast_exp2(d.y));
             l2[c / 2] = __fadd2_rn(l2[c / 2], pv);
-#pragma unroll
-            for (int z = 0; z < 2; ++z) {
-              const float pz = z ? pv.y : pv.x;
-              const uint32_t bits = __float_as_uint(pz);
-              const float hi = __uint_as_float(bits & 0xffff0000u);
-              const uint32_t lo = (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(pz - hi));
-              const uint32_t rh = (uint32_t)(h * NH + c + z), rl = rh + N;   // P^T rows: hi, lo
-              sts_u16(pbase + rh * 128 + ((pchunk ^ (rh & 7u)) << 4), bits >> 16);
-              sts_u16(pbase + rl * 128 + ((pchunk ^ (rl & 7u)) << 4), lo);
-            }
+            const uint32_t bx = __float_as_uint(pv.x), by = __float_as_uint(pv.y);
+            phi[c / 2] = __byte_perm(bx, by, 0x7632);          // upper halves: bf16 hi (truncated)
+            const float2 lo = __fadd2_rn(pv, make_float2(-__uint_as_float(bx & 0xffff0000u),
+                                                          -__uint_as_float(by & 0xffff0000u)));
+            const __nv_bfloat162 lb = __floats2bfloat162_rn(lo.x, lo.y);
+            plo[c / 2] = *reinterpret_cast<const uint32_t*>(&lb);
           }
+        }
+        // P^T[pb] was last read by the O^T MMAs of tile tc - NBP
+        if (stid == 0) TRACE(11, tc);
+        if (tc >= C::NBP) mbar_wait(PEMPTY(pb), ((tc / C::NBP) - 1) & 1);
+        if (stid == 0) TRACE(12, tc);
+        const uint32_t pbase = sbase + C::OFF_P + pb * C::kPBytes;
+#pragma unroll
+        for (int e = 0; e < NH / 8; ++e) {
+          const int eh = h * (NH / 8) + e;               // hi chunk; lo chunks follow N / 8 later
+          sts_v4(pbase + paddr(eh), phi[4 * e], phi[4 * e + 1], phi[4 * e + 2], phi[4 * e + 3]);
+          sts_v4(pbase + paddr(eh + N / 8), plo[4 * e], plo[4 * e + 1], plo[4 * e + 2],
+                 plo[4 * e + 3]);
         }
         fence_proxy_smem();
         mbar_arrive(PFULL(pb));

@@ -179,6 +179,18 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
   d |= (uint64_t)2 << 61;   // SWIZZLE_128B
   return d;
 }
+// Same, SWIZZLE_32B (layout type 6): MN-major atoms of 16 elements x 8 rows
+// (Swizzle<1,4,3>: address bit 4 ^= bit 7); LBO = stride between 16-element
+// MN blocks, SBO = stride between 8-row K groups.
+__device__ __forceinline__ uint64_t sdesc_sw32(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;   // version (Blackwell)
+  d |= (uint64_t)6 << 61;   // SWIZZLE_32B
+  return d;
+}
 // Instruction descriptor kind::f16: fp32 accumulate, bf16 A and B.
 __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int a_mn_major, int b_mn_major) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn_major << 15) |

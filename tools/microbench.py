@@ -145,6 +145,9 @@ def main():
         out["verify"] = [attn_at(8, 8, 64, 128, 8192, t=9, path=2, reps=6, layers=2)]
     if args.what == "tc8":            # ncu target: 70B-shaped decode on tensor cores, M = 8
         out["verify"] = [attn_at(8, 8, 64, 128, 8192, t=1, path=2, reps=6, layers=2)]
+    if args.what == "tcsweep":        # keys-on-lanes kernel: 70B shape, M = 8 t
+        out["tck"] = [attn_at(8, 8, 64, 128, cap, t=t, path=4, reps=8, layers=4)
+                      for cap in (8192, 32768) for t in (1, 2, 4, 5, 8, 9)]
     if args.what == "tcrepro":
         out["verify"] = [attn_at(8, 8, 64, 128, 1024, t=9, path=1, reps=4, layers=2)]
     if args.what == "attn4096":       # ncu target: 7B shape at full context
