@@ -164,6 +164,15 @@ int bmc_commit(bmc_t h, int n_accepted);
 /* bmc_commit_rows: per-row acceptance, n_accepted_host[B] (host array). */
 int bmc_commit_rows(bmc_t h, const int* n_accepted_host);
 
+/* bmc_commit_step: bmc_commit_rows(hs[l], n_accepted_host) for the L layers
+   of one speculative iteration (the counterpart of bmc_spec_step).
+   Every layer must accept the same n_accepted_host[B] (layers share the token
+   sequence).  Layers that share stream, capacity, lengths and staged count
+   get ONE zero-fill launch (rejected drafts, reading R9) per 32 layers; others
+   are committed one by one.  Errors: as bmc_commit_rows, checked on every
+   layer before anything is enqueued. */
+int bmc_commit_step(const bmc_t* hs, int L, const int* n_accepted_host);
+
 /* bmc_commit_path: commit one accepted root-to-node path per batch row
    (P:L447): path_host[b * max_depth + i], i < m_host[b], node
    indices of increasing depth (path[0] a root, path[i] a child of

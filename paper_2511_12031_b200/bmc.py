@@ -35,7 +35,7 @@ _NAMES = {0: "OK", -1: "ARG", -2: "STATE", -3: "CAPACITY", -4: "OOM", -5: "CUDA"
 
 EXPORTS = ["bmc_create", "bmc_create_ex", "bmc_append", "bmc_append_n", "bmc_spec_write",
            "bmc_sdpa", "bmc_admissible", "bmc_spec_step",
-           "bmc_commit", "bmc_commit_rows", "bmc_commit_path", "bmc_spec_write_tree",
+           "bmc_commit", "bmc_commit_rows", "bmc_commit_step", "bmc_commit_path", "bmc_spec_write_tree",
            "bmc_decode_step", "bmc_destroy", "bmc_stats", "bmc_kv_view",
            "bmc_valid", "bmc_read_cache", "bmc_sync", "bmc_set_option", "bmc_launch_count", "bmc_last_error"]
 
@@ -79,6 +79,7 @@ def load(path: str = SO_PATH):
     L.bmc_sdpa.argtypes = [vp, vp, i, vp]
     L.bmc_commit.argtypes = [vp, i]
     L.bmc_commit_rows.argtypes = [vp, ctypes.POINTER(ctypes.c_int)]
+    L.bmc_commit_step.argtypes = [vp, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
     L.bmc_destroy.argtypes = [vp]
     L.bmc_spec_write_tree.argtypes = [vp, vp, vp, i, ctypes.POINTER(ctypes.c_int)]
     L.bmc_commit_path.argtypes = [vp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int), i]
@@ -182,6 +183,12 @@ def bmc_spec_step(plan: StepPlan, K, V, Kd, Vd, k: int, Q, O) -> int:
     """One speculative iteration over the plan's layers; returns k_adm.
     K, V, Kd, Vd, Q, O: ctypes pointer arrays from plan.ptrs(...)."""
     return _check(load().bmc_spec_step(plan.hs, plan.L, K, V, Kd, Vd, k, Q, O), "bmc_spec_step")
+
+
+def bmc_commit_step(plan: StepPlan, n_accepted) -> int:
+    """Per-row commit of every layer of the plan (one zero-fill launch)."""
+    arr = (ctypes.c_int * len(n_accepted))(*[int(x) for x in n_accepted])
+    return _check(load().bmc_commit_step(plan.hs, plan.L, arr), "bmc_commit_step")
 
 
 def bmc_spec_write_tree(h, K_draft, V_draft, k: int, parent) -> int:

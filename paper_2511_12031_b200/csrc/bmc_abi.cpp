@@ -962,8 +962,9 @@ static int commit_impl(bmc_t h, const int* m) {
     if (rc) return rc;
   }
   bmc::ZeroArgs z;
-  z.k = h->kbuf.ptr;
-  z.v = h->vbuf.ptr;
+  z.k[0] = h->kbuf.ptr;
+  z.v[0] = h->vbuf.ptr;
+  z.L = 1;
   z.B = h->B;
   z.H_kv = h->H_kv;
   z.cap = h->cap;
@@ -1048,6 +1049,72 @@ int bmc_commit_rows(bmc_t h, const int* n_accepted_host) {
       return fail(BMC_ERR_STATE, "a staged token tree is committed with bmc_commit_path");
   }
   return commit_impl(h, n_accepted_host);
+}
+
+int bmc_commit_step(const bmc_t* hs, int L, const int* n_accepted_host) {
+  if (!hs || L < 1 || !n_accepted_host) return fail(BMC_ERR_ARG, "null argument or L < 1");
+  // validate every layer before enqueueing anything (as bmc_commit_rows)
+  for (int l = 0; l < L; ++l) {
+    const bmc_t h = hs[l];
+    int rc = enter(h);
+    if (rc) return rc;
+    if (h->B != hs[0]->B) return fail(BMC_ERR_ARG, "layer %d: batch differs from layer 0", l);
+    for (int b = 0; b < h->B; ++b) {
+      const int m = n_accepted_host[b];
+      if (h->staged == 0 && m > 0) return fail(BMC_ERR_STATE, "layer %d: nothing staged", l);
+      if (m < 0 || m > h->staged)
+        return fail(BMC_ERR_ARG, "n_accepted[%d]=%d outside [0, %d] (layer %d)", b, m, h->staged, l);
+      if (h->tree && m > 0)
+        return fail(BMC_ERR_STATE, "a staged token tree is committed with bmc_commit_path");
+    }
+  }
+  const bmc_t h0 = hs[0];
+  bool fused = true;
+  for (int l = 0; l < L; ++l) {
+    const bmc_t a = hs[l];
+    if (a->n_app || a->n_draft || a->H_kv != h0->H_kv || a->stream != h0->stream ||
+        a->device != h0->device || a->cap != h0->cap || a->row_bytes != h0->row_bytes ||
+        a->staged != h0->staged || a->valid != h0->valid)
+      fused = false;
+  }
+  if (!fused) {
+    for (int l = 0; l < L; ++l) {
+      int rc = enter(hs[l]);
+      if (rc) return rc;
+      rc = commit_impl(hs[l], n_accepted_host);
+      if (rc) return rc;
+    }
+    return 0;
+  }
+  // one zero_rows launch per kMaxZeroLayers layers for the rejected drafts (reading R9)
+  bmc::ZeroArgs z;
+  z.B = h0->B;
+  z.H_kv = h0->H_kv;
+  z.cap = h0->cap;
+  z.row_bytes = h0->row_bytes;
+  z.max_rows = 0;
+  for (int b = 0; b < h0->B; ++b) {
+    z.row_lo[b] = h0->valid[b] + n_accepted_host[b];
+    z.row_hi[b] = h0->valid[b] + h0->staged;
+    z.max_rows = std::max(z.max_rows, h0->staged - n_accepted_host[b]);
+  }
+  if (z.max_rows > 0) {
+    for (int l0 = 0; l0 < L; l0 += bmc::kMaxZeroLayers) {
+      z.L = std::min(bmc::kMaxZeroLayers, L - l0);
+      for (int l = 0; l < z.L; ++l) {
+        z.k[l] = hs[l0 + l]->kbuf.ptr;
+        z.v[l] = hs[l0 + l]->vbuf.ptr;
+      }
+      CK(h0, bmc::launch_zero_rows(z, h0->stream), "zero_rows");
+    }
+  }
+  for (int l = 0; l < L; ++l) {
+    const bmc_t h = hs[l];
+    for (int b = 0; b < h->B; ++b) h->valid[b] += n_accepted_host[b];
+    h->staged = 0;
+    h->tree = 0;
+  }
+  return 0;
 }
 
 int bmc_destroy(bmc_t h) {

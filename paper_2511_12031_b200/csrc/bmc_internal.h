@@ -33,8 +33,11 @@ struct RowsArgs {
 };
 cudaError_t launch_write_rows(const RowsArgs& a, cudaStream_t s);
 
+constexpr int kMaxZeroLayers = 32;
 struct ZeroArgs {
-  void* k; void* v;                       // [U][cap][D]
+  void* k[kMaxZeroLayers];                // per layer [U][cap][D] (L layers of one shape)
+  void* v[kMaxZeroLayers];
+  int L;
   int B, H_kv;
   long long cap;
   int row_bytes;

@@ -107,11 +107,14 @@ cudaError_t launch_write_rows(const RowsArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-__global__ void zero_rows_kernel(const ZeroArgs a) {
+// grid covers L layers x {K, V} x units x max_rows x 16-byte chunks
+__global__ void zero_rows_kernel(const __grid_constant__ ZeroArgs a) {
   const int row_vec = a.row_bytes / 16;
   const long long per_tensor = (long long)a.B * a.H_kv * a.max_rows * row_vec;
   long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= 2 * per_tensor) return;
+  if (i >= 2 * a.L * per_tensor) return;
+  const int layer = (int)(i / (2 * per_tensor));
+  i -= layer * 2 * per_tensor;
   const int tensor = (int)(i / per_tensor);
   i -= tensor * per_tensor;
   const int vec = (int)(i % row_vec);
@@ -121,12 +124,12 @@ __global__ void zero_rows_kernel(const ZeroArgs a) {
   const int b = (int)(u / a.H_kv);
   const int lo = a.row_lo[b], hi = a.row_hi[b];
   if (lo + row >= hi) return;
-  int4* dst = (int4*)(tensor == 0 ? a.k : a.v);
+  int4* dst = (int4*)(tensor == 0 ? a.k[layer] : a.v[layer]);
   dst[(u * a.cap + lo + row) * row_vec + vec] = make_int4(0, 0, 0, 0);
 }
 
 cudaError_t launch_zero_rows(const ZeroArgs& a, cudaStream_t s) {
-  const long long total = 2LL * a.B * a.H_kv * a.max_rows * (a.row_bytes / 16);
+  const long long total = 2LL * a.L * a.B * a.H_kv * a.max_rows * (a.row_bytes / 16);
   if (total == 0) return cudaSuccess;
   const int threads = 256;
   zero_rows_kernel<<<(unsigned)((total + threads - 1) / threads), threads, 0, s>>>(a);

@@ -250,7 +250,8 @@ def test_spec_step_matches_per_layer_calls(H_kv, H_q, k, L):
     launch per 32 layers: CUDA cores for M <= 2, keys-on-lanes tcgen05 up to
     M = 80, per-layer launches above) matches per-layer append / spec_write /
     sdpa calls: admissions, caches and ledgers identical, outputs equal up to
-    the split-K summation order; per-row commits in between."""
+    the split-K summation order; per-row commits in between (bmc_commit_step
+    against per-layer bmc_commit_rows)."""
     B, D, N, r = 2, 128, 160, 24
     dev = torch.device("cuda")
     a = [bmc.KVCache(B, H_kv, H_q, D, r, N, dtype="bf16") for _ in range(L)]
@@ -283,8 +284,13 @@ def test_spec_step_matches_per_layer_calls(H_kv, H_q, k, L):
         for l in range(L):
             torch.testing.assert_close(oa[l], ob[l], rtol=0, atol=2e-5)
         acc = [int((it * 7 + 3 * bb) % (kad + 1)) for bb in range(B)]
+        if kad:   # bmc_commit_step: one zero-fill launch per 32 layers; errors before any work
+            with pytest.raises(bmc.BMCError):
+                bmc.bmc_commit_step(plan, [kad + 1] * B)
+            bmc.bmc_commit_step(plan, acc)
         for l in range(L):
-            a[l].commit_rows(acc)
+            if not kad:
+                a[l].commit_rows(acc)
             b[l].commit_rows(acc)
         it += 1
     for l in range(L):
