@@ -237,11 +237,19 @@ int bmc_sync(bmc_t h);
      4 BMC_OPT_SKIP_PADDING   1 = length-aware ABLATION: SDPA streams only the
                               rows some query sees instead of all cap rows
                               (not the method: P:L441, L853; results are
-                              identical, bytes differ)  */
+                              identical, bytes differ)
+     5 BMC_OPT_COPY_ON_READ   1 (default) = a BMC growth inside bmc_decode_step
+                              (CUDA-core attention path) is copied by the
+                              attention kernel while it streams the old
+                              buffer (old rows read once, new
+                              buffer written once, no separate realloc
+                              kernel); 0 = separate realloc_copy_zero launch.
+                              Cache contents and ledger are identical.  */
 #define BMC_OPT_ATTN_CTAS 1
 #define BMC_OPT_ATTN_PATH 2
 #define BMC_OPT_ARENA 3
 #define BMC_OPT_SKIP_PADDING 4
+#define BMC_OPT_COPY_ON_READ 5
 int bmc_set_option(bmc_t h, int key, long long value);
 
 /* Kernels launched by this library in this process so far (all handles). */

@@ -25,6 +25,14 @@
 //    fp32 registers; q is held pre-scaled by log2(e)/sqrt(D) and scores use
 //    exp2.  Dot products use packed FFMA2; the per-row reduction uses warp
 //    shuffles over the lanes that split the row.
+//  * Copy-on-read growth (SURVEY NEXT-1, P:L676-678 fused with P:L853): at a
+//    growth step the tiles are read from the OLD buffer (rows < cap_old) and
+//    from an L2-resident zero page (rows >= cap_old), and every staged tile
+//    (after the appended row is patched in) is written to the NEW buffer with
+//    a bulk shared->global copy.  That is the realloc copy + zero fill + row
+//    write of the growth without a separate kernel and without reading the
+//    new buffer back: cap_old rows read + cap_new rows written instead of
+//    cap_old + cap_new (copy) + cap_new (attention).
 //  * At a unit boundary the warps merge in shared memory.  A unit covered by
 //    one CTA writes O directly; otherwise each CTA writes a partial
 //    (max, sum, o) record and the last CTA to finish the unit (atomic
@@ -77,6 +85,28 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read() {   // smem sources of my bulk stores are read
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_g2s_plain(void* dst, const void* src, uint32_t bytes,
+                                               uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
 __device__ __forceinline__ uint64_t evict_first_policy() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -113,10 +143,18 @@ struct Chunk<float> {
   }
 };
 
+// Zeros for the rows a copy-on-read growth adds (static device memory is
+// zero-initialised; the page stays L2-resident, so it costs no HBM reads).
+__device__ __align__(128) uint8_t g_zero_page[kStageBytes];
+
 // One layer of a launch (host fills it; kernel parameter space).
 struct LayerDesc {
   const uint8_t* K;      // cache [U][cap][D]
   const uint8_t* V;
+  const uint8_t* Ksrc;   // copy-on-read growth: old buffer [U][cap_src][D] (else null);
+  const uint8_t* Vsrc;   //   K / V above are then the new buffer the tiles are written to
+  long long cap_src;     // old row stride
+  long long rows_src;    // rows [0, rows_src) come from the old buffer, the rest are zero
   const uint8_t* Q;      // [B][H_q][t][D]
   float* O;              // [B][H_q][t][D]
   const uint8_t* Knew;   // pending appended row per unit [B][H_kv][D] (n_app == 1)
@@ -249,8 +287,22 @@ __global__ void __launch_bounds__(kThreads, CTAS) attn_step_kernel(const __grid_
     const size_t off = (size_t)(pc.u * ld.cap + row0) * C::ROWB;
     uint8_t* dk = ring + (size_t)ps_stage * 2 * kStageBytes;
     mbar_expect_tx(&full[ps_stage], 2 * bytes);
-    bulk_g2s(dk, ld.K + off, bytes, &full[ps_stage], pol);
-    bulk_g2s(dk + kStageBytes, ld.V + off, bytes, &full[ps_stage], pol);
+    if (ld.Ksrc == nullptr) {
+      bulk_g2s(dk, ld.K + off, bytes, &full[ps_stage], pol);
+      bulk_g2s(dk + kStageBytes, ld.V + off, bytes, &full[ps_stage], pol);
+    } else {   // copy-on-read growth: old rows, then zero rows
+      const long long nold = max(0LL, min(rows, ld.rows_src - row0));
+      const uint32_t bo = (uint32_t)(nold * C::ROWB);
+      if (bo) {
+        const size_t so = (size_t)(pc.u * ld.cap_src + row0) * C::ROWB;
+        bulk_g2s(dk, ld.Ksrc + so, bo, &full[ps_stage], pol);
+        bulk_g2s(dk + kStageBytes, ld.Vsrc + so, bo, &full[ps_stage], pol);
+      }
+      if (bytes > bo) {
+        bulk_g2s_plain(dk + bo, g_zero_page, bytes - bo, &full[ps_stage]);
+        bulk_g2s_plain(dk + kStageBytes + bo, g_zero_page, bytes - bo, &full[ps_stage]);
+      }
+    }
     ++pi;
     advance(p, pc);
     if (++ps_stage == S) ps_stage = 0;
@@ -368,6 +420,15 @@ __global__ void __launch_bounds__(kThreads, CTAS) attn_step_kernel(const __grid_
         consumer_sync();
       }
     }
+    if (ld.Ksrc != nullptr && tid == 0) {
+      // copy-on-read growth: the staged tile (old rows, zero rows, patched
+      // appended row) is the new buffer's content for these rows
+      const size_t off = (size_t)(cc.u * ld.cap + row0) * C::ROWB;
+      const uint32_t bytes = (uint32_t)(rows_in_tile * C::ROWB);
+      bulk_s2g(const_cast<uint8_t*>(ld.K) + off, sk, bytes);
+      bulk_s2g(const_cast<uint8_t*>(ld.V) + off, sv, bytes);
+      bulk_commit();
+    }
 
     if (row0 < max_vis) {  // tiles with no visible row for any query are only streamed
       // K rows of all passes first (independent loads, then independent FMA chains)
@@ -474,6 +535,7 @@ __global__ void __launch_bounds__(kThreads, CTAS) attn_step_kernel(const __grid_
         }
       }
     }
+    if (tid == 0 && ld.Ksrc != nullptr) bulk_wait_read();   // before the stage is refilled
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[stage]);
     if (tid == 0 && pi < t_end) {
@@ -583,6 +645,7 @@ __global__ void __launch_bounds__(kThreads, CTAS) attn_step_kernel(const __grid_
       consumer_sync();  // the flag and merge buffers are reused by the next segment
     }
   }
+  if (tid == 0) bulk_wait_all();   // copy-on-read stores complete before the CTA exits
 }
 
 template <typename T, int D, int MAXM, int CPL, int CTAS, int MAXL>
@@ -636,6 +699,11 @@ cudaError_t launch_chunk(const AttnStepArgs& a, int l0, int nl, int num_sms, cud
     LayerDesc& d = prm.layer[i];
     d.K = (const uint8_t*)h.K;
     d.V = (const uint8_t*)h.V;
+    d.Ksrc = (const uint8_t*)h.Ksrc;
+    d.Vsrc = (const uint8_t*)h.Vsrc;
+    d.cap_src = h.cap_src;
+    d.rows_src = h.rows_src;
+    if (d.Ksrc && h.scan > 0 && h.scan < h.cap) return cudaErrorInvalidValue;
     d.Q = (const uint8_t*)h.Q;
     d.O = h.O;
     d.Knew = (const uint8_t*)h.Knew;

@@ -50,6 +50,13 @@ struct bmc_ctx {
   int attn_ctas = 0;
   int attn_path = 0;
   int skip_padding = 0;          // length-aware ablation, off by default
+  int copy_on_read = 1;          // BMC growth inside the fused decode step
+  // a growth whose copy the next attention launch performs (copy-on-read):
+  // the old buffers and the rows to carry over; never observable between API
+  // calls (bmc_decode_step launches the consuming kernel in the same call)
+  bool cor = false;
+  Buffer cor_k, cor_v;
+  long long cor_cap = 0, cor_rows = 0;
   bmc_stats_t st = {};
   int sticky = 0;
   // staging of host-pointer arguments: 0 appended rows, 1 drafts, 2 Q
@@ -153,6 +160,7 @@ static int cuda_fail(bmc_t h, cudaError_t e, const char* where) {
     if (_e != cudaSuccess) return cuda_fail((h), _e, where); \
   } while (0)
 
+static int cor_materialize(bmc_t h);
 static int enter(bmc_t h) {
   if (!h) return fail(BMC_ERR_ARG, "null handle");
   if (h->sticky) return fail(h->sticky, "handle is in a sticky CUDA error state");
@@ -161,6 +169,7 @@ static int enter(bmc_t h) {
     cudaError_t e = cudaSetDevice(h->device);
     if (e != cudaSuccess) return cuda_fail(h, e, "cudaSetDevice");
   }
+  if (h->cor) return cor_materialize(h);   // never left pending by a successful call
   return 0;
 }
 
@@ -263,9 +272,17 @@ static int device_inputs(bmc_t h, int slot, const void** ptrs, const size_t* byt
   return 0;
 }
 
+static int cor_materialize(bmc_t h);
+
 // Replace the cache buffers by [U][new_cap][D] buffers holding the first
-// copy_rows rows of every unit, zero elsewhere.
-static int reallocate(bmc_t h, long long new_cap, long long copy_rows) {
+// copy_rows rows of every unit, zero elsewhere.  defer: the
+// copy and zero fill are left to the next attention launch (copy-on-read);
+// the ledger is the same either way.
+static int reallocate(bmc_t h, long long new_cap, long long copy_rows, bool defer = false) {
+  if (h->cor) {
+    int rc = cor_materialize(h);
+    if (rc) return rc;
+  }
   const size_t bytes = (size_t)h->U * new_cap * h->row_bytes;
   Buffer nk, nv;
   int rc = bmc::arena_alloc(h->arena, 0, bytes, h->arena_kind, &h->kbuf, h->stream, &nk);
@@ -274,6 +291,21 @@ static int reallocate(bmc_t h, long long new_cap, long long copy_rows) {
   if (rc) {
     bmc::arena_release(h->arena, &nk, h->stream);
     return fail(rc, "arena_alloc(V, %zu bytes) failed", bytes);
+  }
+  if (h->cap > 0) h->st.copy_events += 1;
+  h->st.alloc_events += 1;
+  h->st.copied_bytes += 2LL * h->U * copy_rows * h->row_bytes;
+  h->st.init_written_bytes += 2LL * h->U * new_cap * h->row_bytes;
+  if (defer && h->cap > 0 && copy_rows > 0) {
+    h->cor = true;
+    h->cor_k = h->kbuf;
+    h->cor_v = h->vbuf;
+    h->cor_cap = h->cap;
+    h->cor_rows = copy_rows;
+    h->kbuf = nk;
+    h->vbuf = nv;
+    h->cap = new_cap;
+    return 0;
   }
   bmc::ReallocArgs a;
   a.src_k = h->kbuf.ptr;
@@ -286,10 +318,6 @@ static int reallocate(bmc_t h, long long new_cap, long long copy_rows) {
   a.copy_rows = copy_rows;
   a.row_bytes = h->row_bytes;
   CK(h, bmc::launch_realloc_copy_zero(a, h->stream), "realloc_copy_zero");
-  if (h->cap > 0) h->st.copy_events += 1;
-  h->st.alloc_events += 1;
-  h->st.copied_bytes += 2LL * h->U * copy_rows * h->row_bytes;
-  h->st.init_written_bytes += 2LL * h->U * new_cap * h->row_bytes;
   if (bmc::arena_release(h->arena, &h->kbuf, h->stream) ||
       bmc::arena_release(h->arena, &h->vbuf, h->stream)) {
     h->sticky = BMC_ERR_CUDA;
@@ -299,6 +327,37 @@ static int reallocate(bmc_t h, long long new_cap, long long copy_rows) {
   h->vbuf = nv;
   h->cap = new_cap;
   return 0;
+}
+
+// The old buffers of a copy-on-read growth are free once the consuming
+// attention launch is enqueued (stream-ordered release).
+static int cor_release(bmc_t h) {
+  if (!h->cor) return 0;
+  h->cor = false;
+  if (bmc::arena_release(h->arena, &h->cor_k, h->stream) ||
+      bmc::arena_release(h->arena, &h->cor_v, h->stream)) {
+    h->sticky = BMC_ERR_CUDA;
+    return fail(BMC_ERR_CUDA, "arena_release failed");
+  }
+  return 0;
+}
+
+// A deferred growth whose attention launch will not happen: do the copy and
+// zero fill with the realloc kernel after all.
+static int cor_materialize(bmc_t h) {
+  if (!h->cor) return 0;
+  bmc::ReallocArgs a;
+  a.src_k = h->cor_k.ptr;
+  a.src_v = h->cor_v.ptr;
+  a.dst_k = h->kbuf.ptr;
+  a.dst_v = h->vbuf.ptr;
+  a.U = h->U;
+  a.cap_old = h->cor_cap;
+  a.cap_new = h->cap;
+  a.copy_rows = h->cor_rows;
+  a.row_bytes = h->row_bytes;
+  CK(h, bmc::launch_realloc_copy_zero(a, h->stream), "realloc_copy_zero");
+  return cor_release(h);
 }
 
 static int write_rows(bmc_t h, const void* K, const void* V, int nsrc, int nwrite, int row_shift) {
@@ -342,6 +401,10 @@ static int ensure_workspace(bmc_t h, int M) {
 static void fill_layer(bmc_t h, const void* Q, float* O, bmc::AttnLayer* l) {
   l->K = h->kbuf.ptr;
   l->V = h->vbuf.ptr;
+  l->Ksrc = h->cor ? h->cor_k.ptr : nullptr;
+  l->Vsrc = h->cor ? h->cor_v.ptr : nullptr;
+  l->cap_src = h->cor ? h->cor_cap : 0;
+  l->rows_src = h->cor ? h->cor_rows : 0;
   l->Q = Q;
   l->O = O;
   l->Knew = h->knew;
@@ -448,7 +511,9 @@ int bmc_create(int B, int H_kv, int H_q, int D, int r, int N_max, bmc_t* out) {
 }
 
 // Append = growth if needed + record the row (written by the next SDPA).
-static int append_impl(bmc_t h, const void* K, const void* V) {
+// defer_growth: a BMC growth's copy is done by the attention launch that the
+// caller enqueues next (copy-on-read; only bmc_decode_step's CUDA-core path).
+static int append_impl(bmc_t h, const void* K, const void* V, bool defer_growth = false) {
   int rc = 0;
   if (h->n_app || h->n_draft) rc = flush_pending(h);
   if (rc) return rc;
@@ -456,7 +521,8 @@ static int append_impl(bmc_t h, const void* K, const void* V) {
   if (h->pol == BMC_POLICY_ITERATIVE) {
     rc = reallocate(h, mv + 1, mv);                      // Fig. AttnBlkListing concat
   } else if (h->pol == BMC_POLICY_BMC && mv == h->cap) {
-    rc = reallocate(h, std::min<long long>(h->cap + h->r, h->N_max), h->cap);
+    rc = reallocate(h, std::min<long long>(h->cap + h->r, h->N_max), h->cap,
+                    defer_growth);
   }
   if (rc) return rc;
   const size_t in_bytes = (size_t)h->U * h->row_bytes;
@@ -826,11 +892,13 @@ int bmc_decode_step(const bmc_t* hs, int L, const void* const* K, const void* co
   }
   std::vector<bmc::AttnLayer> layers(L);
   for (int l = 0; l < L; ++l) {
-    int rc = append_impl(hs[l], K[l], V[l]);
-    if (rc) return rc;
-    if (tck) {
-      rc = ensure_workspace(hs[l], G);
-      if (rc) return rc;
+    // copy-on-read growth (BMC policy, CUDA-core kernel, all cap rows streamed)
+    const bool defer = !tck && hs[l]->copy_on_read && !hs[l]->skip_padding;
+    int rc = append_impl(hs[l], K[l], V[l], defer);
+    if (!rc && tck) rc = ensure_workspace(hs[l], G);
+    if (rc) {
+      for (int x = 0; x <= l; ++x) cor_materialize(hs[x]);
+      return rc;
     }
     fill_layer(hs[l], Q[l], O[l], &layers[l]);
   }
@@ -859,9 +927,11 @@ int bmc_decode_step(const bmc_t* hs, int L, const void* const* K, const void* co
     CK(hs[0], bmc::launch_attn_step(a, hs[0]->num_sms, hs[0]->stream), "attn_step");
   }
   for (int l = 0; l < L; ++l) {
+    int rc = cor_release(hs[l]);
+    if (rc) return rc;
     hs[l]->n_app = hs[l]->n_draft = 0;
     account_sdpa(hs[l], 1);
-    int rc = inputs_consumed(hs[l]);
+    rc = inputs_consumed(hs[l]);
     if (rc) return rc;
   }
   return 0;
@@ -1120,8 +1190,13 @@ int bmc_commit_step(const bmc_t* hs, int L, const int* n_accepted_host) {
 int bmc_destroy(bmc_t h) {
   if (!h) return fail(BMC_ERR_ARG, "null handle");
   cudaSetDevice(h->device);
+  if (!h->sticky && h->cor) cor_materialize(h);
   if (!h->sticky && (h->n_app || h->n_draft)) flush_pending(h);
   cudaStreamSynchronize(h->stream);
+  if (h->cor) {
+    bmc::arena_release(h->arena, &h->cor_k, h->stream);
+    bmc::arena_release(h->arena, &h->cor_v, h->stream);
+  }
   pipe_destroy(h->pipe);
   h->pipe = nullptr;
   hio_destroy(h->hio);
@@ -1223,6 +1298,10 @@ int bmc_set_option(bmc_t h, int key, long long value) {
     case BMC_OPT_SKIP_PADDING:
       if (value < 0 || value > 1) return fail(BMC_ERR_ARG, "skip padding");
       h->skip_padding = (int)value;
+      return 0;
+    case BMC_OPT_COPY_ON_READ:
+      if (value < 0 || value > 1) return fail(BMC_ERR_ARG, "copy on read");
+      h->copy_on_read = (int)value;
       return 0;
     default:
       return fail(BMC_ERR_ARG, "unknown option %d", key);

@@ -62,6 +62,11 @@ cudaError_t launch_commit_path(const PathArgs& a, cudaStream_t s);
 // One layer of an attention launch.
 struct AttnLayer {
   const void* K; const void* V;           // cache [U][cap][D]
+  // copy-on-read growth (CUDA-core kernel only): old buffer [U][cap_src][D]
+  // whose first rows_src rows per unit the attention copies into K / V while
+  // streaming them (null: no growth pending)
+  const void* Ksrc = nullptr; const void* Vsrc = nullptr;
+  long long cap_src = 0, rows_src = 0;
   const void* Q;                          // [B][H_q][t][D]
   float* O;                               // [B][H_q][t][D]
   const void* Knew; const void* Vnew;     // pending appended row [B][H_kv][D] (n_app = 1)

@@ -210,6 +210,53 @@ def test_decode_step_matches_per_layer_calls(H_q, path_b):
         x.close()
 
 
+@pytest.mark.parametrize("dtype,D,r,B,N", [("bf16", 128, 24, 3, 170), ("bf16", 128, 64, 2, 200),
+                                           ("f32", 64, 5, 2, 60), ("bf16", 64, 1, 1, 40),
+                                           ("f32", 128, 37, 2, 120)])
+def test_copy_on_read_growth(dtype, D, r, B, N):
+    """a BMC growth inside bmc_decode_step is copied by the
+    attention kernel while it streams the old buffer (old rows + zero page ->
+    new buffer, appended row patched in).  Against the separate realloc
+    kernel (BMC_OPT_COPY_ON_READ = 0): outputs identical at every step
+    (same kernel, same partition), caches bit-identical right after every
+    growth (copied rows, zero rows, appended row), ledgers equal.  r not a
+    multiple of the 16 KiB tile's rows makes tiles straddle the old / new
+    boundary; r = 1 grows every step."""
+    H_kv, H_q, L = 2, 2, 3
+    dev = torch.device("cuda")
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    a = [bmc.KVCache(B, H_kv, H_q, D, r, N, dtype=dtype) for _ in range(L)]
+    b = [bmc.KVCache(B, H_kv, H_q, D, r, N, dtype=dtype) for _ in range(L)]
+    for x in b:
+        x.set_option(bmc.BMC_OPT_COPY_ON_READ, 0)
+    pa, pb = bmc.StepPlan(a), bmc.StepPlan(b)
+    g = torch.Generator(device=dev)
+    g.manual_seed(17)
+    oa = [torch.empty(B, H_q, 1, D, device=dev) for _ in range(L)]
+    ob = [torch.empty(B, H_q, 1, D, device=dev) for _ in range(L)]
+    l0 = bmc.bmc_launch_count()
+    for n in range(1, N + 1):
+        ks = [torch.randn(B, H_kv, D, generator=g, device=dev).to(tdt) for _ in range(L)]
+        vs = [torch.randn(B, H_kv, D, generator=g, device=dev).to(tdt) for _ in range(L)]
+        qs = [torch.randn(B, H_q, 1, D, generator=g, device=dev).to(tdt) for _ in range(L)]
+        bmc.bmc_decode_step(pa, pa.ptrs(ks), pa.ptrs(vs), pa.ptrs(qs), pa.ptrs(oa), n)
+        bmc.bmc_decode_step(pb, pb.ptrs(ks), pb.ptrs(vs), pb.ptrs(qs), pb.ptrs(ob), n)
+        torch.cuda.synchronize()
+        for l in range(L):
+            assert torch.equal(oa[l], ob[l]), (n, l)
+        if (n - 1) % r == 0 or n == N:        # growth steps (and the end)
+            for l in range(L):
+                ka, va = a[l].kv()
+                kb, vb = b[l].kv()
+                assert torch.equal(_bits(ka), _bits(kb)) and torch.equal(_bits(va), _bits(vb)), n
+    for l in range(L):
+        assert a[l].stats() == b[l].stats()
+    grows = a[0].stats()["copy_events"]
+    for x in a + b:
+        x.close()
+    assert grows == math.ceil(N / r) - 1
+
+
 def test_decode_step_host_io_pipeline():
     """bmc_decode_step with pinned host K/V/Q/O (the pipelined end-to-end path:
     copy stream, double-buffered staging) equals the device-pointer step."""
