@@ -606,6 +606,8 @@ bool attn_tc_supported(int D, int dtype, int M) {
 }
 
 cudaError_t launch_attn_tc(const AttnStepArgs& a, int num_sms, cudaStream_t s) {
+  for (int l = 0; l < a.L; ++l)
+    if (a.layers[l].Ksrc) return cudaErrorInvalidValue;   // no copy-on-read in this kernel
   static int attr_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);

@@ -40,6 +40,12 @@
 // bits) + lo (rounded remainder): P = hi + lo to ~2^-16 relative, so the
 // tensor-core P.V keeps the bf16 path inside its 2e-3 budget.
 // Split units use the partial-record + last-CTA combine of combine.cuh.
+// Copy-on-read growth (as in attn_decode.cu): when the launch
+// follows a BMC growth, the producers load 3D boxes {dims, keys, unit} of the
+// OLD buffer (rows >= cap_old are out of bounds: TMA fills zeros), the MMA
+// issuers patch the pending appended / drafted rows into the staged tile and
+// TMA-store it into the NEW buffer before their MMAs, so the growth needs no
+// realloc kernel and the new buffer is written once, never read back.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -123,7 +129,9 @@ __device__ int g_tck_trace_cta;
 // One layer of a launch (a decode step fuses up to 32 layers of one shape)
 struct LayerP {
   CUtensorMap tmK;          // [U*cap rows][128] bf16, box 64 x 128, SWIZZLE_128B
-  CUtensorMap tmV;
+  CUtensorMap tmV;          //   (copy-on-read: [U][cap_old][128] of the old buffer, 3D boxes)
+  CUtensorMap tmKd;         // copy-on-read only: [U][cap][128] of the new buffer
+  CUtensorMap tmVd;
   const __nv_bfloat16* Q;   // [B][H_q][t][D]
   float* O;                 // [B][H_q][t][D]
   const uint8_t* Knew;      // pending appended row [B][H_kv][D] (n_app == 1)
@@ -145,9 +153,42 @@ struct Params {
   int tpu, U, H_kv, H_q, G, t, M, ctas;
   float qscale;
   int tree;
+  int cor;                  // copy-on-read growth launch
   uint32_t anc[32];
   int valid[BMC_MAX_B];
 };
+
+// Copy-on-read: write the pending appended / drafted rows of unit uu that fall
+// into tile rows [row0, row0 + KT) into the staged K or V tile (SWIZZLE_128B
+// boxes of 64 dims x 128 keys); one thread, rare (about one tile per unit).
+template <int MAXL>
+__device__ __forceinline__ void patch_pending(const Params<MAXL>& p, const LayerP& ly, long long uu,
+                                              int row0, uint32_t tile, bool isV) {
+  const int vb = p.valid[(int)(uu / p.H_kv)];
+  const int n = p.n_app + p.n_draft;
+  for (int ri = 0; ri < n; ++ri) {
+    int row;
+    const uint8_t* src;
+    if (p.n_app && ri == 0) {
+      row = vb - 1;
+      src = (isV ? ly.Vnew : ly.Knew) + (size_t)uu * (D * 2);
+    } else {
+      const int di = ri - p.n_app;
+      row = vb + di;
+      src = (isV ? ly.Vd : ly.Kd) + ((size_t)uu * p.kd_stride + di) * (D * 2);
+    }
+    const int r = row - row0;
+    if (r < 0 || r >= KT) continue;
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+      const uint4 v = *reinterpret_cast<const uint4*>(src + c * 16);
+      const uint32_t off = (uint32_t)(c >> 3) * kBox + sw128((uint32_t)r, (uint32_t)(c & 7));
+      asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(tile + off), "r"(v.x), "r"(v.y),
+                   "r"(v.z), "r"(v.w)
+                   : "memory");
+    }
+  }
+}
 
 __device__ __forceinline__ void softmax_sync() {   // the 8 softmax warps
   asm volatile("bar.sync 1, 256;" ::: "memory");
@@ -327,12 +368,18 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
         TRACE(isK ? 0 : 1, (int)(i - t_begin));
         const LayerP& ly = p.lay[MAXL == 1 ? 0 : (int)(gu / p.U)];
         const CUtensorMap* tm = isK ? &ly.tmK : &ly.tmV;
-        const int row = (int)((gu % p.U) * p.cap + (long long)j * KT);
         const uint32_t dst = ring + s * kTileBytes;
         const uint32_t fb = isK ? FULLK(s) : FULLV(s);
         mbar_expect_tx(fb, kTileBytes);
-        tma_load_2d(dst, tm, 0, row, fb, pol);
-        tma_load_2d(dst + kBox, tm, 64, row, fb, pol);
+        if (p.cor) {   // old buffer, zeros past its rows
+          const int uu = (int)(gu % p.U);
+          tma_load_3d(dst, tm, 0, j * KT, uu, fb, pol);
+          tma_load_3d(dst + kBox, tm, 64, j * KT, uu, fb, pol);
+        } else {
+          const int row = (int)((gu % p.U) * p.cap + (long long)j * KT);
+          tma_load_2d(dst, tm, 0, row, fb, pol);
+          tma_load_2d(dst + kBox, tm, 64, row, fb, pol);
+        }
         if (++j == p.tpu) { j = 0; ++gu; }
         if (++s == NS) { s = 0; ph ^= 1; }
       }
@@ -358,10 +405,21 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
           const int b = tc % NB;
           mbar_wait(FULLK(ks), kph);
           TRACE(2, tc);
+          const uint32_t kt = sbase + C::OFF_K + ks * kTileBytes;
+          if (p.cor) {   // copy-on-read: patched tile -> new buffer (read before the refill)
+            const long long gk = i + k;
+            const LayerP& ly = p.lay[MAXL == 1 ? 0 : (int)((gk / p.tpu) / p.U)];
+            const long long uu = (gk / p.tpu) % p.U;
+            const int row0 = (int)(gk % p.tpu) * KT;
+            patch_pending(p, ly, uu, row0, kt, false);
+            fence_proxy_smem();
+            tma_store_3d(&ly.tmKd, kt, 0, row0, (int)uu);
+            tma_store_3d(&ly.tmKd, kt + kBox, 64, row0, (int)uu);
+            bulk_commit_wait_read();
+          }
           mbar_wait(SEMPTY(b), ((tc / NB) & 1) ^ 1);
           TRACE(3, tc);
           fence_after();
-          const uint32_t kt = sbase + C::OFF_K + ks * kTileBytes;
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk) {
             const uint32_t koff = (kk >> 2) * kBox + (kk & 3) * 32;
@@ -379,6 +437,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
         ++item;
         i = iend;
       }
+      if (p.cor) bulk_wait_all();
     }
   } else if (warp == 11) {
     // ------------------------------------------------------ O^T += V^T P^T issuer
@@ -399,8 +458,19 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
           TRACE(5, tc);
           mbar_wait(FULLV(vs), vph);
           TRACE(6, tc);
-          fence_after();
           const uint32_t vt = sbase + C::OFF_V + vs * kTileBytes;
+          if (p.cor) {
+            const long long gk = i + k;
+            const LayerP& ly = p.lay[MAXL == 1 ? 0 : (int)((gk / p.tpu) / p.U)];
+            const long long uu = (gk / p.tpu) % p.U;
+            const int row0 = (int)(gk % p.tpu) * KT;
+            patch_pending(p, ly, uu, row0, vt, true);
+            fence_proxy_smem();
+            tma_store_3d(&ly.tmVd, vt, 0, row0, (int)uu);
+            tma_store_3d(&ly.tmVd, vt + kBox, 64, row0, (int)uu);
+            bulk_commit_wait_read();
+          }
+          fence_after();
           const uint32_t pb = sbase + C::OFF_P + b * C::kPBytes;
 #pragma unroll
           for (int kk = 0; kk < KT / 16; ++kk) {
@@ -417,6 +487,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
         tcount += n;
         i = iend;
       }
+      if (p.cor) bulk_wait_all();
     }
   } else {
     // ------------------------------------------------ softmax + epilogue
@@ -765,25 +836,31 @@ static cudaError_t launch_n(const tck::Params<MAXL>& p, int ctas, cudaStream_t s
 
 // Tensor maps are pure functions of (base, rows): cache them so a fused
 // 32-layer step does not re-encode 64 maps on the host every token.
-static cudaError_t cached_map(CUtensorMap* m, const void* base, long long rows) {
+// units > 0: the 3D [units][rows][128] map of a copy-on-read launch.
+static cudaError_t cached_map(CUtensorMap* m, const void* base, long long rows,
+                              long long units = 0) {
   struct Key {
     const void* base;
-    long long rows;
-    bool operator==(const Key& o) const { return base == o.base && rows == o.rows; }
+    long long rows, units;
+    bool operator==(const Key& o) const {
+      return base == o.base && rows == o.rows && units == o.units;
+    }
   };
   struct Hash {
     size_t operator()(const Key& k) const {
-      return std::hash<const void*>()(k.base) ^ (std::hash<long long>()(k.rows) * 31);
+      return std::hash<const void*>()(k.base) ^ (std::hash<long long>()(k.rows) * 31) ^
+             (std::hash<long long>()(k.units) * 131);
     }
   };
   static thread_local std::unordered_map<Key, CUtensorMap, Hash> cache;
-  const Key k{base, rows};
+  const Key k{base, rows, units};
   auto it = cache.find(k);
   if (it != cache.end()) {
     *m = it->second;
     return cudaSuccess;
   }
-  cudaError_t e = make_map(m, base, rows, tck::KT);
+  cudaError_t e = units > 0 ? make_map3(m, base, units, rows, tck::KT)
+                            : make_map(m, base, rows, tck::KT);
   if (e != cudaSuccess) return e;
   if (cache.size() > 4096) cache.clear();
   cache.emplace(k, *m);
@@ -796,14 +873,26 @@ static cudaError_t launch_layers(const AttnStepArgs& a, int l0, int nl, int num_
   tck::Params<MAXL> p;
   const AttnLayer& h0 = a.layers[l0];
   const long long U = (long long)a.B * a.H_kv;
+  p.cor = h0.Ksrc != nullptr;
   for (int l = 0; l < nl; ++l) {
     const AttnLayer& h = a.layers[l0 + l];
     if (h.cap != h0.cap || h.scan != h0.scan || h.n_app != h0.n_app ||
-        h.n_draft != h0.n_draft || h.kd_stride != h0.kd_stride)
+        h.n_draft != h0.n_draft || h.kd_stride != h0.kd_stride ||
+        (h.Ksrc != nullptr) != (p.cor != 0) || h.cap_src != h0.cap_src)
       return cudaErrorInvalidValue;   // the caller launches such layers one by one
+    if (p.cor && ((h.scan > 0 && h.scan < h.cap) || h.rows_src != h.cap_src))
+      return cudaErrorInvalidValue;   // copy-on-read streams every row of the old buffer
     tck::LayerP& ly = p.lay[l];
-    cudaError_t e = cached_map(&ly.tmK, h.K, U * h.cap);
-    if (e == cudaSuccess) e = cached_map(&ly.tmV, h.V, U * h.cap);
+    cudaError_t e;
+    if (p.cor) {
+      e = cached_map(&ly.tmK, h.Ksrc, h.cap_src, U);
+      if (e == cudaSuccess) e = cached_map(&ly.tmV, h.Vsrc, h.cap_src, U);
+      if (e == cudaSuccess) e = cached_map(&ly.tmKd, h.K, h.cap, U);
+      if (e == cudaSuccess) e = cached_map(&ly.tmVd, h.V, h.cap, U);
+    } else {
+      e = cached_map(&ly.tmK, h.K, U * h.cap);
+      if (e == cudaSuccess) e = cached_map(&ly.tmV, h.V, U * h.cap);
+    }
     if (e != cudaSuccess) return e;
     ly.Q = (const __nv_bfloat16*)h.Q;
     ly.O = h.O;

@@ -584,9 +584,18 @@ int bmc_append_n(bmc_t h, const void* K, const void* V, int n) {
   return 0;
 }
 
+static int spec_write_impl(bmc_t h, const void* K_draft, const void* V_draft, int k);
+
 int bmc_spec_write(bmc_t h, const void* K_draft, const void* V_draft, int k) {
   int rc = enter(h);
   if (rc) return rc;
+  return spec_write_impl(h, K_draft, V_draft, k);
+}
+
+// spec_write without enter(): bmc_spec_step calls it between the (possibly
+// deferred, copy-on-read) growth and the attention launch that performs it
+static int spec_write_impl(bmc_t h, const void* K_draft, const void* V_draft, int k) {
+  int rc = 0;
   if (k < 0) return fail(BMC_ERR_ARG, "k=%d < 0", k);
   if (k > 0 && (!K_draft || !V_draft)) return fail(BMC_ERR_ARG, "draft pointers are null");
   if (h->staged > 0) return fail(BMC_ERR_STATE, "drafts already staged");
@@ -771,17 +780,11 @@ int bmc_spec_step(const bmc_t* hs, int L, const void* const* K, const void* cons
       return fail(BMC_ERR_ARG, "layer %d: bmc_spec_step takes device Q and O", l);
   }
   const int t = 1 + k_adm;
-  for (int l = 0; l < L; ++l) {
-    int rc = append_impl(hs[l], K[l], V[l]);
-    if (rc) return rc;
-    if (k > 0) {
-      rc = bmc_spec_write(hs[l], Kd[l], Vd[l], k);
-      if (rc < 0) return rc;
-    }
-  }
   // one launch for the layers when they share shape, stream, lengths and
   // capacity and the kernel takes several layers (CUDA cores, or the
-  // keys-on-lanes tcgen05 kernel up to M = 80); else one launch per layer
+  // keys-on-lanes tcgen05 kernel up to M = 80); else one launch per layer.
+  // Decided on the state before the appends (layers that agree now agree
+  // after them: they see the same step).
   const bmc_t h0 = hs[0];
   bool fused = true;
   for (int l = 1; l < L; ++l) {
@@ -789,7 +792,8 @@ int bmc_spec_step(const bmc_t* hs, int L, const void* const* K, const void* cons
     if (a->B != h0->B || a->H_kv != h0->H_kv || a->H_q != h0->H_q || a->D != h0->D ||
         a->dt != h0->dt || a->stream != h0->stream || a->device != h0->device ||
         a->valid != h0->valid || a->cap != h0->cap || a->attn_path != h0->attn_path ||
-        a->skip_padding != h0->skip_padding)
+        a->skip_padding != h0->skip_padding || a->pol != h0->pol || a->r != h0->r ||
+        a->N_max != h0->N_max || a->copy_on_read != h0->copy_on_read)
       fused = false;
   }
   const int M = (h0->H_q / h0->H_kv) * t;
@@ -797,6 +801,19 @@ int bmc_spec_step(const bmc_t* hs, int L, const void* const* K, const void* cons
                   (h0->attn_path == 0 && M > kTcMinM && bmc::attn_tc_supported(h0->D, h0->dt, M));
   const bool tck = tc && h0->attn_path != 3 && bmc::attn_tck_supported(h0->D, h0->dt, M);
   if (tc && !tck) fused = false;
+  for (int l = 0; l < L; ++l) {
+    // copy-on-read growth when the fused launch below performs it
+    const bool defer = fused && hs[l]->copy_on_read && !hs[l]->skip_padding;
+    int rc = append_impl(hs[l], K[l], V[l], defer);
+    if (!rc && k > 0) {
+      rc = spec_write_impl(hs[l], Kd[l], Vd[l], k);
+      if (rc > 0) rc = 0;
+    }
+    if (rc) {
+      for (int x = 0; x <= l; ++x) cor_materialize(hs[x]);
+      return rc;
+    }
+  }
   if (!fused) {
     for (int l = 0; l < L; ++l) {
       int rc = launch_sdpa_layer(hs[l], Q[l], O[l], t);
@@ -808,7 +825,10 @@ int bmc_spec_step(const bmc_t* hs, int L, const void* const* K, const void* cons
   for (int l = 0; l < L; ++l) {
     if (tck) {
       int rc = ensure_workspace(hs[l], M);
-      if (rc) return rc;
+      if (rc) {
+        for (int x = 0; x < L; ++x) cor_materialize(hs[x]);
+        return rc;
+      }
     }
     fill_layer(hs[l], Q[l], O[l], &layers[l]);
   }
@@ -823,9 +843,11 @@ int bmc_spec_step(const bmc_t* hs, int L, const void* const* K, const void* cons
     CK(h0, bmc::launch_attn_step(a, h0->num_sms, h0->stream), "attn_step");
   }
   for (int l = 0; l < L; ++l) {
+    int rc = cor_release(hs[l]);
+    if (rc) return rc;
     hs[l]->n_app = hs[l]->n_draft = 0;
     account_sdpa(hs[l], t);
-    int rc = inputs_consumed(hs[l]);
+    rc = inputs_consumed(hs[l]);
     if (rc) return rc;
   }
   return k_adm;
@@ -892,8 +914,9 @@ int bmc_decode_step(const bmc_t* hs, int L, const void* const* K, const void* co
   }
   std::vector<bmc::AttnLayer> layers(L);
   for (int l = 0; l < L; ++l) {
-    // copy-on-read growth (BMC policy, CUDA-core kernel, all cap rows streamed)
-    const bool defer = !tck && hs[l]->copy_on_read && !hs[l]->skip_padding;
+    // copy-on-read growth (BMC policy; CUDA-core or keys-on-lanes kernel; all
+    // cap rows streamed)
+    const bool defer = hs[l]->copy_on_read && !hs[l]->skip_padding;
     int rc = append_impl(hs[l], K[l], V[l], defer);
     if (!rc && tck) rc = ensure_workspace(hs[l], G);
     if (rc) {
@@ -911,7 +934,10 @@ int bmc_decode_step(const bmc_t* hs, int L, const void* const* K, const void* co
     // usual case: one r, one step sequence); else one launch per layer
     bool same = true;
     for (int l = 1; l < L; ++l)
-      if (layers[l].cap != layers[0].cap || layers[l].scan != layers[0].scan) same = false;
+      if (layers[l].cap != layers[0].cap || layers[l].scan != layers[0].scan ||
+          (layers[l].Ksrc != nullptr) != (layers[0].Ksrc != nullptr) ||
+          layers[l].cap_src != layers[0].cap_src)
+        same = false;
     a.ctas = std::min(h0->attn_ctas, h0->num_sms);
     if (same) {
       CK(h0, bmc::launch_attn_tck(a, h0->num_sms, h0->stream), "attn_tck");

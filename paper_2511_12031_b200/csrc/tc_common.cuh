@@ -41,6 +41,29 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* tm,
       "l"(tm), "r"(c0), "r"(c1), "r"(bar), "l"(pol)
       : "memory");
 }
+// 3D boxes {dims, rows, unit} over a [U][cap][128] cache: rows >= cap of a
+// unit are out of bounds (zero-filled on load, dropped on store)
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* tm, int c0, int c1,
+                                            int c2, uint32_t bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(dst),
+      "l"(tm), "r"(c0), "r"(c1), "r"(c2), "r"(bar), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* tm, uint32_t src, int c0, int c1,
+                                             int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                   tm),
+               "r"(c0), "r"(c1), "r"(c2), "r"(src)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit_wait_read() {   // my bulk stores have read smem
+  asm volatile("cp.async.bulk.commit_group;\n\tcp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
 __device__ __forceinline__ uint64_t evict_first_policy() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -233,6 +256,20 @@ inline PFN_encodeTiled encode_fn() {
 }
 
 // bf16 [rows][128] tensor, box 64 columns x box_rows rows, SWIZZLE_128B
+// [U][cap][128] bf16 as a 3D tensor, boxes of 64 dims x box_rows rows x 1 unit
+inline cudaError_t make_map3(CUtensorMap* m, const void* base, long long U, long long cap,
+                             int box_rows) {
+  PFN_encodeTiled fn = encode_fn();
+  if (!fn) return cudaErrorNotSupported;
+  const cuuint64_t dims[3] = {(cuuint64_t)128, (cuuint64_t)cap, (cuuint64_t)U};
+  const cuuint64_t strides[2] = {(cuuint64_t)128 * 2, (cuuint64_t)cap * 128 * 2};
+  const cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
 inline cudaError_t make_map(CUtensorMap* m, const void* base, long long rows, int box_rows) {
   PFN_encodeTiled fn = encode_fn();
   if (!fn) return cudaErrorNotSupported;

@@ -210,19 +210,25 @@ def test_decode_step_matches_per_layer_calls(H_q, path_b):
         x.close()
 
 
-@pytest.mark.parametrize("dtype,D,r,B,N", [("bf16", 128, 24, 3, 170), ("bf16", 128, 64, 2, 200),
-                                           ("f32", 64, 5, 2, 60), ("bf16", 64, 1, 1, 40),
-                                           ("f32", 128, 37, 2, 120)])
-def test_copy_on_read_growth(dtype, D, r, B, N):
+@pytest.mark.parametrize("dtype,D,r,B,N,H_q", [("bf16", 128, 24, 3, 170, 2),
+                                               ("bf16", 128, 64, 2, 200, 2),
+                                               ("f32", 64, 5, 2, 60, 2), ("bf16", 64, 1, 1, 40, 2),
+                                               ("f32", 128, 37, 2, 120, 2),
+                                               ("bf16", 128, 24, 3, 300, 8),
+                                               ("bf16", 128, 128, 2, 300, 16),
+                                               ("bf16", 128, 1, 2, 40, 16)])
+def test_copy_on_read_growth(dtype, D, r, B, N, H_q):
     """a BMC growth inside bmc_decode_step is copied by the
     attention kernel while it streams the old buffer (old rows + zero page ->
     new buffer, appended row patched in).  Against the separate realloc
     kernel (BMC_OPT_COPY_ON_READ = 0): outputs identical at every step
     (same kernel, same partition), caches bit-identical right after every
     growth (copied rows, zero rows, appended row), ledgers equal.  r not a
-    multiple of the 16 KiB tile's rows makes tiles straddle the old / new
-    boundary; r = 1 grows every step."""
-    H_kv, H_q, L = 2, 2, 3
+    multiple of the tile's rows makes tiles straddle the old / new boundary;
+    r = 1 grows every step.  H_q = 2: CUDA-core kernel (bulk copies, zero
+    page); H_q = 8, 16 (G = 4, 8): keys-on-lanes tcgen05 kernel (3D tensor
+    maps, out-of-bounds zero fill, patched tile, tensor-map store)."""
+    H_kv, L = 2, 3
     dev = torch.device("cuda")
     tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
     a = [bmc.KVCache(B, H_kv, H_q, D, r, N, dtype=dtype) for _ in range(L)]
