@@ -111,8 +111,16 @@ int bmc_admissible(bmc_t h, int k);
    bmc_spec_write); Q[l] DEVICE [B][H_q][t][D] and O[l] DEVICE
    [B][H_q][t][D] fp32 with t = 1 + bmc_admissible(hs[l], k) (every layer
    admits the same number).  Returns k_adm >= 0, or an error before anything
-   is enqueued (ARG, STATE, CAPACITY).  Commit afterwards per layer with
-   bmc_commit / bmc_commit_rows. */
+   is enqueued (ARG, STATE, CAPACITY).  Commit afterwards with bmc_commit_step
+   (or per layer with bmc_commit / bmc_commit_rows).
+   All-host form (the end-to-end call): when every K, V, Q, O (and Kd, Vd for
+   k > 0) is a HOST pointer (pinned for asynchrony), the arguments are staged
+   on the first layer's copy stream into double-buffered device slots, the
+   step runs on the compute stream and O is copied back on a download stream;
+   O is readable after bmc_sync(hs[0]), inputs reusable after the copy stream
+   passed them (as bmc_decode_step's host form).  Mixed host / device
+   arguments: K, V, Kd, Vd may be host (staged per call), Q and O must then be
+   device pointers. */
 int bmc_spec_step(const bmc_t* hs, int L, const void* const* K, const void* const* V,
                   const void* const* Kd, const void* const* Vd, int k,
                   const void* const* Q, float* const* O);
@@ -244,12 +252,17 @@ int bmc_sync(bmc_t h);
                               buffer (old rows read once, new
                               buffer written once, no separate realloc
                               kernel); 0 = separate realloc_copy_zero launch.
-                              Cache contents and ledger are identical.  */
+                              Cache contents and ledger are identical.
+     6 BMC_OPT_TCK_GROUPS     softmax column groups of the keys-on-lanes
+                              tcgen05 kernel: 0 auto (4 for G*t > 48, else
+                              2), 2 (384 threads), 4 (640 threads).  Tuning /
+                              A/B only; results agree within the tolerance. */
 #define BMC_OPT_ATTN_CTAS 1
 #define BMC_OPT_ATTN_PATH 2
 #define BMC_OPT_ARENA 3
 #define BMC_OPT_SKIP_PADDING 4
 #define BMC_OPT_COPY_ON_READ 5
+#define BMC_OPT_TCK_GROUPS 6
 int bmc_set_option(bmc_t h, int key, long long value);
 
 /* Kernels launched by this library in this process so far (all handles). */

@@ -252,7 +252,10 @@ int arena_alloc(Arena* a, int tensor, size_t bytes, int kind, const Buffer* keep
   if (!mp) return BMC_ERR_CUDA;
   void* p = nullptr;
   cudaError_t e = cudaMallocFromPoolAsync(&p, bytes, mp, s);
-  if (e == cudaErrorMemoryAllocation) return BMC_ERR_OOM;
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();   // not sticky: clear it so later launch checks do not report it
+    return BMC_ERR_OOM;
+  }
   if (e != cudaSuccess) return BMC_ERR_CUDA;
   out->ptr = p;
   out->bytes = bytes;

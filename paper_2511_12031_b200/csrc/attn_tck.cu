@@ -66,16 +66,23 @@ using namespace tcc;
 constexpr int D = 128;            // head dim (bf16)
 constexpr int KT = 128;           // keys per tile = MMA M of S^T
 constexpr int NB = 2;             // S^T / P^T buffers (tiles in flight)
-constexpr int kThreads = 384;
 constexpr uint32_t kTileBytes = KT * D * 2;   // 32 KiB per tensor per tile
 constexpr uint32_t kBox = 64 * 2 * KT;        // one 64-dim box of a tile: 16 KiB
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kRescale = 8.0f;
 
-template <int N>
+// NG column groups of softmax warps (4 warps each, one per TMEM lane
+// quadrant): 2 (384 threads) or 4 (640 threads: twice the warps per SMSP to
+// hide the TMEM / shared-memory / barrier latencies of large N)
+template <int N, int NG>
 struct Cfg {
   static_assert(N % 16 == 0 && N >= 16 && N <= 80, "query columns");
-  static constexpr int NH = N / 2;                          // columns per softmax half
+  static_assert(NG == 2 || NG == 4, "column groups");
+  static constexpr int NH = N / NG;                         // columns per softmax group
+  static constexpr int kSoftmax = NG * 128;                 // softmax threads
+  static constexpr int kThreads = 128 + kSoftmax;
+  static constexpr int kWarpV = 2 + 4 * NG;                 // V producer
+  static constexpr int kWarpPV = 3 + 4 * NG;                // O^T issuer
   static constexpr int NBP = N < 64 ? 2 : 1;                // P^T buffers
   static constexpr int KS = N <= 16 ? 3 : 2;                // K ring stages
   static constexpr int VS = N <= 32 ? 3 : 2;                // V ring stages
@@ -89,17 +96,18 @@ struct Cfg {
   static constexpr uint32_t kPBlock = KT * 32;                 // LBO: one 16-query block
   static constexpr uint32_t kPBytes = 2 * N / 16 * kPBlock;
   static constexpr uint32_t OFF_BAR = OFF_P + NBP * kPBytes;
-  static constexpr uint32_t OFF_RED = OFF_BAR + 512;           // [2 halves][4 quadrants][NH] f32
-  static constexpr uint32_t OFF_SUM = OFF_RED + 2 * 4 * NH * 4;  // [2][4][NH] f32
-  // running maxima: [2 halves][2 versions][m, m-or-0, m+8][NH] f32
-  static constexpr uint32_t OFF_M = OFF_SUM + 2 * 4 * NH * 4;
-  static constexpr uint32_t OFF_A = OFF_M + 2 * 2 * 3 * NH * 4;  // [2][NH] rescale factors
-  static constexpr uint32_t OFF_LIM = OFF_A + 2 * NH * 4;        // [2][NH] int visible-key limit
-  static constexpr uint32_t OFF_QM = OFF_LIM + 2 * NH * 4;       // [2][NH] ancestor masks
-  static constexpr uint32_t kSmem = OFF_QM + 2 * NH * 4;
+  static constexpr uint32_t OFF_RED = OFF_BAR + 512;            // [NG][4 quadrants][NH] f32
+  static constexpr uint32_t OFF_SUM = OFF_RED + NG * 4 * NH * 4;  // [NG][4][NH] f32
+  // running maxima: [NG][2 versions][m, m-or-0, m+8][NH] f32
+  static constexpr uint32_t OFF_M = OFF_SUM + NG * 4 * NH * 4;
+  static constexpr uint32_t OFF_A = OFF_M + NG * 2 * 3 * NH * 4;  // [NG][NH] rescale factors
+  static constexpr uint32_t OFF_LIM = OFF_A + NG * NH * 4;        // [NG][NH] int visible-key limit
+  static constexpr uint32_t OFF_QM = OFF_LIM + NG * NH * 4;       // [NG][NH] ancestor masks
+  static constexpr uint32_t kSmem = OFF_QM + NG * NH * 4;
   static_assert(kSmem <= 232448, "shared memory");
   static_assert(kQAtom % 1024 == 0 && kPBytes % 1024 == 0, "swizzle atoms");
-  static_assert(NH % 8 == 0, "16-byte P stores");
+  static_assert(NH % 4 == 0, "8- or 16-byte P stores");
+  static constexpr int CS = NH % 8 == 0 ? 8 : 4;               // column step of TMEM / P chunks
   static_assert(NBP * kPBytes >= (4 + 2) * N * 4, "combine scratch in the P area");
   // TMEM columns: S^T[b] at b*N, O^T (hi N cols, lo N cols) at NB*N
   static constexpr uint32_t TM_O = NB * N;
@@ -190,10 +198,11 @@ __device__ __forceinline__ void patch_pending(const Params<MAXL>& p, const Layer
   }
 }
 
-__device__ __forceinline__ void softmax_sync() {   // the 8 softmax warps
-  asm volatile("bar.sync 1, 256;" ::: "memory");
+template <int NT>
+__device__ __forceinline__ void softmax_sync() {   // the softmax warps
+  asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
 }
-__device__ __forceinline__ void half_sync(int h) {  // the 4 warps of one query half
+__device__ __forceinline__ void half_sync(int h) {  // the 4 warps of one column group
   asm volatile("bar.sync %0, 128;" ::"r"(2 + h) : "memory");
 }
 // OR of `pred` over the 4 warps of query half h (a barrier with reduction)
@@ -218,11 +227,11 @@ __device__ __forceinline__ void sts_v4(uint32_t addr, uint32_t a, uint32_t b, ui
 __device__ __forceinline__ void fence_proxy_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
-// NC consecutive fp32 TMEM columns of this warp's lane quadrant (NC % 8 == 0)
+// NC consecutive fp32 TMEM columns of this warp's lane quadrant (NC % 4 == 0)
 template <int NC>
 __device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, float* v) {
 #pragma unroll
-  for (int c = 0; c < NC; c += 8) {
+  for (int c = 0; c + 8 <= NC; c += 8) {
     uint32_t* r = reinterpret_cast<uint32_t*>(v + c);
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
@@ -230,19 +239,34 @@ __device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, float* v) {
           "=r"(r[7])
         : "r"(taddr + c));
   }
+  if constexpr (NC % 8 == 4) {
+    uint32_t* r = reinterpret_cast<uint32_t*>(v + NC - 4);
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(taddr + NC - 4));
+  }
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 template <int NC>
 __device__ __forceinline__ void tmem_st_cols(uint32_t taddr, const float* v) {
 #pragma unroll
-  for (int c = 0; c < NC; c += 8) {
+  for (int c = 0; c + 8 <= NC; c += 8) {
     const uint32_t* r = reinterpret_cast<const uint32_t*>(v + c);
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr + c),
         "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
         : "memory");
   }
+  if constexpr (NC % 8 == 4) {
+    const uint32_t* r = reinterpret_cast<const uint32_t*>(v + NC - 4);
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr + NC - 4),
+                 "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3])
+                 : "memory");
+  }
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void sts_v2(uint32_t addr, uint32_t a, uint32_t b) {
+  asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(addr), "r"(a), "r"(b) : "memory");
 }
 __device__ __forceinline__ float warp_max(float x) {   // one CREDUX on sm_100a
   float y;
@@ -255,9 +279,11 @@ __device__ __forceinline__ float warp_sum(float x) {
   return x;
 }
 
-template <int N, int MAXL>
-__global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_constant__ Params<MAXL> p) {
-  using C = Cfg<N>;
+template <int N, int MAXL, int NG>
+__global__ void __launch_bounds__(Cfg<N, NG>::kThreads, 1)
+    attn_tck_kernel(const __grid_constant__ Params<MAXL> p) {
+  using C = Cfg<N, NG>;
+  constexpr int kThreads = C::kThreads;
   constexpr int NH = C::NH;
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t sbase = su32(smem);
@@ -298,14 +324,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
     }
     for (int b = 0; b < NB; ++b) {
       mbar_init(SFULL(b), 1);
-      mbar_init(SEMPTY(b), 256);
+      mbar_init(SEMPTY(b), C::kSoftmax);
     }
     for (int b = 0; b < C::NBP; ++b) {
-      mbar_init(PFULL(b), 256);
+      mbar_init(PFULL(b), C::kSoftmax);
       mbar_init(PEMPTY(b), 1);
     }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(QFULL(b), 256);
+      mbar_init(QFULL(b), C::kSoftmax);
       mbar_init(QDONE(b), 1);
     }
     mbar_init(ODONE, 1);
@@ -352,7 +378,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
   fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0 || warp == 10) {
+  if (warp == 0 || warp == C::kWarpV) {
     // ------------------------------------------------------ TMA producers
     if (lane == 0) {
       const bool isK = warp == 0;
@@ -439,7 +465,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
       }
       if (p.cor) bulk_wait_all();
     }
-  } else if (warp == 11) {
+  } else if (warp == C::kWarpPV) {
     // ------------------------------------------------------ O^T += V^T P^T issuer
     if (lane == 0) {
       constexpr uint32_t IPV = idesc_bf16(D, 2 * N, 1, 1);   // A = V tile, B = P^T: MN-major
@@ -491,7 +517,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
     }
   } else {
     // ------------------------------------------------ softmax + epilogue
-    const int h = (warp - 2) >> 2;        // query half: columns h*NH .. +NH
+    const int h = (warp - 2) >> 2;        // column group: columns h*NH .. +NH
     const int q = warp & 3;               // TMEM lane quadrant: keys / dims 32q .. +31
     const int kl = q * 32 + lane;         // this thread's key (in a tile) / dim (in O^T)
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
@@ -518,7 +544,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
       const long long uq = guq % p.U;
       const int bq = (int)(uq / p.H_kv), gq = (int)(uq % p.H_kv);
       const size_t r0 = ((size_t)bq * p.H_q + (size_t)gq * p.G) * p.t;
-      for (int x = stid; x < N * 16; x += 256) {
+      for (int x = stid; x < N * 16; x += C::kSoftmax) {
         const int m = x >> 4, c = x & 15;
         uint4 v = make_uint4(0, 0, 0, 0);
         if (m < p.M) v = *reinterpret_cast<const uint4*>(Qs + (r0 + m) * D + c * 8);
@@ -609,12 +635,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
         const float* mthr = msm + mv * 3 * NH + 2 * NH;
         bool need = false;
 #pragma unroll
-        for (int c0 = 0; c0 < NH; c0 += 8) {
-          float mr[8];
+        for (int c0 = 0; c0 < NH; c0 += 4) {
+          float mr[4];
           *reinterpret_cast<float4*>(mr) = *reinterpret_cast<const float4*>(mthr + c0);
-          *reinterpret_cast<float4*>(mr + 4) = *reinterpret_cast<const float4*>(mthr + c0 + 4);
 #pragma unroll
-          for (int e = 0; e < 8; ++e) need |= x[c0 + e] > mr[e];
+          for (int e = 0; e < 4; ++e) need |= x[c0 + e] > mr[e];
         }
         const bool any_ = half_any(h, need);
         if (stid == 0) TRACE(10, tc);
@@ -629,7 +654,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
           // the quadrant-0 warp moves the running maxima into the other
           // version (readers of the current one are ordered by the barriers)
           if (q == 0) {
-            const float* mold = msm + mv * 3 * NH;
+            const float* mold = msm + mv * 3 * NH;   // quadrant maxima of this group: red[4][NH]
             float* mnew = msm + (mv ^ 1) * 3 * NH;
             bool resc = false;
             for (int c = lane; c < NH; c += 32) {
@@ -665,14 +690,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
             mbar_wait(PEMPTY(tp % C::NBP), (tp / C::NBP) & 1);
             fence_after();
 #pragma unroll 1
-            for (int cc = 0; cc < 2 * NH; cc += 8) {
+            for (int cc = 0; cc < 2 * NH; cc += C::CS) {
               const int hl = cc >= NH, c0 = cc - hl * NH;
-              float ov[8];
+              float ov[C::CS];
               const uint32_t ta = tmem + C::TM_O + hl * N + h * NH + c0 + lane_addr;
-              tmem_ld_cols<8>(ta, ov);
+              tmem_ld_cols<C::CS>(ta, ov);
 #pragma unroll
-              for (int e = 0; e < 8; ++e) ov[e] *= asm_[c0 + e];
-              tmem_st_cols<8>(ta, ov);
+              for (int e = 0; e < C::CS; ++e) ov[e] *= asm_[c0 + e];
+              tmem_st_cols<C::CS>(ta, ov);
             }
             fence_before();
           }
@@ -683,12 +708,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
         const float* msf = msm + mv * 3 * NH + NH;   // m, or 0 while m = -inf (then x = -inf)
         uint32_t phi[NH / 2], plo[NH / 2];
 #pragma unroll
-        for (int c0 = 0; c0 < NH; c0 += 8) {
-          float mr[8];
+        for (int c0 = 0; c0 < NH; c0 += 4) {
+          float mr[4];
           *reinterpret_cast<float4*>(mr) = *reinterpret_cast<const float4*>(msf + c0);
-          *reinterpret_cast<float4*>(mr + 4) = *reinterpret_cast<const float4*>(msf + c0 + 4);
 #pragma unroll
-          for (int e = 0; e < 8; e += 2) {
+          for (int e = 0; e < 4; e += 2) {
             const int c = c0 + e;
             const float2 d = __fadd2_rn(make_float2(x[c], x[c + 1]), make_float2(-mr[e], -mr[e + 1]));
             const float2 pv = make_float2(fast_exp2(d.x), fast_exp2(d.y));
@@ -706,12 +730,22 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
         if (tc >= C::NBP) mbar_wait(PEMPTY(pb), ((tc / C::NBP) - 1) & 1);
         if (stid == 0) TRACE(12, tc);
         const uint32_t pbase = sbase + C::OFF_P + pb * C::kPBytes;
+        if constexpr (NH % 8 == 0) {
 #pragma unroll
-        for (int e = 0; e < NH / 8; ++e) {
-          const int eh = h * (NH / 8) + e;               // hi chunk; lo chunks follow N / 8 later
-          sts_v4(pbase + paddr(eh), phi[4 * e], phi[4 * e + 1], phi[4 * e + 2], phi[4 * e + 3]);
-          sts_v4(pbase + paddr(eh + N / 8), plo[4 * e], plo[4 * e + 1], plo[4 * e + 2],
-                 plo[4 * e + 3]);
+          for (int e = 0; e < NH / 8; ++e) {
+            const int eh = h * (NH / 8) + e;             // hi chunk; lo chunks follow N / 8 later
+            sts_v4(pbase + paddr(eh), phi[4 * e], phi[4 * e + 1], phi[4 * e + 2], phi[4 * e + 3]);
+            sts_v4(pbase + paddr(eh + N / 8), plo[4 * e], plo[4 * e + 1], plo[4 * e + 2],
+                   plo[4 * e + 3]);
+          }
+        } else {   // groups of 4 queries: 8-byte halves of the 16-byte chunks
+#pragma unroll
+          for (int e = 0; e < NH / 4; ++e) {
+            const int col = h * NH + 4 * e;
+            const uint32_t half = (uint32_t)((col >> 2) & 1) * 8u;
+            sts_v2(pbase + paddr(col >> 3) + half, phi[2 * e], phi[2 * e + 1]);
+            sts_v2(pbase + paddr((col >> 3) + N / 8) + half, plo[2 * e], plo[2 * e + 1]);
+          }
         }
         fence_proxy_smem();
         mbar_arrive(PFULL(pb));
@@ -737,12 +771,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
       float* my = ly.ws + ((size_t)blockIdx.x * 2 + (item == 0 ? 0 : 1)) * rec;
       const float* mfin = msm + mv * 3 * NH;
 #pragma unroll 1
-      for (int c0 = 0; c0 < NH; c0 += 8) {
-        float o_hi[8], o_lo[8];
-        tmem_ld_cols<8>(tmem + C::TM_O + h * NH + c0 + lane_addr, o_hi);
-        tmem_ld_cols<8>(tmem + C::TM_O + N + h * NH + c0 + lane_addr, o_lo);
+      for (int c0 = 0; c0 < NH; c0 += C::CS) {
+        float o_hi[C::CS], o_lo[C::CS];
+        tmem_ld_cols<C::CS>(tmem + C::TM_O + h * NH + c0 + lane_addr, o_hi);
+        tmem_ld_cols<C::CS>(tmem + C::TM_O + N + h * NH + c0 + lane_addr, o_lo);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
+        for (int e = 0; e < C::CS; ++e) {
           const int c = c0 + e;
           const int m = h * NH + c;
           if (m < p.M) {
@@ -763,22 +797,22 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tck_kernel(const __grid_cons
       fence_before();
       if (nseg > 1) {
         __threadfence();
-        softmax_sync();
+        softmax_sync<C::kSoftmax>();
         if (stid == 0) {
           const int old = atomicAdd(&ly.counters[u], 1);
           *sm_flag = (old == nseg - 1);
         }
-        softmax_sync();
+        softmax_sync<C::kSoftmax>();
         if (*sm_flag) {
           __threadfence();
           // scratch: the P^T buffers (every O^T MMA of this item has completed)
           combine_unit<4>(ly.ws, rec, c_lo, c_hi, ufirst, NT, p.ctas, p.M, D, ly.O + qrow0 * D,
-                          reinterpret_cast<float*>(smem + C::OFF_P), stid, 256,
-                          [] { softmax_sync(); });
+                          reinterpret_cast<float*>(smem + C::OFF_P), stid, C::kSoftmax,
+                          [] { softmax_sync<C::kSoftmax>(); });
           if (stid == 0) ly.counters[u] = 0;
         }
       }
-      softmax_sync();   // sums / column state / flag reuse by the next item
+      softmax_sync<C::kSoftmax>();   // sums / column state / flag reuse by the next item
       if (stid == 0) TRACE(14, tcount + 1);
       tcount += n;
       ++item;
@@ -817,21 +851,29 @@ bool attn_tck_supported(int D, int dtype, int M) {
   return D == 128 && dtype == BMC_BF16 && M >= 1 && M <= 80 && encode_fn() != nullptr;
 }
 
-template <int N, int MAXL>
-static cudaError_t launch_n(const tck::Params<MAXL>& p, int ctas, cudaStream_t s) {
+template <int N, int MAXL, int NG>
+static cudaError_t launch_ng(const tck::Params<MAXL>& p, int ctas, cudaStream_t s) {
+  using C = tck::Cfg<N, NG>;
   static int attr_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);
   if (attr_dev != dev) {
-    cudaError_t e = cudaFuncSetAttribute(tck::attn_tck_kernel<N, MAXL>,
+    cudaError_t e = cudaFuncSetAttribute(tck::attn_tck_kernel<N, MAXL, NG>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)tck::Cfg<N>::kSmem);
+                                         (int)C::kSmem);
     if (e != cudaSuccess) return e;
     attr_dev = dev;
   }
-  tck::attn_tck_kernel<N, MAXL><<<ctas, tck::kThreads, tck::Cfg<N>::kSmem, s>>>(p);
+  tck::attn_tck_kernel<N, MAXL, NG><<<ctas, C::kThreads, C::kSmem, s>>>(p);
   count_launch();
   return cudaGetLastError();
+}
+// softmax column groups: 4 (640 threads) from N = 64 up (measured), else 2;
+// groups != 0 forces (BMC_OPT_TCK_GROUPS, A/B runs)
+template <int N, int MAXL>
+static cudaError_t launch_n(const tck::Params<MAXL>& p, int ctas, cudaStream_t s, int groups) {
+  const int ng = groups ? groups : (N >= 64 ? 4 : 2);
+  return ng == 4 ? launch_ng<N, MAXL, 4>(p, ctas, s) : launch_ng<N, MAXL, 2>(p, ctas, s);
 }
 
 // Tensor maps are pure functions of (base, rows): cache them so a fused
@@ -927,17 +969,17 @@ static cudaError_t launch_layers(const AttnStepArgs& a, int l0, int nl, int num_
   p.ctas = ctas;
   if (p.total_tiles == 0) return cudaSuccess;
   if constexpr (MAXL > 1) {   // multi-layer launches: GQA decode and speculative steps
-    if (p.M <= 16) return launch_n<16, MAXL>(p, ctas, s);
-    if (p.M <= 32) return launch_n<32, MAXL>(p, ctas, s);
-    if (p.M <= 48) return launch_n<48, MAXL>(p, ctas, s);
-    if (p.M <= 64) return launch_n<64, MAXL>(p, ctas, s);
-    return launch_n<80, MAXL>(p, ctas, s);
+    if (p.M <= 16) return launch_n<16, MAXL>(p, ctas, s, a.tck_groups);
+    if (p.M <= 32) return launch_n<32, MAXL>(p, ctas, s, a.tck_groups);
+    if (p.M <= 48) return launch_n<48, MAXL>(p, ctas, s, a.tck_groups);
+    if (p.M <= 64) return launch_n<64, MAXL>(p, ctas, s, a.tck_groups);
+    return launch_n<80, MAXL>(p, ctas, s, a.tck_groups);
   } else {
-    if (p.M <= 16) return launch_n<16, 1>(p, ctas, s);
-    if (p.M <= 32) return launch_n<32, 1>(p, ctas, s);
-    if (p.M <= 48) return launch_n<48, 1>(p, ctas, s);
-    if (p.M <= 64) return launch_n<64, 1>(p, ctas, s);
-    return launch_n<80, 1>(p, ctas, s);
+    if (p.M <= 16) return launch_n<16, 1>(p, ctas, s, a.tck_groups);
+    if (p.M <= 32) return launch_n<32, 1>(p, ctas, s, a.tck_groups);
+    if (p.M <= 48) return launch_n<48, 1>(p, ctas, s, a.tck_groups);
+    if (p.M <= 64) return launch_n<64, 1>(p, ctas, s, a.tck_groups);
+    return launch_n<80, 1>(p, ctas, s, a.tck_groups);
   }
 }
 

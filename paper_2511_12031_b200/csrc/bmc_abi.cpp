@@ -51,6 +51,7 @@ struct bmc_ctx {
   int attn_path = 0;
   int skip_padding = 0;          // length-aware ablation, off by default
   int copy_on_read = 1;          // BMC growth inside the fused decode step
+  int tck_groups = 0;            // keys-on-lanes kernel softmax column groups (0 auto)
   // a growth whose copy the next attention launch performs (copy-on-read):
   // the old buffers and the rows to carry over; never observable between API
   // calls (bmc_decode_step launches the consuming kernel in the same call)
@@ -435,6 +436,7 @@ static void fill_args(bmc_t h, int t, bmc::AttnStepArgs* a) {
   a->dtype = h->dt;
   a->ctas = std::min(h->attn_ctas, h->max_ctas);
   a->tree = h->tree;
+  a->tck_groups = h->tck_groups;
   for (int i = 0; i < 32; ++i) a->anc[i] = h->anc[i];
   for (int b = 0; b < h->B; ++b) a->valid[b] = h->valid[b];
 }
@@ -537,6 +539,23 @@ static int append_impl(bmc_t h, const void* K, const void* V, bool defer_growth 
   h->st.append_written_bytes += 2LL * h->U * h->row_bytes;
   for (auto& v : h->valid) v += 1;
   return 0;
+}
+
+// Append of layer l inside a fused step whose layers [l0, l) may hold
+// deferred (copy-on-read) growths: if deferring this layer's growth runs out
+// of memory, those growths are done by the realloc kernel (freeing their old
+// buffers) and the append is retried without deferral.
+static int append_fused(const bmc_t* hs, int l0, int l, const void* K, const void* V,
+                        bool defer) {
+  int rc = append_impl(hs[l], K, V, defer);
+  if (rc == BMC_ERR_OOM && defer) {
+    for (int x = l0; x < l; ++x) {
+      rc = cor_materialize(hs[x]);
+      if (rc) return rc;
+    }
+    rc = append_impl(hs[l], K, V, false);
+  }
+  return rc;
 }
 
 int bmc_append(bmc_t h, const void* K, const void* V) {
@@ -760,11 +779,32 @@ int bmc_admissible(bmc_t h, int k) {
   return (int)std::min<long long>(k, cap - mv1);
 }
 
+static int spec_step_host(const bmc_t* hs, int L, const void* const* K, const void* const* V,
+                          const void* const* Kd, const void* const* Vd, int k,
+                          const void* const* Q, float* const* O);
+
 int bmc_spec_step(const bmc_t* hs, int L, const void* const* K, const void* const* V,
                   const void* const* Kd, const void* const* Vd, int k, const void* const* Q,
                   float* const* O) {
   if (!hs || L < 1 || !K || !V || !Q || !O || k < 0 || (k > 0 && (!Kd || !Vd)))
     return fail(BMC_ERR_ARG, "null argument or k < 0");
+  {
+    // all-host arguments take the pipelined host-I/O path
+    bool all_host = true;
+    for (int l = 0; l < L && all_host; ++l)
+      if (!K[l] || !V[l] || !Q[l] || !O[l] || ptr_kind(K[l]) == 0 || ptr_kind(V[l]) == 0 ||
+          ptr_kind(Q[l]) == 0 || ptr_kind(O[l]) == 0 ||
+          (k > 0 && (!Kd[l] || !Vd[l] || ptr_kind(Kd[l]) == 0 || ptr_kind(Vd[l]) == 0)))
+        all_host = false;
+    if (all_host) {
+      for (int l = 1; l < L; ++l)
+        if (hs[l]->B != hs[0]->B || hs[l]->H_kv != hs[0]->H_kv || hs[l]->H_q != hs[0]->H_q ||
+            hs[l]->D != hs[0]->D || hs[l]->dt != hs[0]->dt || hs[l]->stream != hs[0]->stream ||
+            hs[l]->device != hs[0]->device)
+          return fail(BMC_ERR_ARG, "host-I/O speculative step needs layers of one shape and stream");
+      return spec_step_host(hs, L, K, V, Kd, Vd, k, Q, O);
+    }
+  }
   // validate every layer before enqueueing anything; all layers must admit
   // the same number of drafts (they share the step sequence)
   int k_adm = -1;
@@ -801,57 +841,65 @@ int bmc_spec_step(const bmc_t* hs, int L, const void* const* K, const void* cons
                   (h0->attn_path == 0 && M > kTcMinM && bmc::attn_tc_supported(h0->D, h0->dt, M));
   const bool tck = tc && h0->attn_path != 3 && bmc::attn_tck_supported(h0->D, h0->dt, M);
   if (tc && !tck) fused = false;
-  for (int l = 0; l < L; ++l) {
-    // copy-on-read growth when the fused launch below performs it
-    const bool defer = fused && hs[l]->copy_on_read && !hs[l]->skip_padding;
-    int rc = append_impl(hs[l], K[l], V[l], defer);
-    if (!rc && k > 0) {
-      rc = spec_write_impl(hs[l], Kd[l], Vd[l], k);
-      if (rc > 0) rc = 0;
-    }
-    if (rc) {
-      for (int x = 0; x <= l; ++x) cor_materialize(hs[x]);
-      return rc;
-    }
-  }
   if (!fused) {
+    for (int l = 0; l < L; ++l) {
+      int rc = append_impl(hs[l], K[l], V[l]);
+      if (!rc && k > 0) {
+        rc = spec_write_impl(hs[l], Kd[l], Vd[l], k);
+        if (rc > 0) rc = 0;
+      }
+      if (rc) return rc;
+    }
     for (int l = 0; l < L; ++l) {
       int rc = launch_sdpa_layer(hs[l], Q[l], O[l], t);
       if (rc) return rc;
     }
     return k_adm;
   }
+  // Layers in chunks of kMaxLayersPerLaunch: appends + drafts (growths
+  // deferred to the attention, copy-on-read), the chunk's verify launch, then
+  // the old buffers are released (at most one chunk holds old + new buffers).
   std::vector<bmc::AttnLayer> layers(L);
-  for (int l = 0; l < L; ++l) {
-    if (tck) {
-      int rc = ensure_workspace(hs[l], M);
+  for (int l0 = 0; l0 < L; l0 += bmc::kMaxLayersPerLaunch) {
+    const int nl = std::min(bmc::kMaxLayersPerLaunch, L - l0);
+    for (int l = l0; l < l0 + nl; ++l) {
+      const bool defer = hs[l]->copy_on_read && !hs[l]->skip_padding;
+      int rc = append_fused(hs, l0, l, K[l], V[l], defer);
+      if (!rc && k > 0) {
+        rc = spec_write_impl(hs[l], Kd[l], Vd[l], k);
+        if (rc > 0) rc = 0;
+      }
+      if (!rc && tck) rc = ensure_workspace(hs[l], M);
       if (rc) {
-        for (int x = 0; x < L; ++x) cor_materialize(hs[x]);
+        for (int x = l0; x <= l; ++x) cor_materialize(hs[x]);
         return rc;
       }
+      fill_layer(hs[l], Q[l], O[l], &layers[l]);
     }
-    fill_layer(hs[l], Q[l], O[l], &layers[l]);
-  }
-  bmc::AttnStepArgs a;
-  fill_args(h0, t, &a);
-  a.L = L;
-  a.layers = layers.data();
-  if (tck) {
-    a.ctas = std::min(h0->attn_ctas, h0->num_sms);
-    CK(h0, bmc::launch_attn_tck(a, h0->num_sms, h0->stream), "attn_tck");
-  } else {
-    CK(h0, bmc::launch_attn_step(a, h0->num_sms, h0->stream), "attn_step");
+    bmc::AttnStepArgs a;
+    fill_args(hs[l0], t, &a);
+    a.L = nl;
+    a.layers = &layers[l0];
+    if (tck) {
+      a.ctas = std::min(h0->attn_ctas, h0->num_sms);
+      CK(h0, bmc::launch_attn_tck(a, h0->num_sms, h0->stream), "attn_tck");
+    } else {
+      CK(h0, bmc::launch_attn_step(a, h0->num_sms, h0->stream), "attn_step");
+    }
+    for (int l = l0; l < l0 + nl; ++l) {
+      int rc = cor_release(hs[l]);
+      if (rc) return rc;
+    }
   }
   for (int l = 0; l < L; ++l) {
-    int rc = cor_release(hs[l]);
-    if (rc) return rc;
     hs[l]->n_app = hs[l]->n_draft = 0;
     account_sdpa(hs[l], t);
-    rc = inputs_consumed(hs[l]);
+    int rc = inputs_consumed(hs[l]);
     if (rc) return rc;
   }
   return k_adm;
 }
+
 
 static int decode_step_host(const bmc_t* hs, int L, const void* const* K, const void* const* V,
                             const void* const* Q, float* const* O, int n_valid);
@@ -912,54 +960,91 @@ int bmc_decode_step(const bmc_t* hs, int L, const void* const* K, const void* co
     }
     return 0;
   }
+  // Layers in chunks of kMaxLayersPerLaunch: appends (growths deferred to
+  // the attention, copy-on-read), then the chunk's launch, then the old
+  // buffers are released -- so at most one chunk holds old + new buffers.
   std::vector<bmc::AttnLayer> layers(L);
-  for (int l = 0; l < L; ++l) {
-    // copy-on-read growth (BMC policy; CUDA-core or keys-on-lanes kernel; all
-    // cap rows streamed)
-    const bool defer = hs[l]->copy_on_read && !hs[l]->skip_padding;
-    int rc = append_impl(hs[l], K[l], V[l], defer);
-    if (!rc && tck) rc = ensure_workspace(hs[l], G);
-    if (rc) {
-      for (int x = 0; x <= l; ++x) cor_materialize(hs[x]);
-      return rc;
-    }
-    fill_layer(hs[l], Q[l], O[l], &layers[l]);
-  }
-  bmc::AttnStepArgs a;
-  fill_args(hs[0], 1, &a);
-  a.L = L;
-  a.layers = layers.data();
-  if (tck) {
-    // one launch per 32 layers when every layer has the same capacity (the
-    // usual case: one r, one step sequence); else one launch per layer
-    bool same = true;
-    for (int l = 1; l < L; ++l)
-      if (layers[l].cap != layers[0].cap || layers[l].scan != layers[0].scan ||
-          (layers[l].Ksrc != nullptr) != (layers[0].Ksrc != nullptr) ||
-          layers[l].cap_src != layers[0].cap_src)
-        same = false;
-    a.ctas = std::min(h0->attn_ctas, h0->num_sms);
-    if (same) {
-      CK(h0, bmc::launch_attn_tck(a, h0->num_sms, h0->stream), "attn_tck");
-    } else {
-      for (int l = 0; l < L; ++l) {
-        bmc::AttnStepArgs a1 = a;
-        a1.L = 1;
-        a1.layers = &layers[l];
-        CK(h0, bmc::launch_attn_tck(a1, h0->num_sms, h0->stream), "attn_tck");
+  for (int l0 = 0; l0 < L; l0 += bmc::kMaxLayersPerLaunch) {
+    const int nl = std::min(bmc::kMaxLayersPerLaunch, L - l0);
+    for (int l = l0; l < l0 + nl; ++l) {
+      // copy-on-read growth (BMC policy; CUDA-core or keys-on-lanes kernel;
+      // all cap rows streamed)
+      const bool defer = hs[l]->copy_on_read && !hs[l]->skip_padding;
+      int rc = append_fused(hs, l0, l, K[l], V[l], defer);
+      if (!rc && tck) rc = ensure_workspace(hs[l], G);
+      if (rc) {
+        for (int x = l0; x <= l; ++x) cor_materialize(hs[x]);
+        return rc;
       }
+      fill_layer(hs[l], Q[l], O[l], &layers[l]);
     }
-  } else {
-    CK(hs[0], bmc::launch_attn_step(a, hs[0]->num_sms, hs[0]->stream), "attn_step");
+    bmc::AttnStepArgs a;
+    fill_args(hs[l0], 1, &a);
+    a.L = nl;
+    a.layers = &layers[l0];
+    if (tck) {
+      // one launch for the chunk when every layer has the same capacity (the
+      // usual case: one r, one step sequence); else one launch per layer
+      bool same = true;
+      for (int l = l0 + 1; l < l0 + nl; ++l)
+        if (layers[l].cap != layers[l0].cap || layers[l].scan != layers[l0].scan ||
+            (layers[l].Ksrc != nullptr) != (layers[l0].Ksrc != nullptr) ||
+            layers[l].cap_src != layers[l0].cap_src)
+          same = false;
+      a.ctas = std::min(h0->attn_ctas, h0->num_sms);
+      if (same) {
+        CK(h0, bmc::launch_attn_tck(a, h0->num_sms, h0->stream), "attn_tck");
+      } else {
+        for (int l = l0; l < l0 + nl; ++l) {
+          bmc::AttnStepArgs a1 = a;
+          a1.L = 1;
+          a1.layers = &layers[l];
+          CK(h0, bmc::launch_attn_tck(a1, h0->num_sms, h0->stream), "attn_tck");
+        }
+      }
+    } else {
+      CK(hs[0], bmc::launch_attn_step(a, hs[0]->num_sms, hs[0]->stream), "attn_step");
+    }
+    for (int l = l0; l < l0 + nl; ++l) {
+      int rc = cor_release(hs[l]);
+      if (rc) return rc;
+    }
   }
   for (int l = 0; l < L; ++l) {
-    int rc = cor_release(hs[l]);
-    if (rc) return rc;
     hs[l]->n_app = hs[l]->n_draft = 0;
     account_sdpa(hs[l], 1);
-    rc = inputs_consumed(hs[l]);
+    int rc = inputs_consumed(hs[l]);
     if (rc) return rc;
   }
+  return 0;
+}
+
+// The host-I/O pipeline of the first layer's handle, with staging slots of at
+// least per_in / per_out bytes (grown on demand; growing syncs the handle).
+static int pipe_ensure(bmc_t h0, size_t per_in, size_t per_out, Pipe** out) {
+  Pipe* pp = h0->pipe;
+  if (!pp || pp->in_bytes < per_in || pp->out_bytes < per_out) {
+    if (pp) {
+      cudaStreamSynchronize(h0->stream);
+      per_in = std::max(per_in, pp->in_bytes);
+      per_out = std::max(per_out, pp->out_bytes);
+      pipe_destroy(pp);
+    }
+    pp = new Pipe();
+    h0->pipe = pp;
+    CK(h0, cudaStreamCreateWithFlags(&pp->copy, cudaStreamNonBlocking), "pipe stream");
+    CK(h0, cudaStreamCreateWithFlags(&pp->down, cudaStreamNonBlocking), "pipe stream");
+    for (int i = 0; i < 2; ++i) {
+      CK(h0, cudaEventCreateWithFlags(&pp->in_ready[i], cudaEventDisableTiming), "pipe event");
+      CK(h0, cudaEventCreateWithFlags(&pp->compute_done[i], cudaEventDisableTiming), "pipe event");
+      CK(h0, cudaEventCreateWithFlags(&pp->out_done[i], cudaEventDisableTiming), "pipe event");
+      CK(h0, cudaMalloc((void**)&pp->in_slot[i], per_in), "pipe staging");
+      CK(h0, cudaMalloc((void**)&pp->out_slot[i], per_out), "pipe staging");
+    }
+    pp->in_bytes = per_in;
+    pp->out_bytes = per_out;
+  }
+  *out = pp;
   return 0;
 }
 
@@ -983,26 +1068,9 @@ static int decode_step_host(const bmc_t* hs, int L, const void* const* K, const 
   const size_t o = (size_t)h0->B * h0->H_q * h0->D * sizeof(float);
   // staging slot: [K of every layer][V ...][Q ...]; output slot [O ...]
   const size_t per_in = (2 * kv + q) * L, per_out = o * L;
-  Pipe* pp = h0->pipe;
-  if (!pp || pp->in_bytes < per_in || pp->out_bytes < per_out) {
-    if (pp) {
-      cudaStreamSynchronize(h0->stream);
-      pipe_destroy(pp);
-    }
-    pp = new Pipe();
-    h0->pipe = pp;
-    CK(h0, cudaStreamCreateWithFlags(&pp->copy, cudaStreamNonBlocking), "pipe stream");
-    CK(h0, cudaStreamCreateWithFlags(&pp->down, cudaStreamNonBlocking), "pipe stream");
-    for (int i = 0; i < 2; ++i) {
-      CK(h0, cudaEventCreateWithFlags(&pp->in_ready[i], cudaEventDisableTiming), "pipe event");
-      CK(h0, cudaEventCreateWithFlags(&pp->compute_done[i], cudaEventDisableTiming), "pipe event");
-      CK(h0, cudaEventCreateWithFlags(&pp->out_done[i], cudaEventDisableTiming), "pipe event");
-      CK(h0, cudaMalloc((void**)&pp->in_slot[i], per_in), "pipe staging");
-      CK(h0, cudaMalloc((void**)&pp->out_slot[i], per_out), "pipe staging");
-    }
-    pp->in_bytes = per_in;
-    pp->out_bytes = per_out;
-  }
+  Pipe* pp = nullptr;
+  rc = pipe_ensure(h0, per_in, per_out, &pp);
+  if (rc) return rc;
   const int slot = (int)(pp->step & 1);
   std::vector<const void*> dK(L), dV(L), dQ(L);
   std::vector<float*> dO(L);
@@ -1050,6 +1118,65 @@ static int decode_step_host(const bmc_t* hs, int L, const void* const* K, const 
   pp->primed[slot] = true;
   pp->step += 1;
   return 0;
+}
+
+// Host-pointer speculative step (the end-to-end form of bmc_spec_step): every
+// layer's K, V, drafts and verify queries are staged on the copy stream into
+// slot s%2, the device-pointer step runs on the compute stream, the outputs
+// go back on the download stream (as decode_step_host).
+static int spec_step_host(const bmc_t* hs, int L, const void* const* K, const void* const* V,
+                          const void* const* Kd, const void* const* Vd, int k,
+                          const void* const* Q, float* const* O) {
+  bmc_t h0 = hs[0];
+  int rc = enter(h0);
+  if (rc) return rc;
+  const int k_adm = bmc_admissible(h0, k);
+  if (k_adm < 0) return k_adm;
+  const int t = 1 + k_adm;
+  const size_t kv = (size_t)h0->U * h0->row_bytes;
+  const size_t kd = k_adm > 0 ? (size_t)h0->U * k * h0->row_bytes : 0;
+  const size_t q = (size_t)h0->B * h0->H_q * t * h0->row_bytes;
+  const size_t o = (size_t)h0->B * h0->H_q * t * h0->D * sizeof(float);
+  Pipe* pp = nullptr;
+  rc = pipe_ensure(h0, (2 * kv + 2 * kd + q) * L, o * L, &pp);
+  if (rc) return rc;
+  const int slot = (int)(pp->step & 1);
+  std::vector<const void*> dK(L), dV(L), dKd(L), dVd(L), dQ(L);
+  std::vector<float*> dO(L);
+  char* base = pp->in_slot[slot];
+  char* ob = pp->out_slot[slot];
+  for (int l = 0; l < L; ++l) {
+    dK[l] = base + kv * l;
+    dV[l] = base + kv * (L + l);
+    dKd[l] = base + kv * 2 * L + kd * l;
+    dVd[l] = base + kv * 2 * L + kd * (L + l);
+    dQ[l] = base + (kv + kd) * 2 * L + q * l;
+    dO[l] = reinterpret_cast<float*>(ob + o * l);
+  }
+  if (pp->primed[slot]) CK(h0, cudaStreamWaitEvent(pp->copy, pp->compute_done[slot], 0), "wait");
+  for (int l = 0; l < L; ++l) {
+    CK(h0, cudaMemcpyAsync((void*)dK[l], K[l], kv, cudaMemcpyHostToDevice, pp->copy), "H2D");
+    CK(h0, cudaMemcpyAsync((void*)dV[l], V[l], kv, cudaMemcpyHostToDevice, pp->copy), "H2D");
+    if (kd) {
+      CK(h0, cudaMemcpyAsync((void*)dKd[l], Kd[l], kd, cudaMemcpyHostToDevice, pp->copy), "H2D");
+      CK(h0, cudaMemcpyAsync((void*)dVd[l], Vd[l], kd, cudaMemcpyHostToDevice, pp->copy), "H2D");
+    }
+    CK(h0, cudaMemcpyAsync((void*)dQ[l], Q[l], q, cudaMemcpyHostToDevice, pp->copy), "H2D");
+  }
+  CK(h0, cudaEventRecord(pp->in_ready[slot], pp->copy), "record");
+  CK(h0, cudaStreamWaitEvent(h0->stream, pp->in_ready[slot], 0), "wait");
+  if (pp->primed[slot]) CK(h0, cudaStreamWaitEvent(h0->stream, pp->out_done[slot], 0), "wait");
+  rc = bmc_spec_step(hs, L, dK.data(), dV.data(), kd ? dKd.data() : dK.data(),
+                     kd ? dVd.data() : dV.data(), kd ? k : 0, dQ.data(), dO.data());
+  if (rc < 0) return rc;
+  CK(h0, cudaEventRecord(pp->compute_done[slot], h0->stream), "record");
+  CK(h0, cudaStreamWaitEvent(pp->down, pp->compute_done[slot], 0), "wait");
+  for (int l = 0; l < L; ++l)
+    CK(h0, cudaMemcpyAsync(O[l], dO[l], o, cudaMemcpyDeviceToHost, pp->down), "D2H");
+  CK(h0, cudaEventRecord(pp->out_done[slot], pp->down), "record");
+  pp->primed[slot] = true;
+  pp->step += 1;
+  return k_adm;
 }
 
 static int commit_impl(bmc_t h, const int* m) {
@@ -1328,6 +1455,10 @@ int bmc_set_option(bmc_t h, int key, long long value) {
     case BMC_OPT_COPY_ON_READ:
       if (value < 0 || value > 1) return fail(BMC_ERR_ARG, "copy on read");
       h->copy_on_read = (int)value;
+      return 0;
+    case BMC_OPT_TCK_GROUPS:
+      if (value != 0 && value != 2 && value != 4) return fail(BMC_ERR_ARG, "tck groups");
+      h->tck_groups = (int)value;
       return 0;
     default:
       return fail(BMC_ERR_ARG, "unknown option %d", key);

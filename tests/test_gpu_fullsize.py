@@ -263,6 +263,51 @@ def test_copy_on_read_growth(dtype, D, r, B, N, H_q):
     assert grows == math.ceil(N / r) - 1
 
 
+def test_spec_step_host_io_pipeline():
+    """bmc_spec_step with pinned host K/V/drafts/Q/O (staged on the library's
+    copy stream, outputs downloaded on its download stream) equals the
+    device-pointer step: outputs bit-identical, caches bit-identical."""
+    B, H_kv, H_q, D, N, r, L, k = 2, 2, 8, 128, 120, 16, 3, 4
+    dev = torch.device("cuda")
+    a = [bmc.KVCache(B, H_kv, H_q, D, r, N, dtype="bf16") for _ in range(L)]
+    b = [bmc.KVCache(B, H_kv, H_q, D, r, N, dtype="bf16") for _ in range(L)]
+    pa, pb = bmc.StepPlan(a), bmc.StepPlan(b)
+    g = torch.Generator().manual_seed(5)
+    it = 0
+    while max(a[0].valid()) < N - 1 - k:
+        kad = bmc.bmc_admissible(a[0].h, k)
+        t = 1 + kad
+        mk = lambda *shape: [torch.randn(*shape, generator=g).to(torch.bfloat16).pin_memory()
+                             for _ in range(L)]
+        ks, vs, kd, vd = mk(B, H_kv, D), mk(B, H_kv, D), mk(B, H_kv, k, D), mk(B, H_kv, k, D)
+        qs = mk(B, H_q, t, D)
+        oa = [torch.empty(B, H_q, t, D).pin_memory() for _ in range(L)]
+        ob = [torch.empty(B, H_q, t, D, device=dev) for _ in range(L)]
+        got = bmc.bmc_spec_step(pa, pa.ptrs(ks), pa.ptrs(vs), pa.ptrs(kd), pa.ptrs(vd), k,
+                                pa.ptrs(qs), pa.ptrs(oa))
+        assert got == kad
+        dv = lambda xs: [x.to(dev) for x in xs]
+        kk, vv, kdd, vdd, qq = dv(ks), dv(vs), dv(kd), dv(vd), dv(qs)
+        assert bmc.bmc_spec_step(pb, pb.ptrs(kk), pb.ptrs(vv), pb.ptrs(kdd), pb.ptrs(vdd), k,
+                                 pb.ptrs(qq), pb.ptrs(ob)) == kad
+        a[0].sync()
+        torch.cuda.synchronize()
+        for l in range(L):
+            assert torch.equal(oa[l], ob[l].cpu()), (it, l)
+        acc = [int((it * 5 + 2 * bb) % (kad + 1)) for bb in range(B)]
+        if kad:
+            bmc.bmc_commit_step(pa, acc)
+            bmc.bmc_commit_step(pb, acc)
+        it += 1
+    for x, y in zip(a, b):
+        kx, vx = x.kv()
+        ky, vy = y.kv()
+        assert torch.equal(_bits(kx), _bits(ky)) and torch.equal(_bits(vx), _bits(vy))
+        assert x.stats() == y.stats()
+    for x in a + b:
+        x.close()
+
+
 def test_decode_step_host_io_pipeline():
     """bmc_decode_step with pinned host K/V/Q/O (the pipelined end-to-end path:
     copy stream, double-buffered staging) equals the device-pointer step."""

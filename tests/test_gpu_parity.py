@@ -210,6 +210,33 @@ def test_tcgen05_verify_path(path, H_kv, H_q, k, ctas):
     p.close()
 
 
+@pytest.mark.parametrize("groups", [2, 4])
+@pytest.mark.parametrize("H_kv,H_q,k,ctas", [(2, 2, 4, 7), (2, 6, 7, 0), (1, 8, 3, 0),
+                                             (2, 16, 4, 5), (1, 8, 7, 0), (1, 8, 8, 3),
+                                             (1, 16, 4, 0)])
+def test_tcgen05_softmax_groups(groups, H_kv, H_q, k, ctas):
+    """Keys-on-lanes kernel with 2 or 4 softmax column groups (384 / 640
+    threads; BMC_OPT_TCK_GROUPS) against the oracle for N = 16 ... 80 query
+    columns (M = 5, 24, 32, 40, 64, 72, 80): 4 groups of N/4 columns exercise
+    the 4-column TMEM loads and 8-byte P stores (N/4 = 4, 12, 20)."""
+    p = Pair(2, H_kv, H_q, 128, 24, 300, dtype="bf16", seed=31, ctas=ctas)
+    p.gpu.set_option(bmc.BMC_OPT_ATTN_PATH, 4)
+    p.gpu.set_option(bmc.BMC_OPT_TCK_GROUPS, groups)
+    for _ in range(3):
+        p.append()
+    p.sdpa()
+    it = 0
+    while p.orc.stats()["valid_max"] < 280:
+        p.append()
+        k_adm = p.spec_write(k) if k else 0
+        p.sdpa(n_valid=-1)
+        if k_adm:
+            p.commit_rows(synth.acceptance(31, it, 2, k_adm))
+        it += 1
+    p.check_state()
+    p.close()
+
+
 @pytest.mark.parametrize("path", [3, 4])
 def test_tcgen05_peaky_long(path):
     """Near one-hot rows through the tensor-core paths: P is split into

@@ -16,7 +16,8 @@ import torch  # noqa: E402
 from paper_2511_12031_b200 import bmc  # noqa: E402
 
 
-def attn_at(B, H_kv, H_q, D, cap, t=1, reps=50, dtype="bf16", ctas=0, layers=8, path=0):
+def attn_at(B, H_kv, H_q, D, cap, t=1, reps=50, dtype="bf16", ctas=0, layers=8, path=0,
+            groups=0):
     """SDPA over `layers` independent handles filled to `cap` rows (upfront
     policy so the buffer is exactly cap rows), round-robin so each launch reads
     an L2-cold cache."""
@@ -28,6 +29,8 @@ def attn_at(B, H_kv, H_q, D, cap, t=1, reps=50, dtype="bf16", ctas=0, layers=8, 
         if ctas:
             h.set_option(bmc.BMC_OPT_ATTN_CTAS, ctas)
         h.set_option(bmc.BMC_OPT_ATTN_PATH, path)
+        if groups:
+            h.set_option(bmc.BMC_OPT_TCK_GROUPS, groups)
         hs.append(h)
     k = torch.randn(B, H_kv, D, device="cuda").to(tdt)
     for h in hs:
@@ -52,7 +55,8 @@ def attn_at(B, H_kv, H_q, D, cap, t=1, reps=50, dtype="bf16", ctas=0, layers=8, 
     by = 2.0 * B * H_kv * cap * D * eb + B * H_q * t * D * (eb + 4)
     for h in hs:
         h.close()
-    return {"cap": cap, "t": t, "M": (H_q // H_kv) * t, "path": path, "us": ms * 1e3,
+    return {"cap": cap, "t": t, "M": (H_q // H_kv) * t, "path": path, "groups": groups,
+            "us": ms * 1e3,
             "GBps": by / ms / 1e6}
 
 
@@ -148,6 +152,9 @@ def main():
     if args.what == "tcsweep":        # keys-on-lanes kernel: 70B shape, M = 8 t
         out["tck"] = [attn_at(8, 8, 64, 128, cap, t=t, path=4, reps=8, layers=4)
                       for cap in (8192, 32768) for t in (1, 2, 4, 5, 8, 9)]
+    if args.what == "tcgroups":       # softmax column groups 2 vs 4, 70B shape
+        out["tck"] = [attn_at(8, 8, 64, 128, cap, t=t, path=4, reps=8, layers=4, groups=g)
+                      for cap in (8192, 32768) for t in (1, 2, 4, 6, 8, 9) for g in (2, 4)]
     if args.what == "tcrepro":
         out["verify"] = [attn_at(8, 8, 64, 128, 1024, t=9, path=1, reps=4, layers=2)]
     if args.what == "attn4096":       # ncu target: 7B shape at full context
