@@ -254,8 +254,8 @@ int bmc_sync(bmc_t h);
                               kernel); 0 = separate realloc_copy_zero launch.
                               Cache contents and ledger are identical.
      6 BMC_OPT_TCK_GROUPS     softmax column groups of the keys-on-lanes
-                              tcgen05 kernel: 0 auto (4 for G*t > 48, else
-                              2), 2 (384 threads), 4 (640 threads).  Tuning /
+                              tcgen05 kernel: 0 auto (4 for 16 < G*t <= 64,
+                              else 2), 2 (384 threads), 4 (640 threads).  Tuning /
                               A/B only; results agree within the tolerance. */
 #define BMC_OPT_ATTN_CTAS 1
 #define BMC_OPT_ATTN_PATH 2

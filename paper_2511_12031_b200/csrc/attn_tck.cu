@@ -868,11 +868,13 @@ static cudaError_t launch_ng(const tck::Params<MAXL>& p, int ctas, cudaStream_t 
   count_launch();
   return cudaGetLastError();
 }
-// softmax column groups: 4 (640 threads) from N = 64 up (measured), else 2;
-// groups != 0 forces (BMC_OPT_TCK_GROUPS, A/B runs)
+// softmax column groups: 4 (640 threads) for N = 32 ... 64, else 2 (measured
+// on the 70B shape, tools/microbench.py --what tcgroups: +1..7% at M = 32..64;
+// at N = 80 the 96-register budget of 640 threads spills, at N = 16 the
+// groups are too narrow); groups != 0 forces (BMC_OPT_TCK_GROUPS, A/B runs)
 template <int N, int MAXL>
 static cudaError_t launch_n(const tck::Params<MAXL>& p, int ctas, cudaStream_t s, int groups) {
-  const int ng = groups ? groups : (N >= 64 ? 4 : 2);
+  const int ng = groups ? groups : ((N >= 32 && N <= 64) ? 4 : 2);
   return ng == 4 ? launch_ng<N, MAXL, 4>(p, ctas, s) : launch_ng<N, MAXL, 2>(p, ctas, s);
 }
 
