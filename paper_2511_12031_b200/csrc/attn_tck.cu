@@ -74,11 +74,14 @@ constexpr float kRescale = 8.0f;
 // NG column groups of softmax warps (4 warps each, one per TMEM lane
 // quadrant): 2 (384 threads) or 4 (640 threads: twice the warps per SMSP to
 // hide the TMEM / shared-memory / barrier latencies of large N)
-template <int N, int NG>
+// NS <= N: query columns the softmax handles (the MMAs run N, a multiple of
+// 16; NS = 72 skips the 8 padding columns of the 70B verify step, M = 72)
+template <int N, int NG, int NS = N>
 struct Cfg {
   static_assert(N % 16 == 0 && N >= 16 && N <= 80, "query columns");
   static_assert(NG == 2 || NG == 4, "column groups");
-  static constexpr int NH = N / NG;                         // columns per softmax group
+  static_assert(NS <= N && NS % (4 * NG) == 0, "softmax columns");
+  static constexpr int NH = NS / NG;                        // columns per softmax group
   static constexpr int kSoftmax = NG * 128;                 // softmax threads
   static constexpr int kThreads = 128 + kSoftmax;
   static constexpr int kWarpV = 2 + 4 * NG;                 // V producer
@@ -279,10 +282,10 @@ __device__ __forceinline__ float warp_sum(float x) {
   return x;
 }
 
-template <int N, int MAXL, int NG>
-__global__ void __launch_bounds__(Cfg<N, NG>::kThreads, 1)
+template <int N, int MAXL, int NG, int NS>
+__global__ void __launch_bounds__(Cfg<N, NG, NS>::kThreads, 1)
     attn_tck_kernel(const __grid_constant__ Params<MAXL> p) {
-  using C = Cfg<N, NG>;
+  using C = Cfg<N, NG, NS>;
   constexpr int kThreads = C::kThreads;
   constexpr int NH = C::NH;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -382,7 +385,7 @@ __global__ void __launch_bounds__(Cfg<N, NG>::kThreads, 1)
     // ------------------------------------------------------ TMA producers
     if (lane == 0) {
       const bool isK = warp == 0;
-      const int NS = isK ? C::KS : C::VS;
+      const int nst = isK ? C::KS : C::VS;
       const uint32_t ring = sbase + (isK ? C::OFF_K : C::OFF_V);
       const uint64_t pol = evict_first_policy();
       int s = 0;
@@ -407,7 +410,7 @@ __global__ void __launch_bounds__(Cfg<N, NG>::kThreads, 1)
           tma_load_2d(dst + kBox, tm, 64, row, fb, pol);
         }
         if (++j == p.tpu) { j = 0; ++gu; }
-        if (++s == NS) { s = 0; ph ^= 1; }
+        if (++s == nst) { s = 0; ph ^= 1; }
       }
     }
   } else if (warp == 1) {
@@ -851,20 +854,20 @@ bool attn_tck_supported(int D, int dtype, int M) {
   return D == 128 && dtype == BMC_BF16 && M >= 1 && M <= 80 && encode_fn() != nullptr;
 }
 
-template <int N, int MAXL, int NG>
+template <int N, int MAXL, int NG, int NS = N>
 static cudaError_t launch_ng(const tck::Params<MAXL>& p, int ctas, cudaStream_t s) {
-  using C = tck::Cfg<N, NG>;
+  using C = tck::Cfg<N, NG, NS>;
   static int attr_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);
   if (attr_dev != dev) {
-    cudaError_t e = cudaFuncSetAttribute(tck::attn_tck_kernel<N, MAXL, NG>,
+    cudaError_t e = cudaFuncSetAttribute(tck::attn_tck_kernel<N, MAXL, NG, NS>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)C::kSmem);
     if (e != cudaSuccess) return e;
     attr_dev = dev;
   }
-  tck::attn_tck_kernel<N, MAXL, NG><<<ctas, C::kThreads, C::kSmem, s>>>(p);
+  tck::attn_tck_kernel<N, MAXL, NG, NS><<<ctas, C::kThreads, C::kSmem, s>>>(p);
   count_launch();
   return cudaGetLastError();
 }
@@ -875,6 +878,9 @@ static cudaError_t launch_ng(const tck::Params<MAXL>& p, int ctas, cudaStream_t 
 template <int N, int MAXL>
 static cudaError_t launch_n(const tck::Params<MAXL>& p, int ctas, cudaStream_t s, int groups) {
   const int ng = groups ? groups : ((N >= 32 && N <= 64) ? 4 : 2);
+  if constexpr (N == 80) {   // M <= 72 (the 70B verify step): softmax over 72 columns
+    if (groups == 0 && p.M <= 72) return launch_ng<80, MAXL, 2, 72>(p, ctas, s);
+  }
   return ng == 4 ? launch_ng<N, MAXL, 4>(p, ctas, s) : launch_ng<N, MAXL, 2>(p, ctas, s);
 }
 

@@ -210,7 +210,7 @@ def test_tcgen05_verify_path(path, H_kv, H_q, k, ctas):
     p.close()
 
 
-@pytest.mark.parametrize("groups", [2, 4])
+@pytest.mark.parametrize("groups", [0, 2, 4])
 @pytest.mark.parametrize("H_kv,H_q,k,ctas", [(2, 2, 4, 7), (2, 6, 7, 0), (1, 8, 3, 0),
                                              (2, 16, 4, 5), (1, 8, 7, 0), (1, 8, 8, 3),
                                              (1, 16, 4, 0)])
