@@ -255,9 +255,7 @@ int bmc_sync(bmc_t h);
                               Cache contents and ledger are identical.
      6 BMC_OPT_TCK_GROUPS     softmax column groups of the keys-on-lanes
                               tcgen05 kernel: 0 auto (4 for 16 < G*t <= 64,
-                              else 2; at 64 < G*t <= 72 the softmax skips the
-                              8 padding columns), 2 (384 threads), 4 (640
-                              threads), both over all N columns.  Tuning /
+                              else 2), 2 (384 threads), 4 (640 threads).  Tuning /
                               A/B only; results agree within the tolerance. */
 #define BMC_OPT_ATTN_CTAS 1
 #define BMC_OPT_ATTN_PATH 2

@@ -75,7 +75,9 @@ constexpr float kRescale = 8.0f;
 // quadrant): 2 (384 threads) or 4 (640 threads: twice the warps per SMSP to
 // hide the TMEM / shared-memory / barrier latencies of large N)
 // NS <= N: query columns the softmax handles (the MMAs run N, a multiple of
-// 16; NS = 72 skips the 8 padding columns of the 70B verify step, M = 72)
+// 16).  A softmax over 72 of 80 columns at M = 72 measured no faster (the
+// tile period there is set by shared-memory traffic), so the
+// launcher always uses NS = N.
 template <int N, int NG, int NS = N>
 struct Cfg {
   static_assert(N % 16 == 0 && N >= 16 && N <= 80, "query columns");
@@ -878,9 +880,6 @@ static cudaError_t launch_ng(const tck::Params<MAXL>& p, int ctas, cudaStream_t 
 template <int N, int MAXL>
 static cudaError_t launch_n(const tck::Params<MAXL>& p, int ctas, cudaStream_t s, int groups) {
   const int ng = groups ? groups : ((N >= 32 && N <= 64) ? 4 : 2);
-  if constexpr (N == 80) {   // M <= 72 (the 70B verify step): softmax over 72 columns
-    if (groups == 0 && p.M <= 72) return launch_ng<80, MAXL, 2, 72>(p, ctas, s);
-  }
   return ng == 4 ? launch_ng<N, MAXL, 4>(p, ctas, s) : launch_ng<N, MAXL, 2>(p, ctas, s);
 }
 

@@ -152,7 +152,7 @@ def main():
     if args.what == "tcsweep":        # keys-on-lanes kernel: 70B shape, M = 8 t
         out["tck"] = [attn_at(8, 8, 64, 128, cap, t=t, path=4, reps=8, layers=4)
                       for cap in (8192, 32768) for t in (1, 2, 4, 5, 8, 9)]
-    if args.what == "tc72ab":         # M = 72: auto (softmax over 72 columns) vs forced 2 groups
+    if args.what == "tc72ab":         # M = 72: auto vs forced 2 groups (A/B harness)
         out["tck"] = [attn_at(8, 8, 64, 128, cap, t=9, path=4, reps=10, layers=4, groups=g)
                       for cap in (8192, 32768) for g in (0, 2, 0, 2)]
     if args.what == "tcgroups":       # softmax column groups 2 vs 4, 70B shape
