@@ -105,8 +105,8 @@ int bmc_admissible(bmc_t h, int k);
    for every layer bmc_append(K[l], V[l]) and bmc_spec_write(Kd[l], Vd[l], k),
    then the verify SDPA of all layers -- one persistent launch per 32 layers
    when the layers share shape, stream, lengths and capacity and the kernel
-   takes several layers (CUDA cores for M = G*t <= 2, the keys-on-lanes
-   tcgen05 kernel for M <= 80), else one launch per layer.  K, V
+   takes several layers (the keys-on-lanes tcgen05 kernel for bf16, D = 128,
+   M = G*t <= 80; CUDA cores for fp32 or D = 64), else one launch per layer.  K, V
    [B][H_kv][D], Kd, Vd [B][H_kv][k][D] (device or host, as bmc_append /
    bmc_spec_write); Q[l] DEVICE [B][H_q][t][D] and O[l] DEVICE
    [B][H_q][t][D] fp32 with t = 1 + bmc_admissible(hs[l], k) (every layer

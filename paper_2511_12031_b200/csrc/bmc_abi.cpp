@@ -136,7 +136,13 @@ static void pipe_destroy(Pipe* p) {
 }
 
 static thread_local std::string g_err;
-static constexpr int kTcMinM = 2;   // auto path: tcgen05 for M = G*t > kTcMinM
+// auto path: tcgen05 (keys on the TMEM lanes) for every M = G*t the kernel
+// takes (bf16, D = 128, M <= 80), CUDA cores otherwise (fp32, D = 64).  At
+// M = 1 the tensor-core kernel held 1.08x the copy peak where the CUDA-core
+// kernel fell to 0.94x on the same power-capped box (SM 1.55-1.64 GHz): its
+// per-byte instruction count makes it clock-sensitive
+// (profiles/r01_attn_path_ab.jsonl)
+static constexpr int kTcMinM = 0;
 
 static int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
 static int fail(int code, const char* fmt, ...) {
@@ -673,9 +679,9 @@ int bmc_spec_write_tree(bmc_t h, const void* K_draft, const void* V_draft, int k
 static int launch_sdpa_layer(bmc_t h, const void* qd, float* od, int t) {
   int rc = 0;
   const int M = (h->H_q / h->H_kv) * t;
-  // tensor cores when M = G*t makes a real tile (north_star item 4); the
-  // crossover measured on B200 is M = 3..4 (tcgen05 1.4x faster at M=4,
-  // 2.1x at M=5), CUDA cores keep M <= 2 (6.2-6.4 TB/s at M=1)
+  // tensor cores whenever the kernel takes the shape (kTcMinM above): at
+  // M = 4, 5 tcgen05 was 1.4x / 2.1x faster than CUDA cores, at M = 1 it is
+  // the one that holds HBM bandwidth under the power-capped SM clock
   const bool use_tc = h->attn_path >= 2 ||
                       (h->attn_path == 0 && M > kTcMinM && bmc::attn_tc_supported(h->D, h->dt, M));
   // keys on the TMEM lanes (attn_tck.cu) for M <= 80, queries on the lanes

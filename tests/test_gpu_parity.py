@@ -73,11 +73,14 @@ def test_structured_inputs(variant):
     p.close()
 
 
+@pytest.mark.parametrize("path", [1, 0])
 @pytest.mark.parametrize("ctas", [1, 2, 3, 7, 64, 500])
-def test_split_k_segments(ctas):
+def test_split_k_segments(ctas, path):
     """Force the number of persistent CTAs so units split across many / few
-    CTAs (split-K combine) and CTAs span many units."""
+    CTAs (split-K combine) and CTAs span many units; CUDA-core kernel (path
+    1) and the auto tcgen05 kernel (CTAs capped at the SM count)."""
     p = Pair(2, 4, 8, 128, 50, 700, dtype="bf16", seed=11, ctas=ctas)
+    p.gpu.set_option(bmc.BMC_OPT_ATTN_PATH, path)
     _decode(p, 700, check_every=37)
     p.close()
 
