@@ -1,0 +1,48 @@
+"""Where a 7B-shaped generation (32 layers, B=16, 0 -> 4096, r=128) spends
+its time: host time of each bmc_decode_step call and GPU time between events,
+growth steps vs the other steps, for three generations in a row (the first
+one fills the stream-ordered pool)."""
+import os
+import sys
+import time
+
+sys.path.insert(0, os.getcwd())
+import torch  # noqa: E402
+
+from paper_2511_12031_b200 import bmc  # noqa: E402
+
+L, B, H, D, N, r = 32, 16, 32, 128, 4096, 128
+k = [torch.randn(B, H, D, device="cuda").to(torch.bfloat16) for _ in range(L)]
+q = [torch.randn(B, H, 1, D, device="cuda").to(torch.bfloat16) for _ in range(L)]
+o = [torch.empty(B, H, 1, D, device="cuda") for _ in range(L)]
+
+
+def gen(tag):
+    hs = [bmc.KVCache(B, H, H, D, r, N, dtype="bf16") for _ in range(L)]
+    plan = bmc.StepPlan(hs)
+    K, Q, O = plan.ptrs(k), plan.ptrs(q), plan.ptrs(o)
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(N + 1)]
+    host = [0.0] * (N + 1)
+    T0 = time.perf_counter()
+    ev[0].record()
+    for n in range(1, N + 1):
+        t0 = time.perf_counter()
+        bmc.bmc_decode_step(plan, K, K, Q, O, n)
+        host[n] = time.perf_counter() - t0
+        ev[n].record()
+    torch.cuda.synchronize()
+    T1 = time.perf_counter()
+    g = [ev[n - 1].elapsed_time(ev[n]) for n in range(1, N + 1)]
+    grow = [n for n in range(2, N + 1) if (n - 1) % r == 0]
+    gs = sum(g[n - 1] for n in grow)
+    hg = sum(host[n] for n in grow) * 1e3
+    print(f"{tag}: wall {1e3 * (T1 - T0):.0f} ms, gpu {sum(g):.0f} ms; {len(grow)} growth steps: "
+          f"gpu {gs:.0f} ms, host {hg:.0f} ms; other steps: host {1e3 * sum(host) - hg:.0f} ms; "
+          f"max growth host {max(host[n] for n in grow) * 1e3:.1f} ms", flush=True)
+    for h in hs:
+        h.close()
+
+
+for i in range(3):
+    gen(f"gen{i}")
