@@ -1025,6 +1025,30 @@ int bmc_decode_step(const bmc_t* hs, int L, const void* const* K, const void* co
   return 0;
 }
 
+// Copy L per-layer blocks of sz bytes.  One cudaMemcpyAsync when both sides
+// are address-contiguous across the layers and the runtime accepts the span
+// (two pinned allocations can merely abut: the span then crosses them and the
+// call fails with cudaErrorInvalidValue before enqueueing anything, so the
+// copies go layer by layer); else one copy per layer.
+static cudaError_t copy_layers(void* const* dst, const void* const* src, size_t sz, int L,
+                               cudaMemcpyKind kind, cudaStream_t s) {
+  bool contiguous = true;
+  for (int l = 1; l < L && contiguous; ++l)
+    if ((const char*)src[l] != (const char*)src[0] + sz * l ||
+        (char*)dst[l] != (char*)dst[0] + sz * l)
+      contiguous = false;
+  if (contiguous) {
+    cudaError_t e = cudaMemcpyAsync(dst[0], src[0], sz * L, kind, s);
+    if (e != cudaErrorInvalidValue) return e;
+    cudaGetLastError();   // not sticky; fall back to per-layer copies
+  }
+  for (int l = 0; l < L; ++l) {
+    cudaError_t e = cudaMemcpyAsync(dst[l], src[l], sz, kind, s);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 // The host-I/O pipeline of the first layer's handle, with staging slots of at
 // least per_in / per_out bytes (grown on demand; growing syncs the handle).
 static int pipe_ensure(bmc_t h0, size_t per_in, size_t per_out, Pipe** out) {
@@ -1091,18 +1115,10 @@ static int decode_step_host(const bmc_t* hs, int L, const void* const* K, const 
     dO[l] = reinterpret_cast<float*>(ob + o * l);
   }
   // one copy per tensor when the caller's per-layer buffers are contiguous
-  auto contiguous = [&](const void* const* a, size_t sz) {
-    for (int l = 1; l < L; ++l)
-      if ((const char*)a[l] != (const char*)a[0] + sz * l) return false;
-    return true;
-  };
   auto h2d = [&](char* dst, const void* const* src, size_t sz) -> int {
-    if (contiguous(src, sz)) {
-      CK(h0, cudaMemcpyAsync(dst, src[0], sz * L, cudaMemcpyHostToDevice, pp->copy), "H2D");
-    } else {
-      for (int l = 0; l < L; ++l)
-        CK(h0, cudaMemcpyAsync(dst + sz * l, src[l], sz, cudaMemcpyHostToDevice, pp->copy), "H2D");
-    }
+    std::vector<void*> d(L);
+    for (int l = 0; l < L; ++l) d[l] = dst + sz * l;
+    CK(h0, copy_layers(d.data(), src, sz, L, cudaMemcpyHostToDevice, pp->copy), "H2D");
     return 0;
   };
   if (pp->primed[slot]) CK(h0, cudaStreamWaitEvent(pp->copy, pp->compute_done[slot], 0), "wait");
@@ -1114,12 +1130,8 @@ static int decode_step_host(const bmc_t* hs, int L, const void* const* K, const 
   if (rc) return rc;
   CK(h0, cudaEventRecord(pp->compute_done[slot], h0->stream), "record");
   CK(h0, cudaStreamWaitEvent(pp->down, pp->compute_done[slot], 0), "wait");
-  if (contiguous((const void* const*)O, o)) {
-    CK(h0, cudaMemcpyAsync(O[0], ob, o * L, cudaMemcpyDeviceToHost, pp->down), "D2H");
-  } else {
-    for (int l = 0; l < L; ++l)
-      CK(h0, cudaMemcpyAsync(O[l], dO[l], o, cudaMemcpyDeviceToHost, pp->down), "D2H");
-  }
+  CK(h0, copy_layers((void* const*)O, (const void* const*)dO.data(), o, L, cudaMemcpyDeviceToHost,
+                     pp->down), "D2H");
   CK(h0, cudaEventRecord(pp->out_done[slot], pp->down), "record");
   pp->primed[slot] = true;
   pp->step += 1;
@@ -1160,15 +1172,16 @@ static int spec_step_host(const bmc_t* hs, int L, const void* const* K, const vo
     dO[l] = reinterpret_cast<float*>(ob + o * l);
   }
   if (pp->primed[slot]) CK(h0, cudaStreamWaitEvent(pp->copy, pp->compute_done[slot], 0), "wait");
-  for (int l = 0; l < L; ++l) {
-    CK(h0, cudaMemcpyAsync((void*)dK[l], K[l], kv, cudaMemcpyHostToDevice, pp->copy), "H2D");
-    CK(h0, cudaMemcpyAsync((void*)dV[l], V[l], kv, cudaMemcpyHostToDevice, pp->copy), "H2D");
-    if (kd) {
-      CK(h0, cudaMemcpyAsync((void*)dKd[l], Kd[l], kd, cudaMemcpyHostToDevice, pp->copy), "H2D");
-      CK(h0, cudaMemcpyAsync((void*)dVd[l], Vd[l], kd, cudaMemcpyHostToDevice, pp->copy), "H2D");
-    }
-    CK(h0, cudaMemcpyAsync((void*)dQ[l], Q[l], q, cudaMemcpyHostToDevice, pp->copy), "H2D");
-  }
+  // one copy per tensor when the caller's per-layer buffers are contiguous
+  // (the staging slot keeps every tensor's layers contiguous), else per layer
+  auto h2d = [&](const std::vector<const void*>& dst, const void* const* src, size_t sz) -> int {
+    CK(h0, copy_layers((void* const*)dst.data(), src, sz, L, cudaMemcpyHostToDevice, pp->copy),
+       "H2D");
+    return 0;
+  };
+  if ((rc = h2d(dK, K, kv)) || (rc = h2d(dV, V, kv)) || (kd && (rc = h2d(dKd, Kd, kd))) ||
+      (kd && (rc = h2d(dVd, Vd, kd))) || (rc = h2d(dQ, Q, q)))
+    return rc;
   CK(h0, cudaEventRecord(pp->in_ready[slot], pp->copy), "record");
   CK(h0, cudaStreamWaitEvent(h0->stream, pp->in_ready[slot], 0), "wait");
   if (pp->primed[slot]) CK(h0, cudaStreamWaitEvent(h0->stream, pp->out_done[slot], 0), "wait");
@@ -1177,8 +1190,8 @@ static int spec_step_host(const bmc_t* hs, int L, const void* const* K, const vo
   if (rc < 0) return rc;
   CK(h0, cudaEventRecord(pp->compute_done[slot], h0->stream), "record");
   CK(h0, cudaStreamWaitEvent(pp->down, pp->compute_done[slot], 0), "wait");
-  for (int l = 0; l < L; ++l)
-    CK(h0, cudaMemcpyAsync(O[l], dO[l], o, cudaMemcpyDeviceToHost, pp->down), "D2H");
+  CK(h0, copy_layers((void* const*)O, (const void* const*)dO.data(), o, L, cudaMemcpyDeviceToHost,
+                     pp->down), "D2H");
   CK(h0, cudaEventRecord(pp->out_done[slot], pp->down), "record");
   pp->primed[slot] = true;
   pp->step += 1;

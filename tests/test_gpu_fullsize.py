@@ -267,10 +267,12 @@ def test_copy_on_read_growth(dtype, D, r, B, N, H_q, path):
     assert grows == math.ceil(N / r) - 1
 
 
-def test_spec_step_host_io_pipeline():
+@pytest.mark.parametrize("contiguous", [False, True])
+def test_spec_step_host_io_pipeline(contiguous):
     """bmc_spec_step with pinned host K/V/drafts/Q/O (staged on the library's
-    copy stream, outputs downloaded on its download stream) equals the
-    device-pointer step: outputs bit-identical, caches bit-identical."""
+    copy stream, outputs downloaded on its download stream; one copy per
+    tensor when the layers' buffers are contiguous) equals the device-pointer
+    step: outputs bit-identical, caches bit-identical."""
     B, H_kv, H_q, D, N, r, L, k = 2, 2, 8, 128, 120, 16, 3, 4
     dev = torch.device("cuda")
     a = [bmc.KVCache(B, H_kv, H_q, D, r, N, dtype="bf16") for _ in range(L)]
@@ -281,11 +283,16 @@ def test_spec_step_host_io_pipeline():
     while max(a[0].valid()) < N - 1 - k:
         kad = bmc.bmc_admissible(a[0].h, k)
         t = 1 + kad
-        mk = lambda *shape: [torch.randn(*shape, generator=g).to(torch.bfloat16).pin_memory()
-                             for _ in range(L)]
+        if contiguous:
+            mk = lambda *shape: list(torch.randn(L, *shape, generator=g).to(torch.bfloat16)
+                                     .pin_memory().unbind(0))
+        else:
+            mk = lambda *shape: [torch.randn(*shape, generator=g).to(torch.bfloat16).pin_memory()
+                                 for _ in range(L)]
         ks, vs, kd, vd = mk(B, H_kv, D), mk(B, H_kv, D), mk(B, H_kv, k, D), mk(B, H_kv, k, D)
         qs = mk(B, H_q, t, D)
-        oa = [torch.empty(B, H_q, t, D).pin_memory() for _ in range(L)]
+        oa = (list(torch.empty(L, B, H_q, t, D).pin_memory().unbind(0)) if contiguous
+              else [torch.empty(B, H_q, t, D).pin_memory() for _ in range(L)])
         ob = [torch.empty(B, H_q, t, D, device=dev) for _ in range(L)]
         got = bmc.bmc_spec_step(pa, pa.ptrs(ks), pa.ptrs(vs), pa.ptrs(kd), pa.ptrs(vd), k,
                                 pa.ptrs(qs), pa.ptrs(oa))
