@@ -265,6 +265,17 @@ int bmc_sync(bmc_t h);
 #define BMC_OPT_TCK_GROUPS 6
 int bmc_set_option(bmc_t h, int key, long long value);
 
+/* bmc_pool_reserve: map `bytes` of device memory into the library's
+   stream-ordered pool on `device` (-1 = current) now: one allocation and
+   free (synchronous), kept by the pool (release threshold = max).  Growth
+   allocations of every handle are then carved from it instead
+   of waiting for the driver to grow the pool, which on B200 blocks the host
+   for up to 0.6 s per growth step (profiles/r01_growth_cost_7b.txt).  Cache
+   capacities and the ledger are unchanged; the memory is held by the
+   process like a serving deployment's KV budget.  Errors: ARG (bytes < 0),
+   OOM, CUDA. */
+int bmc_pool_reserve(int device, long long bytes);
+
 /* Kernels launched by this library in this process so far (all handles). */
 unsigned long long bmc_launch_count(void);
 

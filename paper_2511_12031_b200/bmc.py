@@ -37,7 +37,7 @@ _NAMES = {0: "OK", -1: "ARG", -2: "STATE", -3: "CAPACITY", -4: "OOM", -5: "CUDA"
 
 EXPORTS = ["bmc_create", "bmc_create_ex", "bmc_append", "bmc_append_n", "bmc_spec_write",
            "bmc_sdpa", "bmc_admissible", "bmc_spec_step",
-           "bmc_commit", "bmc_commit_rows", "bmc_commit_step", "bmc_commit_path", "bmc_spec_write_tree",
+           "bmc_commit", "bmc_commit_rows", "bmc_commit_step", "bmc_commit_path", "bmc_pool_reserve", "bmc_spec_write_tree",
            "bmc_decode_step", "bmc_destroy", "bmc_stats", "bmc_kv_view",
            "bmc_valid", "bmc_read_cache", "bmc_sync", "bmc_set_option", "bmc_launch_count", "bmc_last_error"]
 
@@ -82,6 +82,7 @@ def load(path: str = SO_PATH):
     L.bmc_commit.argtypes = [vp, i]
     L.bmc_commit_rows.argtypes = [vp, ctypes.POINTER(ctypes.c_int)]
     L.bmc_commit_step.argtypes = [vp, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
+    L.bmc_pool_reserve.argtypes = [ctypes.c_int, ctypes.c_longlong]
     L.bmc_destroy.argtypes = [vp]
     L.bmc_spec_write_tree.argtypes = [vp, vp, vp, i, ctypes.POINTER(ctypes.c_int)]
     L.bmc_commit_path.argtypes = [vp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int), i]
@@ -149,6 +150,11 @@ def bmc_spec_write(h, K_draft, V_draft, k: int) -> int:
 
 def bmc_sdpa(h, Q, n_valid: int, O) -> int:
     return _check(load().bmc_sdpa(h, _ptr(Q), n_valid, _ptr(O)), "bmc_sdpa")
+
+
+def bmc_pool_reserve(device: int, nbytes: int) -> int:
+    """Map nbytes of device memory into the library's growth pool now."""
+    return _check(load().bmc_pool_reserve(device, nbytes), "bmc_pool_reserve")
 
 
 def bmc_commit(h, n_accepted: int) -> int:

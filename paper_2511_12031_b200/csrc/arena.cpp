@@ -16,6 +16,7 @@
 //     take only two values per tensor.
 //   kind 1 (pool): cudaMallocFromPoolAsync / cudaFreeAsync on a per-device
 //     memory pool with an unbounded release threshold (stream-ordered reuse).
+#include <cstdlib>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
@@ -275,6 +276,32 @@ int arena_release(Arena* a, Buffer* b, cudaStream_t s) {
     (void)a;
   }
   *b = Buffer();
+  return rc;
+}
+
+// Map `bytes` of physical memory into the device's stream-ordered pool now
+// (allocate + free once; the release threshold keeps it), so later growth
+// allocations are carved from it instead of waiting for the driver to grow
+// the pool (measured: up to 0.6 s host stalls per growth step otherwise).
+int pool_reserve(int device, size_t bytes) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  cudaMemPool_t mp = mempool_for(device);
+  if (!mp) return BMC_ERR_CUDA;
+  if (bytes == 0) return 0;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != device && cudaSetDevice(device) != cudaSuccess) return BMC_ERR_CUDA;
+  void* p = nullptr;
+  int rc = 0;
+  cudaError_t e = cudaMallocFromPoolAsync(&p, bytes, mp, 0);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    rc = BMC_ERR_OOM;
+  } else if (e != cudaSuccess || cudaFreeAsync(p, 0) != cudaSuccess ||
+             cudaStreamSynchronize(0) != cudaSuccess) {
+    rc = BMC_ERR_CUDA;
+  }
+  if (prev != device) cudaSetDevice(prev);
   return rc;
 }
 

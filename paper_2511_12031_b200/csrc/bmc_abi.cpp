@@ -1484,6 +1484,17 @@ int bmc_set_option(bmc_t h, int key, long long value) {
   }
 }
 
+int bmc_pool_reserve(int device, long long bytes) {
+  if (bytes < 0) return fail(BMC_ERR_ARG, "bytes < 0");
+  if (device < 0) {
+    cudaError_t e = cudaGetDevice(&device);
+    if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaGetDevice");
+  }
+  const int rc = bmc::pool_reserve(device, (size_t)bytes);
+  if (rc) return fail(rc, "pool_reserve(%lld bytes) failed", bytes);
+  return 0;
+}
+
 unsigned long long bmc_launch_count(void) { return bmc::launch_count(); }
 
 const char* bmc_last_error(void) { return g_err.c_str(); }

@@ -55,6 +55,8 @@ def test_argument_errors_before_cuda(lib):
         assert bmc.bmc_last_error()
     assert lib.bmc_append(None, None, None) == bmc.BMC_ERR_ARG
     assert lib.bmc_destroy(None) == bmc.BMC_ERR_ARG
+    assert lib.bmc_pool_reserve(0, ctypes.c_longlong(-5)) == bmc.BMC_ERR_ARG
+    assert lib.bmc_commit_step(None, 1, None) == bmc.BMC_ERR_ARG
     assert lib.bmc_launch_count() == 0
 
 

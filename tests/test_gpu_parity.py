@@ -73,6 +73,16 @@ def test_structured_inputs(variant):
     p.close()
 
 
+def test_pool_reserve_then_decode():
+    """bmc_pool_reserve maps memory into the growth pool up front; growths
+    afterwards are carved from it and the decode matches the oracle."""
+    assert bmc.bmc_pool_reserve(-1, 256 << 20) == 0
+    assert bmc.bmc_pool_reserve(0, 0) == 0
+    p = Pair(2, 2, 4, 128, 16, 120, dtype="bf16", seed=41)
+    _decode(p, 120, check_every=7)
+    p.close()
+
+
 @pytest.mark.parametrize("path", [1, 0])
 @pytest.mark.parametrize("ctas", [1, 2, 3, 7, 64, 500])
 def test_split_k_segments(ctas, path):
