@@ -170,6 +170,73 @@ def test_fullsize_speculative_7b():
     c.close()
 
 
+def test_fullsize_speculative_70b_long():
+    """BASELINE configs[4] (70B-long shape: B=8, 64 q / 8 kv heads, k=8 chain
+    drafts, r=256, context to 32768) through the fused bmc_spec_step the bench
+    times (keys-on-lanes tcgen05 verify, M = 8*(1+k_adm) up to 72, copy-on-read
+    growth) and bmc_commit_step, two layers; sampled (batch row, kv head)
+    units of layer 1 replayed in per-unit oracles (UPFRONT, with the GPU's
+    admitted counts: mask invariance makes the padding irrelevant)."""
+    B, Hk, Hq, D, N, r, k, L = 8, 8, 64, 128, 32768, 256, 8, 2
+    G = Hq // Hk
+    dev = torch.device("cuda")
+    cs = [bmc.KVCache(B, Hk, Hq, D, r, N, dtype="bf16") for _ in range(L)]
+    plan = bmc.StepPlan(cs)
+    g = torch.Generator(device=dev)
+    g.manual_seed(70)
+    units = [(0, 0), (7, 7), (3, 5)]
+    hist = {u: [] for u in units}
+    it = 0
+    while max(cs[0].valid()) < N - 1:
+        kk = min(k, N - max(cs[0].valid()) - 1)
+        k_adm = bmc.bmc_admissible(cs[0].h, kk)
+        t = 1 + k_adm
+        kn = [torch.randn(B, Hk, D, generator=g, device=dev).to(torch.bfloat16) for _ in range(L)]
+        vn = [torch.randn(B, Hk, D, generator=g, device=dev).to(torch.bfloat16) for _ in range(L)]
+        kd = [torch.randn(B, Hk, k, D, generator=g, device=dev).to(torch.bfloat16)
+              for _ in range(L)]
+        vd = [torch.randn(B, Hk, k, D, generator=g, device=dev).to(torch.bfloat16)
+              for _ in range(L)]
+        q = [torch.randn(B, Hq, t, D, generator=g, device=dev).to(torch.bfloat16)
+             for _ in range(L)]
+        o = [torch.empty(B, Hq, t, D, device=dev) for _ in range(L)]
+        got = bmc.bmc_spec_step(plan, plan.ptrs(kn), plan.ptrs(vn), plan.ptrs(kd), plan.ptrs(vd),
+                                kk, plan.ptrs(q), plan.ptrs(o))
+        assert got == k_adm
+        m = [min(x, k_adm) for x in synth.acceptance(13, it, B, k)]
+        sample = it % 700 == 0 or max(cs[0].valid()) > N - 20
+        for (b, h) in units:
+            hist[(b, h)].append((kn[1][b, h].cpu(), vn[1][b, h].cpu(), kd[1][b, h, :k_adm].cpu(),
+                                 vd[1][b, h, :k_adm].cpu(),
+                                 q[1][b, h * G:(h + 1) * G].cpu() if sample else None,
+                                 o[1][b, h * G:(h + 1) * G].cpu().numpy() if sample else None,
+                                 m[b]))
+        if k_adm:
+            bmc.bmc_commit_step(plan, m)
+        it += 1
+    worst, checks = 0.0, 0
+    for (b, h), ops in hist.items():
+        orc = O.Oracle(1, 1, G, D, r, N, dtype=O.BF16, policy=O.POLICY_UPFRONT)
+        for (kn_, vn_, kd_, vd_, q_, o_, mb) in ops:
+            orc.append(kn_.reshape(1, 1, D), vn_.reshape(1, 1, D))
+            ka = kd_.shape[0]
+            if ka:
+                assert orc.spec_write(kd_.reshape(1, 1, ka, D).contiguous(),
+                                      vd_.reshape(1, 1, ka, D).contiguous(), ka) == ka
+            if q_ is not None:
+                ref = orc.sdpa(q_.reshape(1, G, 1 + ka, D).contiguous(), -1)
+                worst = max(worst, float(np.abs(o_.reshape(ref.shape) - ref).max()))
+                checks += 1
+            if ka:
+                orc.commit(min(mb, ka))
+        orc.close()
+    assert checks > 20 and worst <= TOL_BF16, (checks, worst)
+    for c in cs:
+        s = c.stats()
+        assert s["alloc_events"] == math.ceil(s["valid_max"] / r) or s["capacity"] == N
+        c.close()
+
+
 @pytest.mark.parametrize("H_q,path_b", [(4, 1), (8, 0)])
 def test_decode_step_matches_per_layer_calls(H_q, path_b):
     """bmc_decode_step (fused multi-layer launch, >32 layers -> 2 launches)
