@@ -88,4 +88,36 @@ for n in range(1, 20):
 torch.cuda.synchronize()
 for c in caches:
     c.close()
+# copy-on-read growth in the CUDA-core kernel (path 1) over a multi-layer step
+caches = [bmc.KVCache(1, 2, 2, 128, 8, 32, dtype="bf16") for _ in range(3)]
+for c in caches:
+    c.set_option(bmc.BMC_OPT_ATTN_PATH, 1)
+plan = bmc.StepPlan(caches)
+for n in range(1, 20):
+    bmc.bmc_decode_step(plan, plan.ptrs(ks), plan.ptrs(ks), plan.ptrs(qs), plan.ptrs(os_), n)
+torch.cuda.synchronize()
+for c in caches:
+    c.close()
+# speculative step (G = 8, k = 8: M up to 72) with copy-on-read growth and
+# bmc_commit_step; then 4 softmax column groups (M = 32)
+for groups, Hq, k in ((0, 16, 8), (4, 8, 3)):
+    caches = [bmc.KVCache(1, 2, Hq, 128, 16, 64, dtype="bf16") for _ in range(2)]
+    for c in caches:
+        c.set_option(bmc.BMC_OPT_TCK_GROUPS, groups)
+    plan = bmc.StepPlan(caches)
+    kn = [torch.randn(1, 2, 128, device="cuda").to(torch.bfloat16) for _ in range(2)]
+    kd = [torch.randn(1, 2, k, 128, device="cuda").to(torch.bfloat16) for _ in range(2)]
+    it = 0
+    while max(caches[0].valid()) < 64 - 1 - k:
+        kad = bmc.bmc_admissible(caches[0].h, k)
+        q = [torch.randn(1, Hq, 1 + kad, 128, device="cuda").to(torch.bfloat16) for _ in range(2)]
+        o = [torch.empty(1, Hq, 1 + kad, 128, device="cuda") for _ in range(2)]
+        bmc.bmc_spec_step(plan, plan.ptrs(kn), plan.ptrs(kn), plan.ptrs(kd), plan.ptrs(kd), k,
+                          plan.ptrs(q), plan.ptrs(o))
+        if kad:
+            bmc.bmc_commit_step(plan, [it % (kad + 1)])
+        torch.cuda.synchronize()
+        it += 1
+    for c in caches:
+        c.close()
 print("sanitize target ok")
