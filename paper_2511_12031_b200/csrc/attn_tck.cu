@@ -75,9 +75,9 @@ constexpr float kRescale = 8.0f;
 // quadrant): 2 (384 threads) or 4 (640 threads: twice the warps per SMSP to
 // hide the TMEM / shared-memory / barrier latencies of large N)
 // NS <= N: query columns the softmax handles (the MMAs run N, a multiple of
-// 16).  A softmax over 72 of 80 columns at M = 72 measured no faster (the
-// tile period there is set by shared-memory traffic), so the
-// launcher always uses NS = N.
+// 16).  Softmax over 72 of 80 columns at M = 72 and over 8 of 16 at M = 1
+// measured no faster (same-box A/Bs: the M = 72 tile period is set by
+// shared-memory traffic, M = 1 is HBM-bound), so the launcher uses NS = N.
 template <int N, int NG, int NS = N>
 struct Cfg {
   static_assert(N % 16 == 0 && N >= 16 && N <= 80, "query columns");
