@@ -7,6 +7,8 @@ shares no code with it (see oracle/oracle.h for what it computes and the
 PAPER.md passages each function follows).
 
 Parity status: every function is pinned by ``tests/test_oracle_pins.py``
+(incl. the ITERATIVE+SD exact-size ledger and kv_bytes_read closed forms;
+``tools/mutate_oracle.sh`` checks that 11 plausible mutations each fail a pin)
 (closed forms P:L392/L410/L437, the SD worked example P:L863-866, brute-force
 SDPA, fp64 torch SDPA, GQA replication, policy degeneracy).  No function is
 "parity unpinned".

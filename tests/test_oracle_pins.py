@@ -646,3 +646,136 @@ def test_append_n_errors(oracle_mod):
     with pytest.raises(O.OracleError) as e:
         orc.append_n(K3, V3, 3)
     assert e.value.code == -2
+
+
+# ------------------------------------------- ITERATIVE with speculation (R17)
+
+def _iter_sd_run(P, I, k, m, *, B=2, H=2, d=4, N=256, sdpa=False, check=None):
+    """Prompt of P single appends, then I speculative iterations under the
+    ITERATIVE policy: append x_last, spec_write k drafts, (SDPA), commit m."""
+    orc = O.Oracle(B, H, H, d, 1, N, dtype=O.F32, policy=O.POLICY_ITERATIVE)
+    for n in range(P):
+        x = synth.step_inputs(41, 0, n, B=B, H_kv=H, H_q=H, D=d, dtype="f32")
+        orc.append(x["k"], x["v"])
+        if check:
+            check("append", orc.stats())
+    for i in range(I):
+        x = synth.step_inputs(41, 0, 1000 + i, B=B, H_kv=H, H_q=H, D=d, dtype="f32")
+        orc.append(x["k"], x["v"])
+        if check:
+            check("append", orc.stats())
+        xd = synth.step_inputs(41, 0, 2000 + i, B=B, H_kv=H, H_q=H, D=d, k_draft=k,
+                               t=1 + k, dtype="f32")
+        ka = orc.spec_write(xd["kd"], xd["vd"], k)
+        if check:
+            check("spec", orc.stats())
+        if sdpa:
+            orc.sdpa(xd["q"][:, :, :1 + ka].contiguous(), orc.stats()["valid_max"])
+        orc.commit(min(m, ka))
+        if check:
+            check("commit", orc.stats())
+    return orc
+
+
+def test_iterative_sd_buffers_are_exact_size(oracle_mod):
+    """P:L340 ("copies them into the new K and V matrices (size increased by one
+    additional row)") and the update_cache listing P:L352-359 (allocate, then
+    concat the new block): an iterative buffer never holds a padded row.  So
+    after an append the capacity is the committed length, after a speculative
+    write it is the committed length plus the drafts, and a commit that
+    rejects drafts leaves them as zero rows that the next append drops
+    (reading R17).  Each reallocation copies exactly the rows that hold data
+    (valid_max before the call)."""
+    prev = {}
+
+    def check(what, s):
+        if what == "append":
+            assert s["capacity"] == s["valid_max"], s
+        elif what == "spec":
+            assert s["capacity"] == s["valid_max"] + s["staged"], s
+        else:
+            assert s["staged"] == 0 and s["capacity"] == prev["capacity"], s
+        if what != "commit":
+            # one new allocation per call; it copies the rows that held data
+            assert s["alloc_events"] == prev.get("alloc_events", 0) + 1
+            moved = (s["copied_bytes"] - prev.get("copied_bytes", 0)) // (2 * 2 * 2 * 4 * 4)
+            assert moved == prev.get("valid_max", 0), (what, moved, prev)
+        prev.update(s)
+
+    _iter_sd_run(P=5, I=9, k=4, m=2, check=check)
+    prev.clear()
+    _iter_sd_run(P=1, I=6, k=3, m=0, check=check)
+
+
+@pytest.mark.parametrize("P,I,k,m", [(5, 9, 4, 2), (1, 7, 3, 3), (12, 4, 8, 0), (3, 10, 1, 1)])
+def test_iterative_sd_ledger_closed_form(oracle_mod, P, I, k, m):
+    """HF-concat growth under speculation (reading R17), summed by
+    hand.  Prompt: P appends copy sum_{n<P} n = P(P-1)/2 rows and write
+    sum_{n<=P} n = P(P+1)/2 rows per unit.  Iteration i starts at
+    v_i = P + i(1+m): the append copies v_i rows into v_i+1, the speculative
+    write copies v_i+1 rows into v_i+1+k, so over I iterations the copies are
+    I(2P+1) + (1+m)I(I-1) rows and the initialised rows I(2P+2+k) + (1+m)I(I-1);
+    2 allocations per iteration; the final capacity is v_{I-1}+1+k and the
+    valid length P + I(1+m).  Each iteration's verify SDPA streams all
+    v_i+1+k rows (S 8(d)): sum = I(P+1+k) + (1+m)I(I-1)/2 rows.
+    MACs: 2*B*H_q*t*cap*D per call with t = 1+k."""
+    B, H, d = 2, 2, 4
+    orc = _iter_sd_run(P, I, k, m, B=B, H=H, d=d, sdpa=True)
+    s = orc.stats()
+    row = 2 * B * H * d * 4                       # K and V, all units, fp32
+    assert s["alloc_events"] == P + 2 * I
+    assert s["copy_events"] == (P - 1) + 2 * I
+    assert s["copied_bytes"] == row * (P * (P - 1) // 2 + I * (2 * P + 1) + (1 + m) * I * (I - 1))
+    assert s["init_written_bytes"] == row * (P * (P + 1) // 2 + I * (2 * P + 2 + k)
+                                             + (1 + m) * I * (I - 1))
+    assert s["valid_max"] == s["valid_min"] == P + I * (1 + m)
+    assert s["capacity"] == P + (I - 1) * (1 + m) + 1 + k
+    rows_read = I * (P + 1 + k) + (1 + m) * I * (I - 1) // 2
+    assert s["kv_bytes_read"] == row * rows_read
+    assert s["macs"] == 2 * B * H * (1 + k) * rows_read * d
+
+
+def test_iterative_sd_matches_bmc_sd(oracle_mod):
+    """Reading R17 vs P:L864-869: with room for every draft, ITERATIVE and
+    BMC speculation hold the same committed rows and give bit-identical fp64
+    outputs (mask invariance); only the ledger differs."""
+    B, H, d, k = 2, 2, 4, 3
+    it = O.Oracle(B, H, H, d, 1, 128, dtype=O.BF16, policy=O.POLICY_ITERATIVE)
+    bm = O.Oracle(B, H, H, d, 64, 128, dtype=O.BF16, policy=O.POLICY_BMC)
+    for i, m in enumerate([2, 0, 3, 1, 3]):
+        x = synth.step_inputs(43, 0, i, B=B, H_kv=H, H_q=H, D=d, dtype="bf16")
+        xd = synth.step_inputs(43, 0, 100 + i, B=B, H_kv=H, H_q=H, D=d, k_draft=k, t=1 + k,
+                               dtype="bf16")
+        outs = []
+        for orc in (it, bm):
+            orc.append(x["k"], x["v"])
+            assert orc.spec_write(xd["kd"], xd["vd"], k) == k
+            outs.append(orc.sdpa(xd["q"], orc.stats()["valid_max"]))
+            orc.commit(m)
+        assert np.array_equal(outs[0], outs[1])
+    n = it.stats()["valid_max"]
+    assert bm.stats()["valid_max"] == n
+    Ki, Vi = it.read_cache()
+    Kb, Vb = bm.read_cache()
+    assert np.array_equal(Ki[:, :n], Kb[:, :n]) and np.array_equal(Vi[:, :n], Vb[:, :n])
+
+
+@pytest.mark.parametrize("N,r", [(32, 4), (40, 8), (30, 7)])
+def test_kv_bytes_read_closed_form(oracle_mod, N, r):
+    """SURVEY 8(d) algorithmic bytes: every SDPA streams K and V over all cap
+    rows, padding included ("wasteful computation" of the zero rows).
+    Decoding N tokens reads 2*U*D*eb * sum_n cap(n) bytes with
+    cap(n) = min(r*ceil(n/r), N) (BMC), n (ITERATIVE), N (UPFRONT); for r | N the
+    BMC sum is N(N+r)/2 rows."""
+    B, H, d = 1, 2, 2
+    row = 2 * B * H * d * 4
+    bm, _ = _run_decode(O.POLICY_BMC, B=B, H_kv=H, H_q=H, D=d, N=N, r=r)
+    assert bm.stats()["kv_bytes_read"] == row * sum(min(r * math.ceil(n / r), N)
+                                                    for n in range(1, N + 1))
+    if N % r == 0:
+        assert bm.stats()["kv_bytes_read"] == row * N * (N + r) // 2
+    it, _ = _run_decode(O.POLICY_ITERATIVE, B=B, H_kv=H, H_q=H, D=d, N=N, r=1)
+    assert it.stats()["kv_bytes_read"] == row * N * (N + 1) // 2
+    up, _ = _run_decode(O.POLICY_UPFRONT, B=B, H_kv=H, H_q=H, D=d, N=N, r=N)
+    assert up.stats()["kv_bytes_read"] == row * N * N
+    assert bm.stats()["sdpa_calls"] == it.stats()["sdpa_calls"] == N
