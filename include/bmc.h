@@ -111,7 +111,12 @@ int bmc_admissible(bmc_t h, int k);
    bmc_spec_write); Q[l] DEVICE [B][H_q][t][D] and O[l] DEVICE
    [B][H_q][t][D] fp32 with t = 1 + bmc_admissible(hs[l], k) (every layer
    admits the same number).  Returns k_adm >= 0, or an error before anything
-   is enqueued (ARG, STATE, CAPACITY).  Commit afterwards with bmc_commit_step
+   is enqueued (ARG, STATE, CAPACITY, UNSUPPORTED; workspaces are allocated
+   for every layer before any layer changes).  OOM on a growth allocation:
+   the layers of the 32-layer chunks already launched (layers < 32c) have
+   taken the step, every other layer is rolled back to its state before the
+   call (a growth it completed stays: the retried step does not grow it
+   again); bmc_valid tells the two apart.  Commit afterwards with bmc_commit_step
    (or per layer with bmc_commit / bmc_commit_rows).
    All-host form (the end-to-end call): when every K, V, Q, O (and Kd, Vd for
    k > 0) is a HOST pointer (pinned for asynchrony), the arguments are staged
@@ -195,6 +200,8 @@ int bmc_commit_path(bmc_t h, const int* path_host, const int* m_host, int max_de
    bmc_sdpa(hs[l], Q[l], n_valid, O[l]) (n_valid = the committed length AFTER
    the append, or BMC_PER_ROW).  Arrays of L pointers.  Every layer is
    validated before anything is enqueued.  One call instead of 2L.
+   OOM on a growth allocation: as bmc_spec_step (the chunks already
+   launched have stepped, the other layers are rolled back).
    When every K, V, Q and O is a HOST pointer the step is pipelined: the
    inputs are staged on an internal copy stream (double-buffered, so the copy
    of step s+1 overlaps the kernels of step s) and the outputs are copied back
@@ -256,13 +263,18 @@ int bmc_sync(bmc_t h);
      6 BMC_OPT_TCK_GROUPS     softmax column groups of the keys-on-lanes
                               tcgen05 kernel: 0 auto (4 for 16 < G*t <= 64,
                               else 2), 2 (384 threads), 4 (640 threads).  Tuning /
-                              A/B only; results agree within the tolerance. */
+                              A/B only; results agree within the tolerance.
+     7 BMC_OPT_FAULT_OOM      fault injection for tests: the next `value`
+                              growth allocations of this handle fail with
+                              BMC_ERR_OOM (exercises the fused steps' OOM
+                              fallback and rollback). */
 #define BMC_OPT_ATTN_CTAS 1
 #define BMC_OPT_ATTN_PATH 2
 #define BMC_OPT_ARENA 3
 #define BMC_OPT_SKIP_PADDING 4
 #define BMC_OPT_COPY_ON_READ 5
 #define BMC_OPT_TCK_GROUPS 6
+#define BMC_OPT_FAULT_OOM 7
 int bmc_set_option(bmc_t h, int key, long long value);
 
 /* bmc_pool_reserve: map `bytes` of device memory into the library's

@@ -52,6 +52,7 @@ struct bmc_ctx {
   int skip_padding = 0;          // length-aware ablation, off by default
   int copy_on_read = 1;          // BMC growth inside the fused decode step
   int tck_groups = 0;            // keys-on-lanes kernel softmax column groups (0 auto)
+  int fault_oom = 0;             // test hook: the next n growth allocations fail (BMC_OPT_FAULT_OOM)
   // a growth whose copy the next attention launch performs (copy-on-read):
   // the old buffers and the rows to carry over; never observable between API
   // calls (bmc_decode_step launches the consuming kernel in the same call)
@@ -289,6 +290,10 @@ static int reallocate(bmc_t h, long long new_cap, long long copy_rows, bool defe
   if (h->cor) {
     int rc = cor_materialize(h);
     if (rc) return rc;
+  }
+  if (h->fault_oom > 0) {
+    --h->fault_oom;
+    return fail(BMC_ERR_OOM, "injected allocation failure (BMC_OPT_FAULT_OOM)");
   }
   const size_t bytes = (size_t)h->U * new_cap * h->row_bytes;
   Buffer nk, nv;
@@ -562,6 +567,61 @@ static int append_fused(const bmc_t* hs, int l0, int l, const void* K, const voi
     rc = append_impl(hs[l], K, V, false);
   }
   return rc;
+}
+
+// Undo what append_impl (appended) and spec_write_impl did to a layer whose
+// attention launch has not been enqueued, after an error later in a fused
+// step: a deferred growth is carried out (the new capacity stays, so the
+// retried step does not grow again and the ledger totals match an
+// uninterrupted run), the lengths and the recorded rows are rolled back.
+static void undo_layer_step(bmc_t h, bool appended) {
+  cor_materialize(h);
+  h->st.append_written_bytes -= 2LL * h->U * h->n_draft * h->row_bytes;
+  h->n_draft = 0;
+  h->staged = 0;
+  h->kd = h->vd = nullptr;
+  if (appended) {
+    for (auto& v : h->valid) v -= 1;
+    h->st.append_written_bytes -= 2LL * h->U * h->row_bytes;
+    h->n_app = 0;
+    h->knew = h->vnew = nullptr;
+  }
+  inputs_consumed(h);
+}
+
+// Roll back layers [l0, l_end) of the chunk being built (layers < n_appended
+// had their append done) and keep the first error message.
+static int rollback_chunk(const bmc_t* hs, int l0, int l_end, int n_appended, int rc) {
+  const std::string msg = g_err;
+  for (int x = l0; x < l_end; ++x) undo_layer_step(hs[x], x < n_appended);
+  g_err = msg;
+  return rc;
+}
+
+// One chunk's keys-on-lanes launch: all layers in one launch when they agree
+// on capacity, copy-on-read state and pending rows (the usual case: one r,
+// one step sequence), else one launch per layer (e.g. after an OOM fallback
+// carried some layers' growths out with the realloc kernel).
+static int launch_tck_chunk(bmc_t h0, const bmc::AttnStepArgs& a, bmc::AttnLayer* layers, int nl) {
+  bool same = true;
+  for (int l = 1; l < nl; ++l)
+    if (layers[l].cap != layers[0].cap || layers[l].scan != layers[0].scan ||
+        (layers[l].Ksrc != nullptr) != (layers[0].Ksrc != nullptr) ||
+        layers[l].cap_src != layers[0].cap_src || layers[l].rows_src != layers[0].rows_src ||
+        layers[l].n_app != layers[0].n_app || layers[l].n_draft != layers[0].n_draft ||
+        layers[l].kd_stride != layers[0].kd_stride)
+      same = false;
+  if (same) {
+    CK(h0, bmc::launch_attn_tck(a, h0->num_sms, h0->stream), "attn_tck");
+    return 0;
+  }
+  for (int l = 0; l < nl; ++l) {
+    bmc::AttnStepArgs a1 = a;
+    a1.L = 1;
+    a1.layers = &layers[l];
+    CK(h0, bmc::launch_attn_tck(a1, h0->num_sms, h0->stream), "attn_tck");
+  }
+  return 0;
 }
 
 int bmc_append(bmc_t h, const void* K, const void* V) {
@@ -847,14 +907,33 @@ int bmc_spec_step(const bmc_t* hs, int L, const void* const* K, const void* cons
                   (h0->attn_path == 0 && M > kTcMinM && bmc::attn_tc_supported(h0->D, h0->dt, M));
   const bool tck = tc && h0->attn_path != 3 && bmc::attn_tck_supported(h0->D, h0->dt, M);
   if (tc && !tck) fused = false;
+  // everything that can fail without touching device memory is checked on
+  // every layer before any layer is mutated
+  for (int l = 0; l < L; ++l) {
+    const bmc_t h = hs[l];
+    const int Ml = (h->H_q / h->H_kv) * t;
+    const bool tcl = h->attn_path >= 2 ||
+                     (h->attn_path == 0 && Ml > kTcMinM && bmc::attn_tc_supported(h->D, h->dt, Ml));
+    if (h->attn_path == 4 && !bmc::attn_tck_supported(h->D, h->dt, Ml))
+      return fail(BMC_ERR_UNSUPPORTED, "layer %d: keys-on-lanes tcgen05 path needs bf16, D=128, G*t<=80", l);
+    if (tcl && !bmc::attn_tc_supported(h->D, h->dt, Ml))
+      return fail(BMC_ERR_UNSUPPORTED, "layer %d: tcgen05 path needs bf16, D=128, G*t<=128", l);
+    if (tcl) {
+      int rc = ensure_workspace(h, Ml);
+      if (rc) return rc;
+    }
+  }
   if (!fused) {
+    // appends and drafts of every layer, then the launches: an error in the
+    // first loop rolls the layers back (nothing launched yet)
     for (int l = 0; l < L; ++l) {
       int rc = append_impl(hs[l], K[l], V[l]);
+      if (rc) return rollback_chunk(hs, 0, l, l, rc);
       if (!rc && k > 0) {
         rc = spec_write_impl(hs[l], Kd[l], Vd[l], k);
         if (rc > 0) rc = 0;
       }
-      if (rc) return rc;
+      if (rc) return rollback_chunk(hs, 0, l + 1, l + 1, rc);
     }
     for (int l = 0; l < L; ++l) {
       int rc = launch_sdpa_layer(hs[l], Q[l], O[l], t);
@@ -871,24 +950,23 @@ int bmc_spec_step(const bmc_t* hs, int L, const void* const* K, const void* cons
     for (int l = l0; l < l0 + nl; ++l) {
       const bool defer = hs[l]->copy_on_read && !hs[l]->skip_padding;
       int rc = append_fused(hs, l0, l, K[l], V[l], defer);
-      if (!rc && k > 0) {
+      if (rc) return rollback_chunk(hs, l0, l, l, rc);
+      if (k > 0) {
         rc = spec_write_impl(hs[l], Kd[l], Vd[l], k);
-        if (rc > 0) rc = 0;
+        if (rc < 0) return rollback_chunk(hs, l0, l + 1, l + 1, rc);
       }
-      if (!rc && tck) rc = ensure_workspace(hs[l], M);
-      if (rc) {
-        for (int x = l0; x <= l; ++x) cor_materialize(hs[x]);
-        return rc;
-      }
-      fill_layer(hs[l], Q[l], O[l], &layers[l]);
     }
+    // descriptors only after every append of the chunk: an OOM fallback in
+    // append_fused may have carried out earlier layers' deferred growths
+    for (int l = l0; l < l0 + nl; ++l) fill_layer(hs[l], Q[l], O[l], &layers[l]);
     bmc::AttnStepArgs a;
     fill_args(hs[l0], t, &a);
     a.L = nl;
     a.layers = &layers[l0];
     if (tck) {
       a.ctas = std::min(h0->attn_ctas, h0->num_sms);
-      CK(h0, bmc::launch_attn_tck(a, h0->num_sms, h0->stream), "attn_tck");
+      int rc = launch_tck_chunk(h0, a, &layers[l0], nl);
+      if (rc) return rc;
     } else {
       CK(h0, bmc::launch_attn_step(a, h0->num_sms, h0->stream), "attn_step");
     }
@@ -957,6 +1035,11 @@ int bmc_decode_step(const bmc_t* hs, int L, const void* const* K, const void* co
   for (int l = 1; l < L && tck; ++l)
     if (hs[l]->attn_path != h0->attn_path) fused = false;
   if (tc && !tck) fused = false;
+  if (fused && tck)   // workspaces before any layer is mutated
+    for (int l = 0; l < L; ++l) {
+      int rc = ensure_workspace(hs[l], G);
+      if (rc) return rc;
+    }
   if (!fused) {
     for (int l = 0; l < L; ++l) {
       int rc = bmc_append(hs[l], K[l], V[l]);
@@ -977,37 +1060,19 @@ int bmc_decode_step(const bmc_t* hs, int L, const void* const* K, const void* co
       // all cap rows streamed)
       const bool defer = hs[l]->copy_on_read && !hs[l]->skip_padding;
       int rc = append_fused(hs, l0, l, K[l], V[l], defer);
-      if (!rc && tck) rc = ensure_workspace(hs[l], G);
-      if (rc) {
-        for (int x = l0; x <= l; ++x) cor_materialize(hs[x]);
-        return rc;
-      }
-      fill_layer(hs[l], Q[l], O[l], &layers[l]);
+      if (rc) return rollback_chunk(hs, l0, l, l, rc);
     }
+    // descriptors only after every append of the chunk: an OOM fallback in
+    // append_fused may have carried out earlier layers' deferred growths
+    for (int l = l0; l < l0 + nl; ++l) fill_layer(hs[l], Q[l], O[l], &layers[l]);
     bmc::AttnStepArgs a;
     fill_args(hs[l0], 1, &a);
     a.L = nl;
     a.layers = &layers[l0];
     if (tck) {
-      // one launch for the chunk when every layer has the same capacity (the
-      // usual case: one r, one step sequence); else one launch per layer
-      bool same = true;
-      for (int l = l0 + 1; l < l0 + nl; ++l)
-        if (layers[l].cap != layers[l0].cap || layers[l].scan != layers[l0].scan ||
-            (layers[l].Ksrc != nullptr) != (layers[l0].Ksrc != nullptr) ||
-            layers[l].cap_src != layers[l0].cap_src)
-          same = false;
       a.ctas = std::min(h0->attn_ctas, h0->num_sms);
-      if (same) {
-        CK(h0, bmc::launch_attn_tck(a, h0->num_sms, h0->stream), "attn_tck");
-      } else {
-        for (int l = l0; l < l0 + nl; ++l) {
-          bmc::AttnStepArgs a1 = a;
-          a1.L = 1;
-          a1.layers = &layers[l];
-          CK(h0, bmc::launch_attn_tck(a1, h0->num_sms, h0->stream), "attn_tck");
-        }
-      }
+      int rc = launch_tck_chunk(h0, a, &layers[l0], nl);
+      if (rc) return rc;
     } else {
       CK(hs[0], bmc::launch_attn_step(a, hs[0]->num_sms, hs[0]->stream), "attn_step");
     }
@@ -1478,6 +1543,10 @@ int bmc_set_option(bmc_t h, int key, long long value) {
     case BMC_OPT_TCK_GROUPS:
       if (value != 0 && value != 2 && value != 4) return fail(BMC_ERR_ARG, "tck groups");
       h->tck_groups = (int)value;
+      return 0;
+    case BMC_OPT_FAULT_OOM:
+      if (value < 0 || value > 1000000) return fail(BMC_ERR_ARG, "fault count");
+      h->fault_oom = (int)value;
       return 0;
     default:
       return fail(BMC_ERR_ARG, "unknown option %d", key);

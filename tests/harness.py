@@ -162,3 +162,116 @@ class Pair:
         self.drain()
         self.gpu.close()
         self.orc.close()
+
+
+class Model:
+    """L layers stepped together through the fused C-ABI calls
+    (bmc_decode_step / bmc_spec_step / bmc_commit_step, the calls bench.py
+    times), each layer in lock-step with its own oracle on the same seeded
+    inputs.  check: compare every layer's outputs (else only `check_layers`)."""
+
+    def __init__(self, L, B, H_kv, H_q, D, r, N, dtype="bf16", policy="bmc", seed=5,
+                 check_layers=None, options=()):
+        self.L, self.B, self.H_kv, self.H_q, self.D = L, B, H_kv, H_q, D
+        self.dtype, self.seed = dtype, seed
+        self.gpu = [bmc.KVCache(B, H_kv, H_q, D, r, N, dtype=dtype, policy=policy)
+                    for _ in range(L)]
+        for c in self.gpu:
+            for key, val in options:
+                c.set_option(key, val)
+        pol = {"bmc": O.POLICY_BMC, "iterative": O.POLICY_ITERATIVE,
+               "upfront": O.POLICY_UPFRONT}[policy]
+        self.orc = [O.Oracle(B, H_kv, H_q, D, r, N, dtype=O.F32 if dtype == "f32" else O.BF16,
+                             policy=pol) for _ in range(L)]
+        self.plan = bmc.StepPlan(self.gpu)
+        self.check_layers = range(L) if check_layers is None else check_layers
+        self.step = 0
+        self.worst = 0.0
+        self.keep = []
+
+    def _inputs(self, t, k):
+        xs = [synth.step_inputs(self.seed, l, self.step, B=self.B, H_kv=self.H_kv,
+                                H_q=self.H_q, D=self.D, t=t, k_draft=k, dtype=self.dtype)
+              for l in range(self.L)]
+        self.step += 1
+        return xs
+
+    def _compare(self, outs, refs):
+        for l in self.check_layers:
+            e = err_of(outs[l].cpu().numpy(), refs[l], self.dtype)
+            self.worst = max(self.worst, e)
+            assert e <= 1.0, f"layer {l} step {self.step}: {e:.3f} x tolerance"
+
+    def decode_step(self, check=True):
+        xs = self._inputs(1, 0)
+        n = self.orc[0].stats()["valid_max"] + 1
+        dev = [{k: v.cuda() for k, v in x.items()} for x in xs]
+        outs = [torch.empty(self.B, self.H_q, 1, self.D, device="cuda") for _ in range(self.L)]
+        p = self.plan
+        bmc.bmc_decode_step(p, p.ptrs([d["k"] for d in dev]), p.ptrs([d["v"] for d in dev]),
+                            p.ptrs([d["q"] for d in dev]), p.ptrs(outs), n)
+        self.keep = dev
+        refs = []
+        for l in range(self.L):
+            self.orc[l].append(xs[l]["k"], xs[l]["v"])
+            refs.append(self.orc[l].sdpa(xs[l]["q"], n) if check else None)
+        if check:
+            torch.cuda.synchronize()
+            self._compare(outs, refs)
+        return outs
+
+    def spec_step(self, k, check=True):
+        """One speculative iteration (append + k chain drafts + verify) of
+        every layer; returns k_adm."""
+        k_adm = bmc.bmc_admissible(self.gpu[0].h, k)
+        t = 1 + k_adm
+        xs = self._inputs(t, max(k, 1))
+        dev = [{key: v.cuda() for key, v in x.items()} for x in xs]
+        outs = [torch.empty(self.B, self.H_q, t, self.D, device="cuda") for _ in range(self.L)]
+        p = self.plan
+        got = bmc.bmc_spec_step(p, p.ptrs([d["k"] for d in dev]), p.ptrs([d["v"] for d in dev]),
+                                p.ptrs([d["kd"] for d in dev]), p.ptrs([d["vd"] for d in dev]),
+                                k, p.ptrs([d["q"] for d in dev]), p.ptrs(outs))
+        assert got == k_adm, (got, k_adm)
+        self.keep = dev
+        refs = []
+        for l in range(self.L):
+            o = self.orc[l]
+            o.append(xs[l]["k"], xs[l]["v"])
+            if k > 0:
+                assert o.spec_write(xs[l]["kd"], xs[l]["vd"], k) == k_adm
+            st = o.stats()
+            nv = st["valid_max"] if st["valid_min"] == st["valid_max"] else -1
+            refs.append(o.sdpa(xs[l]["q"], nv) if check else None)
+        if check:
+            torch.cuda.synchronize()
+            self._compare(outs, refs)
+        return k_adm
+
+    def commit_step(self, m):
+        bmc.bmc_commit_step(self.plan, m)
+        for o in self.orc:
+            o.commit_rows(m)
+
+    def check_state(self, layers=None):
+        torch.cuda.synchronize()
+        for l in (range(self.L) if layers is None else layers):
+            sg, so = self.gpu[l].stats(), self.orc[l].stats()
+            for key in STAT_KEYS:
+                assert sg[key] == so[key], (l, key, sg[key], so[key])
+            assert self.gpu[l].valid() == list(self.orc[l].valid())
+            Kg, Vg = self.gpu[l].kv()
+            Ko, Vo = self.orc[l].read_cache()
+            if self.dtype == "bf16":
+                kg = Kg.cpu().view(torch.int16).numpy().view(np.uint16)
+                vg = Vg.cpu().view(torch.int16).numpy().view(np.uint16)
+            else:
+                kg, vg = Kg.cpu().numpy().view(np.uint32), Vg.cpu().numpy().view(np.uint32)
+                Ko, Vo = Ko.view(np.uint32), Vo.view(np.uint32)
+            assert np.array_equal(kg, Ko) and np.array_equal(vg, Vo), f"layer {l} cache differs"
+
+    def close(self):
+        for c in self.gpu:
+            c.close()
+        for o in self.orc:
+            o.close()
