@@ -188,6 +188,10 @@ class Model:
         self.step = 0
         self.worst = 0.0
         self.keep = []
+        # SDPA ledger of every call (the oracle runs SDPA only on checked steps):
+        # per layer K+V bytes of all cap rows, MACs 2*B*H_q*t*cap*D, calls
+        self.sdpa_ledger = [dict(kv_bytes_read=0, macs=0, sdpa_calls=0) for _ in range(L)]
+        self.eb = 4 if dtype == "f32" else 2
 
     def _inputs(self, t, k):
         xs = [synth.step_inputs(self.seed, l, self.step, B=self.B, H_kv=self.H_kv,
@@ -195,6 +199,13 @@ class Model:
               for l in range(self.L)]
         self.step += 1
         return xs
+
+    def _account(self, l, t):
+        st = self.orc[l].stats()
+        led = self.sdpa_ledger[l]
+        led["kv_bytes_read"] += 2 * self.B * self.H_kv * st["capacity"] * self.D * self.eb
+        led["macs"] += 2 * self.B * self.H_q * t * st["capacity"] * self.D
+        led["sdpa_calls"] += 1
 
     def _compare(self, outs, refs):
         for l in self.check_layers:
@@ -204,7 +215,8 @@ class Model:
 
     def decode_step(self, check=True):
         xs = self._inputs(1, 0)
-        n = self.orc[0].stats()["valid_max"] + 1
+        st = self.orc[0].stats()
+        n = st["valid_max"] + 1 if st["valid_min"] == st["valid_max"] else -1   # BMC_PER_ROW
         dev = [{k: v.cuda() for k, v in x.items()} for x in xs]
         outs = [torch.empty(self.B, self.H_q, 1, self.D, device="cuda") for _ in range(self.L)]
         p = self.plan
@@ -214,6 +226,7 @@ class Model:
         refs = []
         for l in range(self.L):
             self.orc[l].append(xs[l]["k"], xs[l]["v"])
+            self._account(l, 1)
             refs.append(self.orc[l].sdpa(xs[l]["q"], n) if check else None)
         if check:
             torch.cuda.synchronize()
@@ -241,6 +254,7 @@ class Model:
             if k > 0:
                 assert o.spec_write(xs[l]["kd"], xs[l]["vd"], k) == k_adm
             st = o.stats()
+            self._account(l, t)
             nv = st["valid_max"] if st["valid_min"] == st["valid_max"] else -1
             refs.append(o.sdpa(xs[l]["q"], nv) if check else None)
         if check:
@@ -257,6 +271,7 @@ class Model:
         torch.cuda.synchronize()
         for l in (range(self.L) if layers is None else layers):
             sg, so = self.gpu[l].stats(), self.orc[l].stats()
+            so.update(self.sdpa_ledger[l])
             for key in STAT_KEYS:
                 assert sg[key] == so[key], (l, key, sg[key], so[key])
             assert self.gpu[l].valid() == list(self.orc[l].valid())

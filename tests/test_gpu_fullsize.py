@@ -131,8 +131,8 @@ def test_fullsize_speculative_7b():
         vn = torch.randn(B, H, D, generator=g, device=dev).to(torch.bfloat16)
         c.append(kn, vn)
         kk = min(k, N - max(c.valid()))
-        kd = torch.randn(B, H, k, D, generator=g, device=dev).to(torch.bfloat16)
-        vd = torch.randn(B, H, k, D, generator=g, device=dev).to(torch.bfloat16)
+        kd = torch.randn(B, H, max(kk, 1), D, generator=g, device=dev).to(torch.bfloat16)
+        vd = torch.randn(B, H, max(kk, 1), D, generator=g, device=dev).to(torch.bfloat16)
         k_adm = c.spec_write(kd, vd, kk) if kk > 0 else 0
         t = 1 + k_adm
         q = torch.randn(B, H, t, D, generator=g, device=dev).to(torch.bfloat16)
@@ -193,9 +193,10 @@ def test_fullsize_speculative_70b_long():
         t = 1 + k_adm
         kn = [torch.randn(B, Hk, D, generator=g, device=dev).to(torch.bfloat16) for _ in range(L)]
         vn = [torch.randn(B, Hk, D, generator=g, device=dev).to(torch.bfloat16) for _ in range(L)]
-        kd = [torch.randn(B, Hk, k, D, generator=g, device=dev).to(torch.bfloat16)
+        # drafts [B][H_kv][kk][D]: the library reads the k it is given
+        kd = [torch.randn(B, Hk, max(kk, 1), D, generator=g, device=dev).to(torch.bfloat16)
               for _ in range(L)]
-        vd = [torch.randn(B, Hk, k, D, generator=g, device=dev).to(torch.bfloat16)
+        vd = [torch.randn(B, Hk, max(kk, 1), D, generator=g, device=dev).to(torch.bfloat16)
               for _ in range(L)]
         q = [torch.randn(B, Hq, t, D, generator=g, device=dev).to(torch.bfloat16)
              for _ in range(L)]

@@ -101,8 +101,8 @@ def test_baselines_speculative_7b_fullsize(policy):
         t = 1 + k_adm
         kn = torch.randn(B, H, D, generator=g, device=dev).to(torch.bfloat16)
         vn = torch.randn(B, H, D, generator=g, device=dev).to(torch.bfloat16)
-        kd = torch.randn(B, H, k, D, generator=g, device=dev).to(torch.bfloat16)
-        vd = torch.randn(B, H, k, D, generator=g, device=dev).to(torch.bfloat16)
+        kd = torch.randn(B, H, max(kk, 1), D, generator=g, device=dev).to(torch.bfloat16)
+        vd = torch.randn(B, H, max(kk, 1), D, generator=g, device=dev).to(torch.bfloat16)
         q = torch.randn(B, H, t, D, generator=g, device=dev).to(torch.bfloat16)
         o = torch.empty(B, H, t, D, device=dev)
         v0 = c.valid()
