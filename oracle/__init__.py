@@ -88,6 +88,15 @@ def lib():
     return _lib
 
 
+def set_threads(n: int) -> None:
+    """OpenMP threads of the oracle's SDPA loop (the libgomp the oracle
+    library loaded; used for bench.py's all-cores and single-core timings)."""
+    lib()
+    import ctypes.util
+    name = ctypes.util.find_library("gomp") or "libgomp.so.1"
+    ctypes.CDLL(name).omp_set_num_threads(int(max(1, n)))
+
+
 def _raw(x, dtype: int) -> np.ndarray:
     """Contiguous raw element bits: fp32 -> float32, bf16 -> uint16 bit patterns.
 

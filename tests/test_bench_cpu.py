@@ -23,7 +23,12 @@ def test_reference_arm_json_line():
     assert d["value"] > 0 and d["unit"] == "tokens/s" and d["higher_is_better"] is True
     assert d["n_gpus"] == 1 and d["steps"] == 1 and d["warmup"] == 0 and d["ms_per_step"] > 0
     assert d["config"]["workload"].startswith("toy")
+    assert d["scaling"] == "strong"
+    for key in ("global_batch", "layers", "H_q", "H_kv", "head_dim", "N_max", "r", "policy",
+                "parallelism"):
+        assert key in d["config"], key
     cb = d["cpu_baseline"]
+    assert cb["host"]["nproc"] >= 1 and "cpu_model" in cb["host"]
     assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["sample"] and cb["value"] == d["value"]
     e2e = d["e2e"]
     assert e2e["value"] == d["value"] and e2e["h2d_bytes_per_step"] == 0
