@@ -264,6 +264,10 @@ int bmc_sync(bmc_t h);
                               tcgen05 kernel: 0 auto (4 for 16 < G*t <= 64,
                               else 2), 2 (384 threads), 4 (640 threads).  Tuning /
                               A/B only; results agree within the tolerance.
+     8 BMC_OPT_TCK_PREFETCH   L2 prefetch distance of the keys-on-lanes kernel's
+                              K / V producers, in 128-key tiles ahead of the
+                              shared-memory ring (-1 auto, 0 off).  Tuning /
+                              A/B only; results are identical.
      7 BMC_OPT_FAULT_OOM      fault injection for tests: the next `value`
                               growth allocations of this handle fail with
                               BMC_ERR_OOM (exercises the fused steps' OOM
@@ -275,6 +279,7 @@ int bmc_sync(bmc_t h);
 #define BMC_OPT_COPY_ON_READ 5
 #define BMC_OPT_TCK_GROUPS 6
 #define BMC_OPT_FAULT_OOM 7
+#define BMC_OPT_TCK_PREFETCH 8
 int bmc_set_option(bmc_t h, int key, long long value);
 
 /* bmc_pool_reserve: map `bytes` of device memory into the library's

@@ -29,6 +29,7 @@ BMC_OPT_ATTN_CTAS, BMC_OPT_ATTN_PATH, BMC_OPT_ARENA, BMC_OPT_SKIP_PADDING = 1, 2
 BMC_OPT_COPY_ON_READ = 5
 BMC_OPT_TCK_GROUPS = 6
 BMC_OPT_FAULT_OOM = 7
+BMC_OPT_TCK_PREFETCH = 8
 POLICIES = {"bmc": BMC_POLICY_BMC, "iterative": BMC_POLICY_ITERATIVE,
             "upfront": BMC_POLICY_UPFRONT}
 DTYPES = {"f32": BMC_F32, "bf16": BMC_BF16}

@@ -81,25 +81,33 @@ constexpr float kRescale = 8.0f;
 template <int N, int NG, int NS = N>
 struct Cfg {
   static_assert(N % 16 == 0 && N >= 16 && N <= 80, "query columns");
-  static_assert(NG == 2 || NG == 4, "column groups");
+  static_assert(NG >= 2 && NG <= 4, "column groups");
   static_assert(NS <= N && NS % (4 * NG) == 0, "softmax columns");
   static constexpr int NH = NS / NG;                        // columns per softmax group
   static constexpr int kSoftmax = NG * 128;                 // softmax threads
   static constexpr int kThreads = 128 + kSoftmax;
   static constexpr int kWarpV = 2 + 4 * NG;                 // V producer
   static constexpr int kWarpPV = 3 + 4 * NG;                // O^T issuer
-  static constexpr int NBP = N < 64 ? 2 : 1;                // P^T buffers
+  // NS < N (the 70B verify, M = 72 in an N = 80 tile): the hi / lo stack of
+  // P^T is 2*NS columns wide (PV MMA N = 144, not 160), which frees the shared
+  // memory for a second P^T buffer once Q is single-buffered and loaded by TMA
+  // (QTMA): the softmax of tile i+1 then stores its P^T while the O^T MMAs of
+  // tile i read the other buffer instead of waiting for them
+  static constexpr bool QTMA = NS < N;
+  static constexpr int QB = QTMA ? 1 : 2;                   // Q buffers
+  static constexpr int NBP = (N < 64 || QTMA) ? 2 : 1;      // P^T buffers
   static constexpr int KS = N <= 16 ? 3 : 2;                // K ring stages
   static constexpr int VS = N <= 32 ? 3 : 2;                // V ring stages
+  static constexpr int NQK = QTMA ? NS : N;                 // S^T MMA N (query columns)
   static constexpr uint32_t OFF_K = 0;
   static constexpr uint32_t OFF_V = OFF_K + KS * kTileBytes;
-  static constexpr uint32_t OFF_Q = OFF_V + VS * kTileBytes;   // [2 bufs][2 dim atoms][N][128 B]
+  static constexpr uint32_t OFF_Q = OFF_V + VS * kTileBytes;   // [QB bufs][2 dim atoms][N][128 B]
   static constexpr uint32_t kQAtom = N * 128;
   static constexpr uint32_t kQBytes = 2 * kQAtom;
-  // P^T (MN-major SWIZZLE_32B): [NBP][2N/16 query blocks][128 keys][32 B]
-  static constexpr uint32_t OFF_P = OFF_Q + 2 * kQBytes;
+  // P^T (MN-major SWIZZLE_32B): [NBP][2NS/16 query blocks][128 keys][32 B]
+  static constexpr uint32_t OFF_P = OFF_Q + QB * kQBytes;
   static constexpr uint32_t kPBlock = KT * 32;                 // LBO: one 16-query block
-  static constexpr uint32_t kPBytes = 2 * N / 16 * kPBlock;
+  static constexpr uint32_t kPBytes = 2 * NS / 16 * kPBlock;
   static constexpr uint32_t OFF_BAR = OFF_P + NBP * kPBytes;
   static constexpr uint32_t OFF_RED = OFF_BAR + 512;            // [NG][4 quadrants][NH] f32
   static constexpr uint32_t OFF_SUM = OFF_RED + NG * 4 * NH * 4;  // [NG][4][NH] f32
@@ -114,9 +122,10 @@ struct Cfg {
   static_assert(NH % 4 == 0, "8- or 16-byte P stores");
   static constexpr int CS = NH % 8 == 0 ? 8 : 4;               // column step of TMEM / P chunks
   static_assert(NBP * kPBytes >= (4 + 2) * N * 4, "combine scratch in the P area");
-  // TMEM columns: S^T[b] at b*N, O^T (hi N cols, lo N cols) at NB*N
+  static_assert((2 * NS) % 16 == 0 && NQK % 8 == 0, "MMA N");
+  // TMEM columns: S^T[b] at b*N, O^T (hi NS cols, lo NS cols) at NB*N
   static constexpr uint32_t TM_O = NB * N;
-  static constexpr uint32_t kTmemCols = (NB * N + 2 * N <= 256) ? 256 : 512;
+  static constexpr uint32_t kTmemCols = (NB * N + 2 * NS <= 256) ? 256 : 512;
 };
 
 #ifdef BMC_TC_TRACE
@@ -145,6 +154,7 @@ struct LayerP {
   CUtensorMap tmV;          //   (copy-on-read: [U][cap_old][128] of the old buffer, 3D boxes)
   CUtensorMap tmKd;         // copy-on-read only: [U][cap][128] of the new buffer
   CUtensorMap tmVd;
+  CUtensorMap tmQ;          // QTMA only: [B*H_q*t rows][128] bf16, box 64 x N, SWIZZLE_128B
   const __nv_bfloat16* Q;   // [B][H_q][t][D]
   float* O;                 // [B][H_q][t][D]
   const uint8_t* Knew;      // pending appended row [B][H_kv][D] (n_app == 1)
@@ -167,6 +177,7 @@ struct Params {
   float qscale;
   int tree;
   int cor;                  // copy-on-read growth launch
+  int pf;                   // L2 prefetch distance of the K / V producers (tiles; 0 = off)
   uint32_t anc[32];
   int valid[BMC_MAX_B];
 };
@@ -336,7 +347,7 @@ __global__ void __launch_bounds__(Cfg<N, NG, NS>::kThreads, 1)
       mbar_init(PEMPTY(b), 1);
     }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(QFULL(b), C::kSoftmax);
+      mbar_init(QFULL(b), C::QTMA ? 1 : C::kSoftmax);   // QTMA: the K producer's expect_tx
       mbar_init(QDONE(b), 1);
     }
     mbar_init(ODONE, 1);
@@ -394,7 +405,24 @@ __global__ void __launch_bounds__(Cfg<N, NG, NS>::kThreads, 1)
       uint32_t ph = 0;
       long long gu = t_begin / p.tpu;               // global unit
       int j = (int)(t_begin % p.tpu);
+      int item = 0;
       for (long long i = t_begin; i < t_end; ++i) {
+        if constexpr (C::QTMA) {
+          // the item's Q rows (M of N loaded; the rest are neighbouring rows in
+          // softmax columns >= NS that nobody reads) into the single Q buffer
+          // once the S^T MMAs of the previous item are done with it
+          if (isK && (i == t_begin || j == 0)) {
+            if (item > 0) mbar_wait(QDONE(0), (item - 1) & 1);
+            const LayerP& lq = p.lay[MAXL == 1 ? 0 : (int)(gu / p.U)];
+            const long long uq = gu % p.U;
+            const int row = (int)(((uq / p.H_kv) * p.H_q + (uq % p.H_kv) * p.G) * p.t);
+            const uint32_t qs = sbase + C::OFF_Q;
+            mbar_expect_tx(QFULL(0), C::kQBytes);
+            tma_load_2d(qs, &lq.tmQ, 0, row, QFULL(0), pol);
+            tma_load_2d(qs + C::kQAtom, &lq.tmQ, 64, row, QFULL(0), pol);
+            ++item;
+          }
+        }
         mbar_wait(isK ? EMPTYK(s) : EMPTYV(s), ph ^ 1);
         TRACE(isK ? 0 : 1, (int)(i - t_begin));
         const LayerP& ly = p.lay[MAXL == 1 ? 0 : (int)(gu / p.U)];
@@ -411,6 +439,23 @@ __global__ void __launch_bounds__(Cfg<N, NG, NS>::kThreads, 1)
           tma_load_2d(dst, tm, 0, row, fb, pol);
           tma_load_2d(dst + kBox, tm, 64, row, fb, pol);
         }
+        // the tile pf ahead of this one into L2 (under full HBM load a TMA
+        // load takes ~2-4 us; the ring's 2-3 stages alone cannot cover it)
+        if (p.pf > 0 && i + p.pf < t_end) {
+          const long long ip = i + p.pf;
+          const long long gp = ip / p.tpu;
+          const int jp = (int)(ip % p.tpu);
+          const LayerP& lp = p.lay[MAXL == 1 ? 0 : (int)(gp / p.U)];
+          const CUtensorMap* tp = isK ? &lp.tmK : &lp.tmV;
+          if (p.cor) {
+            tma_prefetch_3d(tp, 0, jp * KT, (int)(gp % p.U));
+            tma_prefetch_3d(tp, 64, jp * KT, (int)(gp % p.U));
+          } else {
+            const int rp = (int)((gp % p.U) * p.cap + (long long)jp * KT);
+            tma_prefetch_2d(tp, 0, rp);
+            tma_prefetch_2d(tp, 64, rp);
+          }
+        }
         if (++j == p.tpu) { j = 0; ++gu; }
         if (++s == nst) { s = 0; ph ^= 1; }
       }
@@ -418,7 +463,7 @@ __global__ void __launch_bounds__(Cfg<N, NG, NS>::kThreads, 1)
   } else if (warp == 1) {
     // ------------------------------------------------------ S^T = K Q^T issuer
     if (lane == 0) {
-      constexpr uint32_t IQK = idesc_bf16(KT, N, 0, 0);
+      constexpr uint32_t IQK = idesc_bf16(KT, C::NQK, 0, 0);
       int ks = 0;
       uint32_t kph = 0;
       long long i = t_begin;
@@ -426,9 +471,9 @@ __global__ void __launch_bounds__(Cfg<N, NG, NS>::kThreads, 1)
       while (i < t_end) {
         const long long gu = i / p.tpu;
         const long long iend = min(t_end, (gu + 1) * p.tpu);
-        const int qb = item & 1;
+        const int qb = C::QB == 1 ? 0 : (item & 1);
         const uint32_t qs = sbase + C::OFF_Q + qb * C::kQBytes;
-        mbar_wait(QFULL(qb), (item >> 1) & 1);
+        mbar_wait(QFULL(qb), C::QB == 1 ? (item & 1) : ((item >> 1) & 1));
         fence_after();
         const int n = (int)(iend - i);
         for (int k = 0; k < n; ++k) {
@@ -473,7 +518,7 @@ __global__ void __launch_bounds__(Cfg<N, NG, NS>::kThreads, 1)
   } else if (warp == C::kWarpPV) {
     // ------------------------------------------------------ O^T += V^T P^T issuer
     if (lane == 0) {
-      constexpr uint32_t IPV = idesc_bf16(D, 2 * N, 1, 1);   // A = V tile, B = P^T: MN-major
+      constexpr uint32_t IPV = idesc_bf16(D, 2 * NS, 1, 1);  // A = V tile, B = P^T: MN-major
       int vs = 0;
       uint32_t vph = 0;
       long long i = t_begin;
@@ -563,7 +608,7 @@ __global__ void __launch_bounds__(Cfg<N, NG, NS>::kThreads, 1)
     uint32_t oph = 0;
     long long i = t_begin;
     int tcount = 0, item = 0;
-    if (i < t_end) load_q(i, 0);
+    if (!C::QTMA && i < t_end) load_q(i, 0);
     while (i < t_end) {
       const long long gu = i / p.tpu;                // global unit: layer * U + unit
       const long long iend = min(t_end, (gu + 1) * p.tpu);
@@ -574,7 +619,7 @@ __global__ void __launch_bounds__(Cfg<N, NG, NS>::kThreads, 1)
       const size_t qrow0 = ((size_t)b_ * p.H_q + (size_t)g_ * p.G) * p.t;   // first query row
       // prefetch the next item's Q into the other buffer once the S^T MMAs of
       // the item before this one are done with it
-      if (iend < t_end) {
+      if (!C::QTMA && iend < t_end) {
         if (item >= 1) mbar_wait(QDONE((item - 1) & 1), ((item - 1) >> 1) & 1);
         load_q(iend, (item + 1) & 1);
       }
@@ -698,7 +743,7 @@ __global__ void __launch_bounds__(Cfg<N, NG, NS>::kThreads, 1)
             for (int cc = 0; cc < 2 * NH; cc += C::CS) {
               const int hl = cc >= NH, c0 = cc - hl * NH;
               float ov[C::CS];
-              const uint32_t ta = tmem + C::TM_O + hl * N + h * NH + c0 + lane_addr;
+              const uint32_t ta = tmem + C::TM_O + hl * NS + h * NH + c0 + lane_addr;
               tmem_ld_cols<C::CS>(ta, ov);
 #pragma unroll
               for (int e = 0; e < C::CS; ++e) ov[e] *= asm_[c0 + e];
@@ -740,7 +785,7 @@ __global__ void __launch_bounds__(Cfg<N, NG, NS>::kThreads, 1)
           for (int e = 0; e < NH / 8; ++e) {
             const int eh = h * (NH / 8) + e;             // hi chunk; lo chunks follow N / 8 later
             sts_v4(pbase + paddr(eh), phi[4 * e], phi[4 * e + 1], phi[4 * e + 2], phi[4 * e + 3]);
-            sts_v4(pbase + paddr(eh + N / 8), plo[4 * e], plo[4 * e + 1], plo[4 * e + 2],
+            sts_v4(pbase + paddr(eh + NS / 8), plo[4 * e], plo[4 * e + 1], plo[4 * e + 2],
                    plo[4 * e + 3]);
           }
         } else {   // groups of 4 queries: 8-byte halves of the 16-byte chunks
@@ -749,7 +794,7 @@ __global__ void __launch_bounds__(Cfg<N, NG, NS>::kThreads, 1)
             const int col = h * NH + 4 * e;
             const uint32_t half = (uint32_t)((col >> 2) & 1) * 8u;
             sts_v2(pbase + paddr(col >> 3) + half, phi[2 * e], phi[2 * e + 1]);
-            sts_v2(pbase + paddr((col >> 3) + N / 8) + half, plo[2 * e], plo[2 * e + 1]);
+            sts_v2(pbase + paddr((col >> 3) + NS / 8) + half, plo[2 * e], plo[2 * e + 1]);
           }
         }
         fence_proxy_smem();
@@ -779,7 +824,7 @@ __global__ void __launch_bounds__(Cfg<N, NG, NS>::kThreads, 1)
       for (int c0 = 0; c0 < NH; c0 += C::CS) {
         float o_hi[C::CS], o_lo[C::CS];
         tmem_ld_cols<C::CS>(tmem + C::TM_O + h * NH + c0 + lane_addr, o_hi);
-        tmem_ld_cols<C::CS>(tmem + C::TM_O + N + h * NH + c0 + lane_addr, o_lo);
+        tmem_ld_cols<C::CS>(tmem + C::TM_O + NS + h * NH + c0 + lane_addr, o_lo);
 #pragma unroll
         for (int e = 0; e < C::CS; ++e) {
           const int c = c0 + e;
@@ -852,6 +897,10 @@ extern "C" int bmc_tck_trace(long long* out) {   // [16][256] tile events, then 
 }
 #endif
 
+// L2 prefetch distance (tiles ahead of the ring's loads) unless overridden
+// with BMC_OPT_TCK_PREFETCH
+static constexpr int kDefaultPrefetch = 0;
+
 bool attn_tck_supported(int D, int dtype, int M) {
   return D == 128 && dtype == BMC_BF16 && M >= 1 && M <= 80 && encode_fn() != nullptr;
 }
@@ -887,29 +936,30 @@ static cudaError_t launch_n(const tck::Params<MAXL>& p, int ctas, cudaStream_t s
 // 32-layer step does not re-encode 64 maps on the host every token.
 // units > 0: the 3D [units][rows][128] map of a copy-on-read launch.
 static cudaError_t cached_map(CUtensorMap* m, const void* base, long long rows,
-                              long long units = 0) {
+                              long long units = 0, int box_rows = tck::KT) {
   struct Key {
     const void* base;
     long long rows, units;
+    int box;
     bool operator==(const Key& o) const {
-      return base == o.base && rows == o.rows && units == o.units;
+      return base == o.base && rows == o.rows && units == o.units && box == o.box;
     }
   };
   struct Hash {
     size_t operator()(const Key& k) const {
       return std::hash<const void*>()(k.base) ^ (std::hash<long long>()(k.rows) * 31) ^
-             (std::hash<long long>()(k.units) * 131);
+             (std::hash<long long>()(k.units) * 131) ^ ((size_t)k.box * 1009);
     }
   };
   static thread_local std::unordered_map<Key, CUtensorMap, Hash> cache;
-  const Key k{base, rows, units};
+  const Key k{base, rows, units, box_rows};
   auto it = cache.find(k);
   if (it != cache.end()) {
     *m = it->second;
     return cudaSuccess;
   }
-  cudaError_t e = units > 0 ? make_map3(m, base, units, rows, tck::KT)
-                            : make_map(m, base, rows, tck::KT);
+  cudaError_t e = units > 0 ? make_map3(m, base, units, rows, box_rows)
+                            : make_map(m, base, rows, box_rows);
   if (e != cudaSuccess) return e;
   if (cache.size() > 4096) cache.clear();
   cache.emplace(k, *m);
@@ -943,6 +993,11 @@ static cudaError_t launch_layers(const AttnStepArgs& a, int l0, int nl, int num_
       if (e == cudaSuccess) e = cached_map(&ly.tmV, h.V, U * h.cap);
     }
     if (e != cudaSuccess) return e;
+    // Q rows by TMA (the M = 72 verify variant, box of 80 rows); Q is never
+    // written by the library, so the map is keyed on the caller's pointer
+    if (e == cudaSuccess && a.H_q / a.H_kv * a.t > 64 && a.H_q / a.H_kv * a.t <= 72)
+      e = cached_map(&ly.tmQ, h.Q, (long long)a.B * a.H_q * a.t, 0, 80);
+    if (e != cudaSuccess) return e;
     ly.Q = (const __nv_bfloat16*)h.Q;
     ly.O = h.O;
     ly.Knew = (const uint8_t*)h.Knew;
@@ -969,6 +1024,7 @@ static cudaError_t launch_layers(const AttnStepArgs& a, int l0, int nl, int num_
   p.M = p.G * a.t;
   p.qscale = tck::kLog2e / sqrtf((float)tck::D);
   p.tree = a.tree;
+  p.pf = a.tck_prefetch >= 0 ? a.tck_prefetch : kDefaultPrefetch;
   for (int i = 0; i < 32; ++i) p.anc[i] = a.anc[i];
   for (int b = 0; b < a.B; ++b) p.valid[b] = a.valid[b];
   int ctas = a.ctas > 0 ? a.ctas : num_sms;
@@ -980,12 +1036,18 @@ static cudaError_t launch_layers(const AttnStepArgs& a, int l0, int nl, int num_
     if (p.M <= 32) return launch_n<32, MAXL>(p, ctas, s, a.tck_groups);
     if (p.M <= 48) return launch_n<48, MAXL>(p, ctas, s, a.tck_groups);
     if (p.M <= 64) return launch_n<64, MAXL>(p, ctas, s, a.tck_groups);
+    if (p.M <= 72)   // 64 < M <= 72: the 70B verify tile (3 softmax groups; 2 for A/B)
+      return a.tck_groups == 2 ? launch_ng<80, MAXL, 2, 72>(p, ctas, s)
+                               : launch_ng<80, MAXL, 3, 72>(p, ctas, s);
     return launch_n<80, MAXL>(p, ctas, s, a.tck_groups);
   } else {
     if (p.M <= 16) return launch_n<16, 1>(p, ctas, s, a.tck_groups);
     if (p.M <= 32) return launch_n<32, 1>(p, ctas, s, a.tck_groups);
     if (p.M <= 48) return launch_n<48, 1>(p, ctas, s, a.tck_groups);
     if (p.M <= 64) return launch_n<64, 1>(p, ctas, s, a.tck_groups);
+    if (p.M <= 72)   // 64 < M <= 72: the 70B verify tile (3 softmax groups; 2 for A/B)
+      return a.tck_groups == 2 ? launch_ng<80, 1, 2, 72>(p, ctas, s)
+                               : launch_ng<80, 1, 3, 72>(p, ctas, s);
     return launch_n<80, 1>(p, ctas, s, a.tck_groups);
   }
 }

@@ -52,6 +52,7 @@ struct bmc_ctx {
   int skip_padding = 0;          // length-aware ablation, off by default
   int copy_on_read = 1;          // BMC growth inside the fused decode step
   int tck_groups = 0;            // keys-on-lanes kernel softmax column groups (0 auto)
+  int tck_prefetch = -1;         // keys-on-lanes kernel L2 prefetch distance (-1 auto)
   int fault_oom = 0;             // test hook: the next n growth allocations fail (BMC_OPT_FAULT_OOM)
   // a growth whose copy the next attention launch performs (copy-on-read):
   // the old buffers and the rows to carry over; never observable between API
@@ -448,6 +449,7 @@ static void fill_args(bmc_t h, int t, bmc::AttnStepArgs* a) {
   a->ctas = std::min(h->attn_ctas, h->max_ctas);
   a->tree = h->tree;
   a->tck_groups = h->tck_groups;
+  a->tck_prefetch = h->tck_prefetch;
   for (int i = 0; i < 32; ++i) a->anc[i] = h->anc[i];
   for (int b = 0; b < h->B; ++b) a->valid[b] = h->valid[b];
 }
@@ -1541,8 +1543,12 @@ int bmc_set_option(bmc_t h, int key, long long value) {
       h->copy_on_read = (int)value;
       return 0;
     case BMC_OPT_TCK_GROUPS:
-      if (value != 0 && value != 2 && value != 4) return fail(BMC_ERR_ARG, "tck groups");
+      if (value != 0 && value != 2 && value != 3 && value != 4) return fail(BMC_ERR_ARG, "tck groups");
       h->tck_groups = (int)value;
+      return 0;
+    case BMC_OPT_TCK_PREFETCH:
+      if (value < -1 || value > 64) return fail(BMC_ERR_ARG, "tck prefetch");
+      h->tck_prefetch = (int)value;
       return 0;
     case BMC_OPT_FAULT_OOM:
       if (value < 0 || value > 1000000) return fail(BMC_ERR_ARG, "fault count");

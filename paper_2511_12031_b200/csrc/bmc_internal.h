@@ -82,7 +82,8 @@ struct AttnStepArgs {
   int B, H_kv, H_q, D, t, dtype;
   int ctas;                               // 0 = auto
   int tree;                               // staged rows form a token tree
-  int tck_groups = 0;                     // keys-on-lanes kernel softmax groups (0 auto, 2, 4)
+  int tck_groups = 0;                     // keys-on-lanes kernel softmax groups (0 auto, 2, 3, 4)
+  int tck_prefetch = -1;                  // keys-on-lanes kernel L2 prefetch distance (-1 auto)
   uint32_t anc[32];                       // tree: bit j of anc[i] = node j is i or an ancestor
   int valid[BMC_MAX_B];                   // committed rows incl. the pending append
   int L;

@@ -17,7 +17,7 @@ from paper_2511_12031_b200 import bmc  # noqa: E402
 
 
 def attn_at(B, H_kv, H_q, D, cap, t=1, reps=50, dtype="bf16", ctas=0, layers=8, path=0,
-            groups=0):
+            groups=0, prefetch=-1):
     """SDPA over `layers` independent handles filled to `cap` rows (upfront
     policy so the buffer is exactly cap rows), round-robin so each launch reads
     an L2-cold cache."""
@@ -31,6 +31,8 @@ def attn_at(B, H_kv, H_q, D, cap, t=1, reps=50, dtype="bf16", ctas=0, layers=8, 
         h.set_option(bmc.BMC_OPT_ATTN_PATH, path)
         if groups:
             h.set_option(bmc.BMC_OPT_TCK_GROUPS, groups)
+        if prefetch >= 0:
+            h.set_option(bmc.BMC_OPT_TCK_PREFETCH, prefetch)
         hs.append(h)
     k = torch.randn(B, H_kv, D, device="cuda").to(tdt)
     for h in hs:
