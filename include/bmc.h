@@ -296,6 +296,14 @@ int bmc_pool_reserve(int device, long long bytes);
 /* Kernels launched by this library in this process so far (all handles). */
 unsigned long long bmc_launch_count(void);
 
+/* Host-time diagnostics of the growth path, per category: 0 growth
+   allocations (arena_alloc), 1 stream-ordered releases, 2 attention-launch
+   calls of the fused steps, 3 helper-thread VMM pre-mapping, 4 VMM mappings
+   done synchronously at a growth (the pre-map was late).  ns[5] and calls[5]
+   (host arrays) receive nanoseconds and call counts since the last reset;
+   reset != 0 zeroes them.  Errors: ARG (null arrays). */
+int bmc_host_profile(long long* ns, long long* calls, int reset);
+
 /* Thread-local message for the last error (empty string if none). */
 const char* bmc_last_error(void);
 

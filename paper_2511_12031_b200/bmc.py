@@ -41,7 +41,7 @@ EXPORTS = ["bmc_create", "bmc_create_ex", "bmc_append", "bmc_append_n", "bmc_spe
            "bmc_sdpa", "bmc_admissible", "bmc_spec_step",
            "bmc_commit", "bmc_commit_rows", "bmc_commit_step", "bmc_commit_path", "bmc_pool_reserve", "bmc_spec_write_tree",
            "bmc_decode_step", "bmc_destroy", "bmc_stats", "bmc_kv_view",
-           "bmc_valid", "bmc_read_cache", "bmc_sync", "bmc_set_option", "bmc_launch_count", "bmc_last_error"]
+           "bmc_valid", "bmc_read_cache", "bmc_sync", "bmc_set_option", "bmc_launch_count", "bmc_host_profile", "bmc_last_error"]
 
 
 class BMCError(RuntimeError):
@@ -96,6 +96,7 @@ def load(path: str = SO_PATH):
     L.bmc_sync.argtypes = [vp]
     L.bmc_set_option.argtypes = [vp, i, ll]
     L.bmc_launch_count.argtypes = []
+    L.bmc_host_profile.argtypes = [ctypes.POINTER(ll), ctypes.POINTER(ll), i]
     L.bmc_launch_count.restype = ctypes.c_ulonglong
     L.bmc_last_error.argtypes = []
     L.bmc_last_error.restype = ctypes.c_char_p
@@ -252,6 +253,17 @@ def bmc_sync(h) -> int:
 
 def bmc_set_option(h, key: int, value: int) -> int:
     return _check(load().bmc_set_option(h, key, value), "bmc_set_option")
+
+
+HOST_CATS = ("alloc", "release", "launch", "premap", "sync_map")
+
+
+def bmc_host_profile(reset: bool = True) -> dict:
+    """Host time (ms) and calls per growth-path category (include/bmc.h)."""
+    ns = (ctypes.c_longlong * 5)()
+    calls = (ctypes.c_longlong * 5)()
+    _check(load().bmc_host_profile(ns, calls, int(reset)), "bmc_host_profile")
+    return {k: (ns[i] / 1e6, int(calls[i])) for i, k in enumerate(HOST_CATS)}
 
 
 def bmc_launch_count() -> int:

@@ -14,6 +14,12 @@
 //     the same step and cannot lend chunks to each other.  Chunks return to
 //     the pool when the handle is destroyed.  Virtual addresses of a handle
 //     take only two values per tensor.
+//     Growth is predictable (BMC: the next growth is r appends away and its
+//     size is cap + r), so the caller asks for the NEXT growth's chunks right
+//     after a growth (arena_premap): a process-wide helper thread creates and
+//     maps them while the decode steps run, and the growth itself finds its
+//     slot mapped -- cuMemCreate / cuMemMap / cuMemSetAccess (~2.5 ms per
+//     layer-growth on B200) leave the host's critical path.
 //   kind 1 (pool): cudaMallocFromPoolAsync / cudaFreeAsync on a per-device
 //     memory pool with an unbounded release threshold (stream-ordered reuse).
 #include <cstdlib>
@@ -22,9 +28,12 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <condition_variable>
+#include <deque>
 #include <map>
 #include <mutex>
 #include <set>
+#include <thread>
 #include <vector>
 
 #include "bmc_internal.h"
@@ -97,6 +106,7 @@ std::set<Arena*> g_arenas;
 }  // namespace
 
 struct Arena {
+  std::mutex mu;          // slot mappings (the helper thread maps ahead)
   int device = 0;
   size_t slot_bytes = 0;  // reserved VA per slot (multiple of chunk)
   size_t chunk = 0;
@@ -197,17 +207,25 @@ static int map_slot(Arena* a, int tensor, int slot, size_t bytes) {
   prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
   prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
   prop.location.id = a->device;
+  if (cudaSetDevice(a->device) != cudaSuccess) return BMC_ERR_CUDA;   // helper thread
   for (size_t i = have; i < need; ++i) {
     CUmemGenericAllocationHandle h;
-    if (!a->pool->free_list.empty()) {
-      h = a->pool->free_list.back();
-      a->pool->free_list.pop_back();
-    } else {
+    bool reuse = false;
+    {
+      std::lock_guard<std::mutex> lk(g_mu);
+      if (!a->pool->free_list.empty()) {
+        h = a->pool->free_list.back();
+        a->pool->free_list.pop_back();
+        reuse = true;
+      }
+    }
+    if (!reuse) {
       CUresult r = drv().create(&h, a->chunk, &prop, 0);
       if (r == CUDA_ERROR_OUT_OF_MEMORY) return BMC_ERR_OOM;
       if (r != CUDA_SUCCESS) return BMC_ERR_CUDA;
     }
     if (drv().map(va + i * a->chunk, a->chunk, 0, h, 0) != CUDA_SUCCESS) {
+      std::lock_guard<std::mutex> lk(g_mu);
       a->pool->free_list.push_back(h);
       return BMC_ERR_CUDA;
     }
@@ -226,7 +244,7 @@ int arena_alloc(Arena* a, int tensor, size_t bytes, int kind, const Buffer* keep
   *out = Buffer();
   if (bytes == 0) bytes = 16;
   if (kind == 0 && a->vmm_ok) {
-    std::lock_guard<std::mutex> lk(g_mu);
+    std::lock_guard<std::mutex> lk(a->mu);   // waits only if a premap of this arena is running
     int slot = (keep && keep->ptr && keep->kind == 0) ? 1 - keep->slot : 0;
     Slot& sl = a->slots[tensor][slot];
     // the slot's previous contents were last used earlier on this stream, so
@@ -236,7 +254,10 @@ int arena_alloc(Arena* a, int tensor, size_t bytes, int kind, const Buffer* keep
       cudaEventDestroy(sl.pending);
       sl.pending = nullptr;
     }
+    const bool missing = (bytes + a->chunk - 1) / a->chunk > a->slots[tensor][slot].chunks.size();
+    const long long t0 = host_now_ns();
     int rc = map_slot(a, tensor, slot, bytes);
+    if (missing) host_time_add(kHostSyncMap, host_now_ns() - t0);   // not premapped in time
     if (rc) return rc;
     out->ptr = (void*)(a->base + (CUdeviceptr)((tensor * 2 + slot) * a->slot_bytes));
     out->bytes = bytes;
@@ -305,8 +326,84 @@ int pool_reserve(int device, size_t bytes) {
   return rc;
 }
 
+// ------------------------------------------------- asynchronous pre-mapping
+namespace {
+struct PremapTask { Arena* a; int tensor, slot; size_t bytes; };
+struct Premapper {
+  std::mutex mu;
+  std::condition_variable cv, idle;
+  std::deque<PremapTask> q;
+  Arena* running = nullptr;
+  bool started = false;
+  unsigned long long done = 0, late = 0;
+  void loop() {
+    for (;;) {
+      PremapTask t;
+      {
+        std::unique_lock<std::mutex> lk(mu);
+        cv.wait(lk, [&] { return !q.empty(); });
+        t = q.front();
+        q.pop_front();
+        running = t.a;
+      }
+      {
+        std::lock_guard<std::mutex> lk(t.a->mu);
+        // the live buffer moved to the target slot in the meantime: the
+        // request is stale (the growth it prepared for has happened)
+        if (t.a->live[t.tensor] != t.slot) {
+          const long long t0 = host_now_ns();
+          map_slot(t.a, t.tensor, t.slot, t.bytes);
+          host_time_add(kHostPremap, host_now_ns() - t0);
+        }
+      }
+      {
+        std::lock_guard<std::mutex> lk(mu);
+        running = nullptr;
+        ++done;
+      }
+      idle.notify_all();
+    }
+  }
+};
+Premapper* g_premap = nullptr;
+std::mutex g_premap_mu;
+
+Premapper* premapper() {
+  std::lock_guard<std::mutex> lk(g_premap_mu);
+  if (!g_premap) {
+    g_premap = new Premapper();   // process lifetime (the thread never exits)
+    std::thread([p = g_premap] { p->loop(); }).detach();
+  }
+  return g_premap;
+}
+}  // namespace
+
+int arena_premap(Arena* a, int tensor, size_t bytes) {
+  if (!a || !a->vmm_ok || tensor < 0 || tensor > 1) return 0;
+  int slot;
+  {
+    std::lock_guard<std::mutex> lk(a->mu);
+    slot = a->live[tensor] < 0 ? 0 : 1 - a->live[tensor];
+    const size_t need = (std::max<size_t>(bytes, 16) + a->chunk - 1) / a->chunk;
+    if (need <= a->slots[tensor][slot].chunks.size()) return 0;   // already mapped
+  }
+  Premapper* p = premapper();
+  {
+    std::lock_guard<std::mutex> lk(p->mu);
+    p->q.push_back(PremapTask{a, tensor, slot, bytes});
+  }
+  p->cv.notify_one();
+  return 0;
+}
+
 void arena_destroy(Arena* a) {
   if (!a) return;
+  if (g_premap) {   // no helper-thread work may touch the arena after this
+    std::unique_lock<std::mutex> lk(g_premap->mu);
+    for (auto it = g_premap->q.begin(); it != g_premap->q.end();)
+      it = it->a == a ? g_premap->q.erase(it) : it + 1;
+    g_premap->idle.wait(lk, [&] { return g_premap->running != a; });
+  }
   std::lock_guard<std::mutex> lk(g_mu);
   for (int t = 0; t < 2; ++t)
     for (int s = 0; s < 2; ++s) {

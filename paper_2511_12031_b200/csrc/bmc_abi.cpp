@@ -298,12 +298,24 @@ static int reallocate(bmc_t h, long long new_cap, long long copy_rows, bool defe
   }
   const size_t bytes = (size_t)h->U * new_cap * h->row_bytes;
   Buffer nk, nv;
+  const long long t_alloc = bmc::host_now_ns();
   int rc = bmc::arena_alloc(h->arena, 0, bytes, h->arena_kind, &h->kbuf, h->stream, &nk);
   if (rc) return fail(rc, "arena_alloc(K, %zu bytes) failed", bytes);
   rc = bmc::arena_alloc(h->arena, 1, bytes, h->arena_kind, &h->vbuf, h->stream, &nv);
+  bmc::host_time_add(bmc::kHostAlloc, bmc::host_now_ns() - t_alloc);
   if (rc) {
     bmc::arena_release(h->arena, &nk, h->stream);
     return fail(rc, "arena_alloc(V, %zu bytes) failed", bytes);
+  }
+  // VMM arena: map the NEXT growth's chunks on the helper thread now (BMC:
+  // r appends away, size cap + r; ITERATIVE: a few rows more)
+  if (h->arena_kind == 0 && h->pol != BMC_POLICY_UPFRONT) {
+    const long long nxt = h->pol == BMC_POLICY_BMC ? std::min<long long>(new_cap + h->r, h->N_max)
+                                                   : std::min<long long>(new_cap + 64, h->N_max);
+    if (nxt > new_cap) {
+      bmc::arena_premap(h->arena, 0, (size_t)h->U * nxt * h->row_bytes);
+      bmc::arena_premap(h->arena, 1, (size_t)h->U * nxt * h->row_bytes);
+    }
   }
   if (h->cap > 0) h->st.copy_events += 1;
   h->st.alloc_events += 1;
@@ -347,11 +359,13 @@ static int reallocate(bmc_t h, long long new_cap, long long copy_rows, bool defe
 static int cor_release(bmc_t h) {
   if (!h->cor) return 0;
   h->cor = false;
+  const long long t0 = bmc::host_now_ns();
   if (bmc::arena_release(h->arena, &h->cor_k, h->stream) ||
       bmc::arena_release(h->arena, &h->cor_v, h->stream)) {
     h->sticky = BMC_ERR_CUDA;
     return fail(BMC_ERR_CUDA, "arena_release failed");
   }
+  bmc::host_time_add(bmc::kHostRelease, bmc::host_now_ns() - t0);
   return 0;
 }
 
@@ -605,6 +619,10 @@ static int rollback_chunk(const bmc_t* hs, int l0, int l_end, int n_appended, in
 // one step sequence), else one launch per layer (e.g. after an OOM fallback
 // carried some layers' growths out with the realloc kernel).
 static int launch_tck_chunk(bmc_t h0, const bmc::AttnStepArgs& a, bmc::AttnLayer* layers, int nl) {
+  struct T {
+    long long t0 = bmc::host_now_ns();
+    ~T() { bmc::host_time_add(bmc::kHostLaunch, bmc::host_now_ns() - t0); }
+  } timer;
   bool same = true;
   for (int l = 1; l < nl; ++l)
     if (layers[l].cap != layers[0].cap || layers[l].scan != layers[0].scan ||
@@ -1571,6 +1589,12 @@ int bmc_pool_reserve(int device, long long bytes) {
 }
 
 unsigned long long bmc_launch_count(void) { return bmc::launch_count(); }
+
+int bmc_host_profile(long long* ns, long long* calls, int reset) {
+  if (!ns || !calls) return fail(BMC_ERR_ARG, "null argument");
+  bmc::host_time_read(ns, calls, reset != 0);
+  return 0;
+}
 
 const char* bmc_last_error(void) { return g_err.c_str(); }
 

@@ -109,6 +109,11 @@ cudaError_t launch_attn_tck(const AttnStepArgs& a, int num_sms, cudaStream_t s);
 
 void count_launch();
 unsigned long long launch_count();
+// Host-time diagnostics (bmc_host_profile): nanoseconds and calls per category
+enum HostCat { kHostAlloc = 0, kHostRelease, kHostLaunch, kHostPremap, kHostSyncMap, kHostCats };
+void host_time_add(int cat, long long ns);
+void host_time_read(long long* ns, long long* calls, bool reset);
+long long host_now_ns();
 
 // ------------------------------------------------------------------ arena
 // Chunk-growth allocator: each handle owns one arena with two ping-pong
@@ -130,6 +135,10 @@ int arena_alloc(Arena* a, int tensor, size_t bytes, int kind, const Buffer* keep
                 cudaStream_t s, Buffer* out);
 // Release a buffer once all work enqueued so far on s has finished with it.
 int arena_release(Arena* a, Buffer* b, cudaStream_t s);
+// VMM arenas: map (on a helper thread, asynchronously) the physical chunks a
+// future arena_alloc of `bytes` for tensor will need in the slot that is not
+// live; a no-op for pool arenas or when already mapped.
+int arena_premap(Arena* a, int tensor, size_t bytes);
 void arena_destroy(Arena* a);
 
 // 0 device / managed, 1 page-locked host, 2 pageable host (cached by range).

@@ -1,3 +1,4 @@
+#include <chrono>
 // cache_kernels.cu -- KV-cache update kernels of the BMC hot path (sm_100a).
 //
 //   realloc_copy_zero : the BMC growth step: for every
@@ -23,6 +24,21 @@ namespace bmc {
 
 static std::atomic<unsigned long long> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+static std::atomic<long long> g_host_ns[kHostCats], g_host_calls[kHostCats];
+void host_time_add(int cat, long long ns) {
+  g_host_ns[cat].fetch_add(ns, std::memory_order_relaxed);
+  g_host_calls[cat].fetch_add(1, std::memory_order_relaxed);
+}
+void host_time_read(long long* ns, long long* calls, bool reset) {
+  for (int i = 0; i < kHostCats; ++i) {
+    ns[i] = reset ? g_host_ns[i].exchange(0) : g_host_ns[i].load();
+    calls[i] = reset ? g_host_calls[i].exchange(0) : g_host_calls[i].load();
+  }
+}
+long long host_now_ns() {
+  return std::chrono::duration_cast<std::chrono::nanoseconds>(
+             std::chrono::steady_clock::now().time_since_epoch()).count();
+}
 unsigned long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
 __device__ __forceinline__ int4 ld_stream(const int4* p) {

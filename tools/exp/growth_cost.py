@@ -12,6 +12,10 @@ import torch  # noqa: E402
 from paper_2511_12031_b200 import bmc  # noqa: E402
 
 L, B, H, D, N, r = 32, 16, 32, 128, 4096, 128
+ARENA = 0 if "--vmm" in sys.argv else 1   # BMC_OPT_ARENA: 0 VMM slots (premapped), 1 pool
+if "--reserve" in sys.argv:                # map the peak footprint into the pool up front
+    bmc.load()
+    bmc.bmc_pool_reserve(0, 2 * B * H * N * D * 2 * (L + L))
 k = [torch.randn(B, H, D, device="cuda").to(torch.bfloat16) for _ in range(L)]
 q = [torch.randn(B, H, 1, D, device="cuda").to(torch.bfloat16) for _ in range(L)]
 o = [torch.empty(B, H, 1, D, device="cuda") for _ in range(L)]
@@ -19,6 +23,8 @@ o = [torch.empty(B, H, 1, D, device="cuda") for _ in range(L)]
 
 def gen(tag):
     hs = [bmc.KVCache(B, H, H, D, r, N, dtype="bf16") for _ in range(L)]
+    for h in hs:
+        h.set_option(bmc.BMC_OPT_ARENA, ARENA)
     plan = bmc.StepPlan(hs)
     K, Q, O = plan.ptrs(k), plan.ptrs(q), plan.ptrs(o)
     torch.cuda.synchronize()
@@ -40,9 +46,12 @@ def gen(tag):
     print(f"{tag}: wall {1e3 * (T1 - T0):.0f} ms, gpu {sum(g):.0f} ms; {len(grow)} growth steps: "
           f"gpu {gs:.0f} ms, host {hg:.0f} ms; other steps: host {1e3 * sum(host) - hg:.0f} ms; "
           f"max growth host {max(host[n] for n in grow) * 1e3:.1f} ms", flush=True)
+    prof = bmc.bmc_host_profile(reset=True)
+    print("   host ms (calls):", {k: (round(v[0], 1), v[1]) for k, v in prof.items()}, flush=True)
     for h in hs:
         h.close()
 
 
+print("arena:", "vmm (helper-thread premap)" if ARENA == 0 else "pool")
 for i in range(3):
     gen(f"gen{i}")
