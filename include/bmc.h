@@ -293,6 +293,12 @@ int bmc_set_option(bmc_t h, int key, long long value);
    OOM, CUDA. */
 int bmc_pool_reserve(int device, long long bytes);
 
+/* bmc_pool_trim: wait for the device, then return the growth pool's unused
+   memory (blocks no live buffer uses, e.g. a previous workload's or a
+   reserve's) to the driver (-1 = current device).  Between workloads only.
+   Errors: CUDA. */
+int bmc_pool_trim(int device);
+
 /* Kernels launched by this library in this process so far (all handles). */
 unsigned long long bmc_launch_count(void);
 

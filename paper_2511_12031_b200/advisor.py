@@ -108,10 +108,19 @@ def bytes_per_layer(N: int, r: int, U: int, D: int, eb: int) -> dict:
     return {"sdpa": sdpa, "copy": copy}
 
 
-def advise_r(N: int, bw_read: float = 1.0, bw_copy: float = 1.0, pow2: bool = True) -> int:
-    """r* = sqrt(2 N BW_read / BW_copy), T* = N / r* rounded to a power of
-    two as the paper does for T, r = N / T."""
-    r = math.sqrt(2 * N * bw_read / bw_copy)
+def advise_r(N: int, bw_read: float = 1.0, bw_copy: float = 1.0, pow2: bool = True,
+             copy_on_read: bool = False, tokens_per_iter: float = 1.0) -> int:
+    """r* = sqrt(f N m BW_read / BW_copy), T* = N / r* rounded to a power of
+    two as the paper does for T, r = N / T.
+    f = 2 with a separate realloc copy (each growth reads cap_old and writes
+    cap_new rows: ~N^2/r rows per decode); f = 1 with copy-on-read growth
+    (the attention already streams the old rows, the growth adds the write of
+    the new buffer: ~N^2/(2r) rows; BW_copy is then that write bandwidth).
+    m = tokens per iteration under speculation: the verify reads cap rows
+    once per iteration, N/m times per decode, while the T growths stay, so
+    r* grows as sqrt(m) and T* ~ sqrt(N/m) (TimeNIter, P:L910-917)."""
+    f = 1.0 if copy_on_read else 2.0
+    r = math.sqrt(f * N * tokens_per_iter * bw_read / bw_copy)
     if not pow2:
         return max(1, min(N, round(r)))
     T = round_pow2(N / r)

@@ -39,7 +39,7 @@ _NAMES = {0: "OK", -1: "ARG", -2: "STATE", -3: "CAPACITY", -4: "OOM", -5: "CUDA"
 
 EXPORTS = ["bmc_create", "bmc_create_ex", "bmc_append", "bmc_append_n", "bmc_spec_write",
            "bmc_sdpa", "bmc_admissible", "bmc_spec_step",
-           "bmc_commit", "bmc_commit_rows", "bmc_commit_step", "bmc_commit_path", "bmc_pool_reserve", "bmc_spec_write_tree",
+           "bmc_commit", "bmc_commit_rows", "bmc_commit_step", "bmc_commit_path", "bmc_pool_reserve", "bmc_pool_trim", "bmc_spec_write_tree",
            "bmc_decode_step", "bmc_destroy", "bmc_stats", "bmc_kv_view",
            "bmc_valid", "bmc_read_cache", "bmc_sync", "bmc_set_option", "bmc_launch_count", "bmc_host_profile", "bmc_last_error"]
 
@@ -85,6 +85,7 @@ def load(path: str = SO_PATH):
     L.bmc_commit_rows.argtypes = [vp, ctypes.POINTER(ctypes.c_int)]
     L.bmc_commit_step.argtypes = [vp, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
     L.bmc_pool_reserve.argtypes = [ctypes.c_int, ctypes.c_longlong]
+    L.bmc_pool_trim.argtypes = [ctypes.c_int]
     L.bmc_destroy.argtypes = [vp]
     L.bmc_spec_write_tree.argtypes = [vp, vp, vp, i, ctypes.POINTER(ctypes.c_int)]
     L.bmc_commit_path.argtypes = [vp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int), i]
@@ -158,6 +159,10 @@ def bmc_sdpa(h, Q, n_valid: int, O) -> int:
 def bmc_pool_reserve(device: int, nbytes: int) -> int:
     """Map nbytes of device memory into the library's growth pool now."""
     return _check(load().bmc_pool_reserve(device, nbytes), "bmc_pool_reserve")
+
+
+def bmc_pool_trim(device: int = -1) -> int:
+    return _check(load().bmc_pool_trim(device), "bmc_pool_trim")
 
 
 def bmc_commit(h, n_accepted: int) -> int:

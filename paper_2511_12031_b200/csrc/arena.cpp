@@ -396,6 +396,20 @@ int arena_premap(Arena* a, int tensor, size_t bytes) {
   return 0;
 }
 
+// Return the pool's unused physical memory to the driver (between workloads).
+int pool_trim(int device) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  cudaMemPool_t mp = mempool_for(device);
+  if (!mp) return BMC_ERR_CUDA;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != device && cudaSetDevice(device) != cudaSuccess) return BMC_ERR_CUDA;
+  const int rc = (cudaDeviceSynchronize() == cudaSuccess && cudaMemPoolTrimTo(mp, 0) == cudaSuccess)
+                     ? 0 : BMC_ERR_CUDA;
+  if (prev != device) cudaSetDevice(prev);
+  return rc;
+}
+
 void arena_destroy(Arena* a) {
   if (!a) return;
   if (g_premap) {   // no helper-thread work may touch the arena after this

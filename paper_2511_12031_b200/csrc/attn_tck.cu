@@ -95,8 +95,13 @@ struct Cfg {
   // tile i read the other buffer instead of waiting for them
   static constexpr bool QTMA = NS < N;
   static constexpr int QB = QTMA ? 1 : 2;                   // Q buffers
+#ifdef BMC_M72_KS3   // experiment: a third K stage instead of the second P^T buffer
+  static constexpr int NBP = N < 64 ? 2 : 1;                // P^T buffers
+  static constexpr int KS = (N <= 16 || QTMA) ? 3 : 2;      // K ring stages
+#else
   static constexpr int NBP = (N < 64 || QTMA) ? 2 : 1;      // P^T buffers
   static constexpr int KS = N <= 16 ? 3 : 2;                // K ring stages
+#endif
   static constexpr int VS = N <= 32 ? 3 : 2;                // V ring stages
   static constexpr int NQK = QTMA ? NS : N;                 // S^T MMA N (query columns)
   static constexpr uint32_t OFF_K = 0;

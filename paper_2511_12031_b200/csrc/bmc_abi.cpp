@@ -1588,6 +1588,16 @@ int bmc_pool_reserve(int device, long long bytes) {
   return 0;
 }
 
+int bmc_pool_trim(int device) {
+  if (device < 0) {
+    cudaError_t e = cudaGetDevice(&device);
+    if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaGetDevice");
+  }
+  const int rc = bmc::pool_trim(device);
+  if (rc) return fail(rc, "pool_trim failed");
+  return 0;
+}
+
 unsigned long long bmc_launch_count(void) { return bmc::launch_count(); }
 
 int bmc_host_profile(long long* ns, long long* calls, int reset) {

@@ -128,6 +128,7 @@ struct Buffer {
 };
 Arena* arena_create(int device, size_t max_bytes_per_tensor, int* err);
 int pool_reserve(int device, size_t bytes);
+int pool_trim(int device);
 // Obtain a buffer of `bytes` for tensor (0 = K, 1 = V) in the slot not
 // holding `keep` (the tensor's live buffer).  kind 0 = VMM slot, 1 =
 // stream-ordered pool allocation (also the fallback when VMM is unsupported).

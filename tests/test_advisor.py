@@ -82,3 +82,25 @@ def test_advise_r_minimises_byte_model():
     assert abs(best - r_star) <= 8
     assert A.advise_r(N) in (64, 128)              # T* = 45.25 -> nearest power of 2 is 32
     assert A.advise_r(N) == 128
+
+
+def test_advise_r_copy_on_read_and_speculation():
+    """Byte model with copy-on-read growth (growth adds the write of cap_new
+    rows, N^2/(2r) in total) is minimised at r* = sqrt(N BW_r/BW_w): at equal
+    bandwidths the brute-force minimum of row*(N(N+r)/2 + N^2/(2r)) over r is
+    sqrt(N).  Speculation with m tokens per iteration reads cap once per
+    iteration: r* = sqrt(m N) (T ~ sqrt(N/m))."""
+    import math
+    from paper_2511_12031_b200 import advisor
+    for N in (1024, 4096, 16384):
+        cost = lambda r: N * (N + r) / 2 + N * N / (2 * r)
+        best = min(range(1, N + 1), key=cost)
+        assert abs(best - math.sqrt(N)) <= 1
+        assert advisor.advise_r(N, copy_on_read=True, pow2=False) == round(math.sqrt(N))
+        for m in (2.0, 4.0):
+            cost_m = lambda r: (N / m) * (N + r) / 2 + N * N / (2 * r)
+            best_m = min(range(1, N + 1), key=cost_m)
+            assert abs(advisor.advise_r(N, copy_on_read=True, pow2=False, tokens_per_iter=m)
+                       - best_m) <= 1
+    # defaults unchanged (separate copy, no speculation): sqrt(2N), T rounded to 2^k
+    assert advisor.advise_r(4096) == 128

@@ -24,13 +24,21 @@ from paper_2511_12031_b200 import bmc  # noqa: E402
 
 
 def run_point(cfg, policy, r, reps=1, skip_padding=False):
+    """One sweep point.  Each point starts from a trimmed growth pool with the
+    workload's peak footprint reserved (as bench.py does), so no point pays
+    (or inherits) the driver's pool-growth stalls."""
     dev = torch.device("cuda", 0)
     stream = torch.cuda.current_stream(dev)
     B = cfg["B"]
+    torch.cuda.synchronize()
+    bmc.bmc_pool_trim(0)
     ring = bench.make_ring(cfg, B, dev)
     t_all = 1 + cfg["k"]
     outs = {t: [torch.empty(B, cfg["H_q"], t, cfg["D"], dtype=torch.float32, device=dev)
                 for _ in range(cfg["L"])] for t in range(1, t_all + 1)}
+    eb = 2 if cfg["dtype"] == "bf16" else 4
+    per_layer = 2 * B * cfg["H_kv"] * cfg["N"] * cfg["D"] * eb
+    bmc.bmc_pool_reserve(0, bench.reserve_bytes(per_layer, cfg["L"], dev, margin=4 << 30))
     gen = bench.Generation(cfg, B, r, policy, ring, outs, stream, 0)
     gen.skip_padding = skip_padding
     gen.run()                                   # warm-up
