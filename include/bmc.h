@@ -266,8 +266,9 @@ int bmc_sync(bmc_t h);
                               A/B only; results agree within the tolerance.
      8 BMC_OPT_TCK_PREFETCH   L2 prefetch distance of the keys-on-lanes kernel's
                               K / V producers, in 128-key tiles ahead of the
-                              shared-memory ring (-1 auto, 0 off).  Tuning /
-                              A/B only; results are identical.
+                              shared-memory ring (-1 auto = 0, off: measured
+                              5-7% slower).  Tuning / A/B only; results are
+                              identical.
      7 BMC_OPT_FAULT_OOM      fault injection for tests: the next `value`
                               growth allocations of this handle fail with
                               BMC_ERR_OOM (exercises the fused steps' OOM

@@ -63,6 +63,17 @@ class Stats(ctypes.Structure):
 _lib = None
 
 
+class _missing:
+    """Stand-in for a symbol an experiment build of the library lacks."""
+
+    def __init__(self, name):
+        self.name = name
+        self.argtypes = self.restype = None
+
+    def __call__(self, *a):
+        raise RuntimeError(f"{self.name} is not in this build of libbmc")
+
+
 def load(path: str = SO_PATH):
     """Load libbmc.so (raises if it has not been built)."""
     global _lib
@@ -72,6 +83,10 @@ def load(path: str = SO_PATH):
     if not os.path.exists(path):
         raise RuntimeError(f"libbmc.so not built at {path}: run __graft_entry__.build()")
     L = ctypes.CDLL(path)
+    if path != SO_PATH:   # experiment builds may predate newer diagnostics
+        for name in ("bmc_pool_trim", "bmc_host_profile"):
+            if not hasattr(L, name):
+                setattr(L, name, _missing(name))
     vp, i, ll = ctypes.c_void_p, ctypes.c_int, ctypes.c_longlong
     L.bmc_create.argtypes = [i, i, i, i, i, i, ctypes.POINTER(vp)]
     L.bmc_create_ex.argtypes = [i, i, i, i, i, i, i, i, i, vp, ctypes.POINTER(vp)]

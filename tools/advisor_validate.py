@@ -49,7 +49,10 @@ def main():
             continue
         cfg = dict(bench.CONFIGS[cname])
         cfg["N"] = N
-        pts = [run_point(cfg, "bmc", r) for r in rs]
+        # short generations are repeated (>= ~8K tokens per timed point) so a
+        # point is not one clock ramp
+        reps = max(1, 8192 // N)
+        pts = [run_point(cfg, "bmc", r, reps=reps) for r in rs]
         best = max(pts, key=lambda p: p["tokens_per_s"])
         m = 1.0
         if cfg["k"]:   # mean tokens per speculative iteration E[m+1] (P_ACCEPT = 0.7)
