@@ -130,6 +130,20 @@ int bmc_spec_step(const bmc_t* hs, int L, const void* const* K, const void* cons
                   const void* const* Kd, const void* const* Vd, int k,
                   const void* const* Q, float* const* O);
 
+/* bmc_spec_step_tree: bmc_spec_step with the drafts placed as a token TREE
+   (bmc_spec_write_tree's topology rules): for every layer
+   bmc_append(K[l], V[l]) and bmc_spec_write_tree(Kd[l], Vd[l], k,
+   parent_host), then the verify SDPA of all layers in one launch per 32
+   layers (query row tau = 1 + i of node i sees the committed rows, its
+   ancestors and itself).  parent_host[k]: one topology for every layer and
+   batch row (host array).  Q, O DEVICE as bmc_spec_step (no all-host form).
+   Returns k_adm (the admitted BFS prefix), errors and rollback as
+   bmc_spec_step, plus ARG / UNSUPPORTED for an invalid topology or k > 32
+   (checked before anything is enqueued).  Commit with bmc_commit_path_step. */
+int bmc_spec_step_tree(const bmc_t* hs, int L, const void* const* K, const void* const* V,
+                       const void* const* Kd, const void* const* Vd, int k,
+                       const int* parent_host, const void* const* Q, float* const* O);
+
 /* Bulk (prompt) append: n rows per unit, K and V [B][H_kv][n][D] in the
    cache dtype (device or host pointers).  Contents and lengths equal n
    bmc_append calls (P:L609 in-place writes); the allocation follows prompt
@@ -194,6 +208,16 @@ int bmc_commit_step(const bmc_t* hs, int L, const int* n_accepted_host);
    valid_b += m_b.  Chain commits (bmc_commit*) of a staged tree are a STATE
    error unless they reject everything. */
 int bmc_commit_path(bmc_t h, const int* path_host, const int* m_host, int max_depth);
+
+/* bmc_commit_path_step: bmc_commit_path(hs[l], path_host, m_host, max_depth)
+   for the L layers of one token-tree iteration (the counterpart of
+   bmc_spec_step_tree; every layer accepts the same paths, they share the
+   token sequence).  Layers that share stream, capacity, lengths and staged
+   count get ONE compaction launch per 32 layers, others are committed one by
+   one.  Errors: as bmc_commit_path, checked on every layer before anything
+   is enqueued. */
+int bmc_commit_path_step(const bmc_t* hs, int L, const int* path_host, const int* m_host,
+                         int max_depth);
 
 /* bmc_decode_step: one plain decode step of a whole model, i.e. for every
    layer l = 0..L-1: bmc_append(hs[l], K[l], V[l]) then

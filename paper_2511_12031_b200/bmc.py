@@ -40,6 +40,7 @@ _NAMES = {0: "OK", -1: "ARG", -2: "STATE", -3: "CAPACITY", -4: "OOM", -5: "CUDA"
 EXPORTS = ["bmc_create", "bmc_create_ex", "bmc_append", "bmc_append_n", "bmc_spec_write",
            "bmc_sdpa", "bmc_admissible", "bmc_spec_step",
            "bmc_commit", "bmc_commit_rows", "bmc_commit_step", "bmc_commit_path", "bmc_pool_reserve", "bmc_pool_trim", "bmc_spec_write_tree",
+           "bmc_spec_step_tree", "bmc_commit_path_step",
            "bmc_decode_step", "bmc_destroy", "bmc_stats", "bmc_kv_view",
            "bmc_valid", "bmc_read_cache", "bmc_sync", "bmc_set_option", "bmc_launch_count", "bmc_host_profile", "bmc_last_error"]
 
@@ -84,7 +85,8 @@ def load(path: str = SO_PATH):
         raise RuntimeError(f"libbmc.so not built at {path}: run __graft_entry__.build()")
     L = ctypes.CDLL(path)
     if path != SO_PATH:   # experiment builds may predate newer diagnostics
-        for name in ("bmc_pool_trim", "bmc_host_profile"):
+        for name in ("bmc_pool_trim", "bmc_host_profile", "bmc_spec_step_tree",
+                     "bmc_commit_path_step"):
             if not hasattr(L, name):
                 setattr(L, name, _missing(name))
     vp, i, ll = ctypes.c_void_p, ctypes.c_int, ctypes.c_longlong
@@ -104,6 +106,9 @@ def load(path: str = SO_PATH):
     L.bmc_destroy.argtypes = [vp]
     L.bmc_spec_write_tree.argtypes = [vp, vp, vp, i, ctypes.POINTER(ctypes.c_int)]
     L.bmc_commit_path.argtypes = [vp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int), i]
+    L.bmc_spec_step_tree.argtypes = [vp, i, vp, vp, vp, vp, i, ctypes.POINTER(ctypes.c_int), vp, vp]
+    L.bmc_commit_path_step.argtypes = [vp, i, ctypes.POINTER(ctypes.c_int),
+                                       ctypes.POINTER(ctypes.c_int), i]
     L.bmc_decode_step.argtypes = [vp, i, vp, vp, vp, vp, i]
     L.bmc_stats.argtypes = [vp, ctypes.POINTER(Stats)]
     L.bmc_kv_view.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(i)]
@@ -228,8 +233,7 @@ def bmc_spec_write_tree(h, K_draft, V_draft, k: int, parent) -> int:
                   "bmc_spec_write_tree")
 
 
-def bmc_commit_path(h, paths) -> int:
-    """paths: one list of node indices (root first) per batch row."""
+def _paths(paths):
     depth = max([len(p) for p in paths] + [1])
     flat = (ctypes.c_int * (len(paths) * depth))()
     m = (ctypes.c_int * len(paths))()
@@ -237,7 +241,28 @@ def bmc_commit_path(h, paths) -> int:
         m[b] = len(pth)
         for i, x in enumerate(pth):
             flat[b * depth + i] = int(x)
+    return flat, m, depth
+
+
+def bmc_commit_path(h, paths) -> int:
+    """paths: one list of node indices (root first) per batch row."""
+    flat, m, depth = _paths(paths)
     return _check(load().bmc_commit_path(h, flat, m, depth), "bmc_commit_path")
+
+
+def bmc_spec_step_tree(plan: StepPlan, K, V, Kd, Vd, k: int, parent, Q, O) -> int:
+    """One token-tree iteration over the plan's layers (parent: k ints,
+    breadth-first, -1 = child of the last committed token); returns k_adm."""
+    par = (ctypes.c_int * max(1, k))(*[int(x) for x in parent])
+    return _check(load().bmc_spec_step_tree(plan.hs, plan.L, K, V, Kd, Vd, k, par, Q, O),
+                  "bmc_spec_step_tree")
+
+
+def bmc_commit_path_step(plan: StepPlan, paths) -> int:
+    """Commit one accepted path per batch row in every layer of the plan."""
+    flat, m, depth = _paths(paths)
+    return _check(load().bmc_commit_path_step(plan.hs, plan.L, flat, m, depth),
+                  "bmc_commit_path_step")
 
 
 def bmc_destroy(h) -> int:

@@ -460,13 +460,15 @@ int pointer_kind(const void* ptr) {
   }
   const int kind = (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) ? 0
                    : (a.type == cudaMemoryTypeHost ? 1 : 2);
-  if (kind < 2) {
-    // device and page-locked host allocations are mapped into the unified
-    // address space: remember their whole range (pageable memory is not)
+  if (kind == 0) {
+    // device allocations are mapped into the unified address space: remember
+    // their whole range.  Page-locked host ranges are not cached: after
+    // cudaFreeHost / cudaHostUnregister the same address can come back as
+    // pageable memory, which must take the pageable (synchronising) paths.
     CUdeviceptr base = 0;
     size_t size = 0;
-    const CUdeviceptr q = kind == 0 ? (CUdeviceptr)p : (CUdeviceptr)a.devicePointer;
-    if (drv().ok && q == (CUdeviceptr)p && drv().range(&base, &size, q) == CUDA_SUCCESS &&
+    const CUdeviceptr q = (CUdeviceptr)p;
+    if (drv().ok && drv().range(&base, &size, q) == CUDA_SUCCESS &&
         size > 0) {
       std::lock_guard<std::mutex> lk(g_rmu);
       if (g_ranges.size() >= 256) g_ranges.pop_back();

@@ -131,6 +131,11 @@ struct Cfg {
   // TMEM columns: S^T[b] at b*N, O^T (hi NS cols, lo NS cols) at NB*N
   static constexpr uint32_t TM_O = NB * N;
   static constexpr uint32_t kTmemCols = (NB * N + 2 * NS <= 256) ? 256 : 512;
+#ifndef BMC_TCK_POLY
+#define BMC_TCK_POLY 0
+#endif
+  // every kPoly-th pair of P values is computed on the FMA pipe (0 = none)
+  static constexpr int kPoly = NS >= 64 ? BMC_TCK_POLY : 0;
 };
 
 #ifdef BMC_TC_TRACE
@@ -288,6 +293,26 @@ __device__ __forceinline__ void tmem_st_cols(uint32_t taddr, const float* v) {
 }
 __device__ __forceinline__ void sts_v2(uint32_t addr, uint32_t a, uint32_t b) {
   asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(addr), "r"(a), "r"(b) : "memory");
+}
+// 2^d for two values on the FMA pipe (the MUFU.EX2 unit is 16 lanes / clock / SM,
+// a quarter of the FP32 pipe): d = n + f, n = round(d) by the 1.5 * 2^23
+// magic-number add, f in [-1/2, 1/2]; 2^f by a degree-4 polynomial (relative
+// error 2.7e-6, fitted on Chebyshev nodes) evaluated with FFMA2; 2^n added to
+// the exponent field.  d < -125 is clamped (2^-125 instead of ~0: the row sum
+// is >= 1 whenever a column has a visible key, so it changes nothing readable).
+__device__ __forceinline__ float2 exp2_poly2(float2 d) {
+  d.x = fmaxf(d.x, -125.f);
+  d.y = fmaxf(d.y, -125.f);
+  const float2 mg = make_float2(12582912.f, 12582912.f);
+  const float2 t = __fadd2_rn(d, mg);
+  const float2 r = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = __fadd2_rn(d, make_float2(-r.x, -r.y));
+  float2 q = __ffma2_rn(make_float2(0.0095701f, 0.0095701f), f, make_float2(0.05591786f, 0.05591786f));
+  q = __ffma2_rn(q, f, make_float2(0.24024744f, 0.24024744f));
+  q = __ffma2_rn(q, f, make_float2(0.6931218f, 0.6931218f));
+  q = __ffma2_rn(q, f, make_float2(0.9999993f, 0.9999993f));
+  return make_float2(__uint_as_float(__float_as_uint(q.x) + (__float_as_uint(t.x) << 23)),
+                     __uint_as_float(__float_as_uint(q.y) + (__float_as_uint(t.y) << 23)));
 }
 __device__ __forceinline__ float warp_max(float x) {   // one CREDUX on sm_100a
   float y;
@@ -770,14 +795,22 @@ __global__ void __launch_bounds__(Cfg<N, NG, NS>::kThreads, 1)
           for (int e = 0; e < 4; e += 2) {
             const int c = c0 + e;
             const float2 d = __fadd2_rn(make_float2(x[c], x[c + 1]), make_float2(-mr[e], -mr[e + 1]));
-            const float2 pv = make_float2(fast_exp2(d.x), fast_exp2(d.y));
+            float2 pv;
+            if (C::kPoly && (c / 2) % (C::kPoly ? C::kPoly : 1) == C::kPoly - 1)
+              pv = exp2_poly2(d);
+            else
+              pv = make_float2(fast_exp2(d.x), fast_exp2(d.y));
             l2[c / 2] = __fadd2_rn(l2[c / 2], pv);
             const uint32_t bx = __float_as_uint(pv.x), by = __float_as_uint(pv.y);
             phi[c / 2] = __byte_perm(bx, by, 0x7632);          // upper halves: bf16 hi (truncated)
             const float2 lo = __fadd2_rn(pv, make_float2(-__uint_as_float(bx & 0xffff0000u),
                                                           -__uint_as_float(by & 0xffff0000u)));
+#ifdef BMC_TCK_LO_TRUNC
+            plo[c / 2] = __byte_perm(__float_as_uint(lo.x), __float_as_uint(lo.y), 0x7632);
+#else
             const __nv_bfloat162 lb = __floats2bfloat162_rn(lo.x, lo.y);
             plo[c / 2] = *reinterpret_cast<const uint32_t*>(&lb);
+#endif
           }
         }
         // P^T[pb] was last read by the O^T MMAs of tile tc - NBP

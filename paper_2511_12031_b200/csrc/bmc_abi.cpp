@@ -595,6 +595,7 @@ static void undo_layer_step(bmc_t h, bool appended) {
   h->st.append_written_bytes -= 2LL * h->U * h->n_draft * h->row_bytes;
   h->n_draft = 0;
   h->staged = 0;
+  h->tree = 0;
   h->kd = h->vd = nullptr;
   if (appended) {
     for (auto& v : h->valid) v -= 1;
@@ -690,6 +691,8 @@ int bmc_append_n(bmc_t h, const void* K, const void* V, int n) {
 }
 
 static int spec_write_impl(bmc_t h, const void* K_draft, const void* V_draft, int k);
+static void set_tree(bmc_t h, const int* parent, int k_adm);
+static int check_parents(const int* parent, int k);
 
 int bmc_spec_write(bmc_t h, const void* K_draft, const void* V_draft, int k) {
   int rc = enter(h);
@@ -739,18 +742,11 @@ int bmc_spec_write_tree(bmc_t h, const void* K_draft, const void* V_draft, int k
   int rc = enter(h);
   if (rc) return rc;
   if (k < 0) return fail(BMC_ERR_ARG, "k=%d < 0", k);
-  if (k > 32) return fail(BMC_ERR_UNSUPPORTED, "token trees of more than 32 nodes");
-  if (k > 0 && !parent_host) return fail(BMC_ERR_ARG, "parent is null");
-  for (int i = 0; i < k; ++i)
-    if (parent_host[i] < -1 || parent_host[i] >= i)
-      return fail(BMC_ERR_ARG, "parent[%d]=%d not in [-1, %d) (breadth-first order)", i,
-                  parent_host[i], i);
-  const int k_adm = bmc_spec_write(h, K_draft, V_draft, k);
+  rc = check_parents(parent_host, k);
+  if (rc) return rc;
+  const int k_adm = spec_write_impl(h, K_draft, V_draft, k);
   if (k_adm < 0) return k_adm;
-  for (int i = 0; i < 32; ++i) h->anc[i] = 0;
-  for (int i = 0; i < k_adm; ++i)
-    h->anc[i] = (1u << i) | (parent_host[i] >= 0 ? h->anc[parent_host[i]] : 0u);
-  h->tree = k_adm > 0;
+  set_tree(h, parent_host, k_adm);
   return k_adm;
 }
 
@@ -869,12 +865,49 @@ static int spec_step_host(const bmc_t* hs, int L, const void* const* K, const vo
                           const void* const* Kd, const void* const* Vd, int k,
                           const void* const* Q, float* const* O);
 
+// Token-tree form of the drafts just written by spec_write_impl (parent
+// validated by the caller): ancestor masks for the verify kernels.
+static void set_tree(bmc_t h, const int* parent, int k_adm) {
+  for (int i = 0; i < 32; ++i) h->anc[i] = 0;
+  for (int i = 0; i < k_adm; ++i)
+    h->anc[i] = (1u << i) | (parent[i] >= 0 ? h->anc[parent[i]] : 0u);
+  h->tree = k_adm > 0;
+}
+
+static int check_parents(const int* parent, int k) {
+  if (k > 32) return fail(BMC_ERR_UNSUPPORTED, "token trees of more than 32 nodes");
+  if (k > 0 && !parent) return fail(BMC_ERR_ARG, "parent is null");
+  for (int i = 0; i < k; ++i)
+    if (parent[i] < -1 || parent[i] >= i)
+      return fail(BMC_ERR_ARG, "parent[%d]=%d not in [-1, %d) (breadth-first order)", i, parent[i], i);
+  return 0;
+}
+
+static int spec_step_impl(const bmc_t* hs, int L, const void* const* K, const void* const* V,
+                          const void* const* Kd, const void* const* Vd, int k,
+                          const int* parent, const void* const* Q, float* const* O);
+
 int bmc_spec_step(const bmc_t* hs, int L, const void* const* K, const void* const* V,
                   const void* const* Kd, const void* const* Vd, int k, const void* const* Q,
                   float* const* O) {
+  return spec_step_impl(hs, L, K, V, Kd, Vd, k, nullptr, Q, O);
+}
+
+int bmc_spec_step_tree(const bmc_t* hs, int L, const void* const* K, const void* const* V,
+                       const void* const* Kd, const void* const* Vd, int k,
+                       const int* parent_host, const void* const* Q, float* const* O) {
+  if (k < 0) return fail(BMC_ERR_ARG, "k=%d < 0", k);
+  int rc = check_parents(parent_host, k);
+  if (rc) return rc;
+  return spec_step_impl(hs, L, K, V, Kd, Vd, k, parent_host, Q, O);
+}
+
+static int spec_step_impl(const bmc_t* hs, int L, const void* const* K, const void* const* V,
+                          const void* const* Kd, const void* const* Vd, int k,
+                          const int* parent, const void* const* Q, float* const* O) {
   if (!hs || L < 1 || !K || !V || !Q || !O || k < 0 || (k > 0 && (!Kd || !Vd)))
     return fail(BMC_ERR_ARG, "null argument or k < 0");
-  {
+  if (!parent) {
     // all-host arguments take the pipelined host-I/O path
     bool all_host = true;
     for (int l = 0; l < L && all_host; ++l)
@@ -951,6 +984,7 @@ int bmc_spec_step(const bmc_t* hs, int L, const void* const* K, const void* cons
       if (rc) return rollback_chunk(hs, 0, l, l, rc);
       if (!rc && k > 0) {
         rc = spec_write_impl(hs[l], Kd[l], Vd[l], k);
+        if (rc >= 0 && parent) set_tree(hs[l], parent, rc);
         if (rc > 0) rc = 0;
       }
       if (rc) return rollback_chunk(hs, 0, l + 1, l + 1, rc);
@@ -974,6 +1008,7 @@ int bmc_spec_step(const bmc_t* hs, int L, const void* const* K, const void* cons
       if (k > 0) {
         rc = spec_write_impl(hs[l], Kd[l], Vd[l], k);
         if (rc < 0) return rollback_chunk(hs, l0, l + 1, l + 1, rc);
+        if (parent) set_tree(hs[l], parent, rc);
       }
     }
     // descriptors only after every append of the chunk: an OOM fallback in
@@ -1309,9 +1344,9 @@ static int commit_impl(bmc_t h, const int* m) {
   return 0;
 }
 
-int bmc_commit_path(bmc_t h, const int* path_host, const int* m_host, int max_depth) {
-  int rc = enter(h);
-  if (rc) return rc;
+// The accepted paths must be root-first, parent-linked node lists of the
+// staged tree (or chain) of h.
+static int check_path(bmc_t h, const int* path_host, const int* m_host, int max_depth) {
   if (!m_host || max_depth < 0) return fail(BMC_ERR_ARG, "null argument");
   for (int b = 0; b < h->B; ++b) {
     const int m = m_host[b];
@@ -1327,27 +1362,87 @@ int bmc_commit_path(bmc_t h, const int* path_host, const int* m_host, int max_de
       if ((has_par ? par : -1) != want) return fail(BMC_ERR_ARG, "row %d: path is not parent-linked", b);
     }
   }
+  return 0;
+}
+
+static void fill_path(bmc_t h, const int* path_host, const int* m_host, int max_depth,
+                      bmc::PathArgs* a) {
+  a->B = h->B;
+  a->H_kv = h->H_kv;
+  a->staged = h->staged;
+  a->cap = h->cap;
+  a->row_bytes = h->row_bytes;
+  for (int b = 0; b < h->B; ++b) {
+    a->valid[b] = h->valid[b];
+    a->m[b] = (unsigned char)m_host[b];
+    for (int i = 0; i < m_host[b]; ++i) a->path[b][i] = (unsigned char)path_host[b * max_depth + i];
+  }
+}
+
+static void path_committed(bmc_t h, const int* m_host) {
+  for (int b = 0; b < h->B; ++b) h->valid[b] += m_host[b];   // P:L447
+  h->staged = 0;
+  h->tree = 0;
+}
+
+int bmc_commit_path(bmc_t h, const int* path_host, const int* m_host, int max_depth) {
+  int rc = enter(h);
+  if (rc) return rc;
+  rc = check_path(h, path_host, m_host, max_depth);
+  if (rc) return rc;
   if (h->n_app || h->n_draft) {
     rc = flush_pending(h);
     if (rc) return rc;
   }
   bmc::PathArgs a;
-  a.k = h->kbuf.ptr;
-  a.v = h->vbuf.ptr;
-  a.B = h->B;
-  a.H_kv = h->H_kv;
-  a.staged = h->staged;
-  a.cap = h->cap;
-  a.row_bytes = h->row_bytes;
-  for (int b = 0; b < h->B; ++b) {
-    a.valid[b] = h->valid[b];
-    a.m[b] = (unsigned char)m_host[b];
-    for (int i = 0; i < m_host[b]; ++i) a.path[b][i] = (unsigned char)path_host[b * max_depth + i];
-  }
+  fill_path(h, path_host, m_host, max_depth, &a);
+  a.L = 1;
+  a.k[0] = h->kbuf.ptr;
+  a.v[0] = h->vbuf.ptr;
   CK(h, bmc::launch_commit_path(a, h->stream), "commit_path");
-  for (int b = 0; b < h->B; ++b) h->valid[b] += m_host[b];
-  h->staged = 0;
-  h->tree = 0;
+  path_committed(h, m_host);
+  return 0;
+}
+
+int bmc_commit_path_step(const bmc_t* hs, int L, const int* path_host, const int* m_host,
+                         int max_depth) {
+  if (!hs || L < 1) return fail(BMC_ERR_ARG, "null argument or L < 1");
+  // validate every layer before enqueueing anything (as bmc_commit_path)
+  for (int l = 0; l < L; ++l) {
+    int rc = enter(hs[l]);
+    if (rc) return rc;
+    if (hs[l]->B != hs[0]->B) return fail(BMC_ERR_ARG, "layer %d: batch differs from layer 0", l);
+    rc = check_path(hs[l], path_host, m_host, max_depth);
+    if (rc) return rc;
+  }
+  const bmc_t h0 = hs[0];
+  bool fused = true;
+  for (int l = 0; l < L; ++l) {
+    const bmc_t a = hs[l];
+    if (a->n_app || a->n_draft || a->H_kv != h0->H_kv || a->stream != h0->stream ||
+        a->device != h0->device || a->cap != h0->cap || a->row_bytes != h0->row_bytes ||
+        a->staged != h0->staged || a->valid != h0->valid)
+      fused = false;
+  }
+  if (!fused) {
+    for (int l = 0; l < L; ++l) {
+      int rc = bmc_commit_path(hs[l], path_host, m_host, max_depth);
+      if (rc) return rc;
+    }
+    return 0;
+  }
+  // one launch per kMaxZeroLayers layers: accepted rows moved, the rest zeroed
+  bmc::PathArgs a;
+  fill_path(h0, path_host, m_host, max_depth, &a);
+  for (int l0 = 0; l0 < L; l0 += bmc::kMaxZeroLayers) {
+    a.L = std::min(bmc::kMaxZeroLayers, L - l0);
+    for (int l = 0; l < a.L; ++l) {
+      a.k[l] = hs[l0 + l]->kbuf.ptr;
+      a.v[l] = hs[l0 + l]->vbuf.ptr;
+    }
+    CK(h0, bmc::launch_commit_path(a, h0->stream), "commit_path");
+  }
+  for (int l = 0; l < L; ++l) path_committed(hs[l], m_host);
   return 0;
 }
 

@@ -47,7 +47,9 @@ struct ZeroArgs {
 cudaError_t launch_zero_rows(const ZeroArgs& a, cudaStream_t s);
 
 struct PathArgs {
-  void* k; void* v;                       // [U][cap][D]
+  void* k[kMaxZeroLayers];                // per layer [U][cap][D] (L layers of one shape)
+  void* v[kMaxZeroLayers];
+  int L;
   int B, H_kv, staged;
   long long cap;
   int row_bytes;
@@ -56,7 +58,7 @@ struct PathArgs {
   unsigned char path[BMC_MAX_B][32];      // accepted node indices, root first
 };
 // Compact the accepted tree path of every unit behind its committed rows and
-// zero the remaining staged rows (one warp per (unit, tensor)).
+// zero the remaining staged rows (one warp per (unit, tensor, layer)).
 cudaError_t launch_commit_path(const PathArgs& a, cudaStream_t s);
 
 // One layer of an attention launch.

@@ -158,10 +158,11 @@ cudaError_t launch_zero_rows(const ZeroArgs& a, cudaStream_t s) {
 __global__ void commit_path_kernel(const __grid_constant__ PathArgs a) {
   const long long u = blockIdx.x;
   const int tensor = blockIdx.y;
+  const int l = blockIdx.z;
   const int b = (int)(u / a.H_kv);
   const int lane = threadIdx.x;
   const int row_vec = a.row_bytes / 16;
-  int4* base = (int4*)(tensor == 0 ? a.k : a.v) + (u * a.cap + a.valid[b]) * row_vec;
+  int4* base = (int4*)(tensor == 0 ? a.k[l] : a.v[l]) + (u * a.cap + a.valid[b]) * row_vec;
   const int m = a.m[b];
   for (int i = 0; i < m; ++i) {
     const int src = a.path[b][i];
@@ -175,8 +176,8 @@ __global__ void commit_path_kernel(const __grid_constant__ PathArgs a) {
 
 cudaError_t launch_commit_path(const PathArgs& a, cudaStream_t s) {
   const long long U = (long long)a.B * a.H_kv;
-  if (U == 0 || a.staged == 0) return cudaSuccess;
-  commit_path_kernel<<<dim3((unsigned)U, 2), 32, 0, s>>>(a);
+  if (U == 0 || a.staged == 0 || a.L < 1) return cudaSuccess;
+  commit_path_kernel<<<dim3((unsigned)U, 2, (unsigned)a.L), 32, 0, s>>>(a);
   count_launch();
   return cudaGetLastError();
 }

@@ -262,6 +262,39 @@ class Model:
             self._compare(outs, refs)
         return k_adm
 
+    def spec_step_tree(self, k, parent, check=True):
+        """One token-tree iteration (append + a k-node tree + verify) of every
+        layer through bmc_spec_step_tree; returns k_adm."""
+        k_adm = bmc.bmc_admissible(self.gpu[0].h, k)
+        t = 1 + k_adm
+        xs = self._inputs(t, max(k, 1))
+        dev = [{key: v.cuda() for key, v in x.items()} for x in xs]
+        outs = [torch.empty(self.B, self.H_q, t, self.D, device="cuda") for _ in range(self.L)]
+        p = self.plan
+        got = bmc.bmc_spec_step_tree(p, p.ptrs([d["k"] for d in dev]),
+                                     p.ptrs([d["v"] for d in dev]), p.ptrs([d["kd"] for d in dev]),
+                                     p.ptrs([d["vd"] for d in dev]), k, parent,
+                                     p.ptrs([d["q"] for d in dev]), p.ptrs(outs))
+        assert got == k_adm, (got, k_adm)
+        self.keep = dev
+        refs = []
+        for l in range(self.L):
+            o = self.orc[l]
+            o.append(xs[l]["k"], xs[l]["v"])
+            if k > 0:
+                assert o.spec_write_tree(xs[l]["kd"], xs[l]["vd"], k, parent) == k_adm
+            self._account(l, t)
+            refs.append(o.sdpa(xs[l]["q"], -1) if check else None)
+        if check:
+            torch.cuda.synchronize()
+            self._compare(outs, refs)
+        return k_adm
+
+    def commit_path_step(self, paths):
+        bmc.bmc_commit_path_step(self.plan, paths)
+        for o in self.orc:
+            o.commit_path(paths)
+
     def commit_step(self, m):
         bmc.bmc_commit_step(self.plan, m)
         for o in self.orc:

@@ -61,8 +61,8 @@ def _run_decode_fullsize(B, H_kv, H_q, D, N, r, L, sample_steps, sample_units, s
 
 
 @pytest.mark.parametrize("cfg", [
-    # BASELINE configs[1]: Llama-2-7B shape, B=16, context 4096, r = 64 (bench default)
-    dict(B=16, H_kv=32, H_q=32, D=128, N=4096, r=64, L=2),
+    # BASELINE configs[1]: Llama-2-7B shape, B=16, context 4096, r = 128 (bench default)
+    dict(B=16, H_kv=32, H_q=32, D=128, N=4096, r=128, L=2),
     # BASELINE configs[3] per GPU: Llama-3-8B GQA (32 q / 8 kv heads), B=64, context 8192
     # (two layers: the fused multi-layer tcgen05 launch of the GQA decode step)
     dict(B=64, H_kv=8, H_q=32, D=128, N=8192, r=128, L=2),

@@ -53,6 +53,74 @@ def test_full_depth_spec_step_70b_heads():
     m.close()
 
 
+def _bfs_tree(k, seed):
+    import numpy as np
+    rng = np.random.default_rng(seed)
+    return [-1] + [int(rng.integers(-1, i)) for i in range(1, k)]
+
+
+def _tree_path(parent, k_adm, salt):
+    """A root-to-node path among the admitted nodes (empty every 5th call)."""
+    if k_adm == 0 or salt % 5 == 4:
+        return []
+    node = (salt * 7 + 3) % k_adm
+    path = []
+    while node >= 0:
+        path.append(node)
+        node = parent[node]
+    return path[::-1]
+
+
+@pytest.mark.parametrize("L,B,H_kv,H_q,k,r", [(32, 2, 32, 32, 26, 40),   # E8 heads, full depth
+                                              (3, 3, 2, 8, 9, 24),      # GQA, M = 40
+                                              (34, 1, 1, 2, 26, 64),    # 32 + 2 layers
+                                              (3, 2, 2, 2, 32, 48)])    # largest tree
+def test_tree_step_fused(L, B, H_kv, H_q, k, r):
+    """bmc_spec_step_tree + bmc_commit_path_step (the token-tree bench
+    mode's calls: every layer's append and k-node tree, one verify launch per
+    32 layers, one path-compaction launch per 32 layers) against per-layer
+    oracles: every output row (ancestor mask), then caches,
+    lengths and ledgers bit-exact; per-row accepted paths of different
+    lengths; topologies change every iteration."""
+    m = Model(L, B, H_kv, H_q, 128, r, 200, seed=26 + k)
+    it = 0
+    while m.orc[0].stats()["valid_max"] < 200 - k - 2:
+        parent = _bfs_tree(k, 100 + it)
+        k_adm = m.spec_step_tree(k, parent, check=(it % 2 == 0))
+        m.commit_path_step([_tree_path(parent, k_adm, it + 3 * b) for b in range(B)])
+        it += 1
+        if it % 7 == 0:
+            m.check_state(layers=(0, L - 1))
+    m.check_state()
+    m.close()
+
+
+def test_tree_step_errors_leave_state():
+    """Invalid topologies, k > 32 and paths that are not parent-linked fail
+    before anything is enqueued (every layer unchanged)."""
+    m = Model(3, 2, 2, 2, 128, 16, 64, seed=3)
+    m.decode_step()
+    before = [(g.stats(), g.valid()) for g in m.gpu]
+    p = m.plan
+    z = [torch.zeros(2, 2, 128, dtype=torch.bfloat16, device="cuda") for _ in range(3)]
+    zd = [torch.zeros(2, 2, 33, 128, dtype=torch.bfloat16, device="cuda") for _ in range(3)]
+    q = [torch.zeros(2, 2, 34, 128, dtype=torch.bfloat16, device="cuda") for _ in range(3)]
+    o = [torch.empty(2, 2, 34, 128, device="cuda") for _ in range(3)]
+    args = (p.ptrs(z), p.ptrs(z), p.ptrs(zd), p.ptrs(zd))
+    with pytest.raises(bmc.BMCError):
+        bmc.bmc_spec_step_tree(p, *args, 3, [-1, 1, 0], p.ptrs(q), p.ptrs(o))   # parent >= i
+    with pytest.raises(bmc.BMCError):
+        bmc.bmc_spec_step_tree(p, *args, 33, [-1] * 33, p.ptrs(q), p.ptrs(o))   # k > 32
+    assert [(g.stats(), g.valid()) for g in m.gpu] == before
+    k_adm = m.spec_step_tree(4, [-1, 0, 0, 1])
+    assert k_adm == 4
+    with pytest.raises(bmc.BMCError):
+        bmc.bmc_commit_path_step(p, [[0, 2, 1], [0]])   # node 1 does not hang off node 2
+    m.commit_path_step([[0, 1, 3], []])
+    m.check_state()
+    m.close()
+
+
 @pytest.mark.parametrize("policy", ["iterative", "upfront"])
 @pytest.mark.parametrize("H_kv,H_q,k", [(2, 2, 4), (2, 16, 4), (1, 8, 8)])
 def test_baselines_under_speculation(policy, H_kv, H_q, k):
