@@ -12,17 +12,20 @@ import torch  # noqa: E402
 from paper_2511_12031_b200 import bmc  # noqa: E402
 
 L, B, H, D, N, r = 32, 16, 32, 128, 4096, 128
+HQ = H
+if "--l3" in sys.argv:      # BASELINE configs[3]: Llama-3-8B GQA, B=64, 0 -> 8192
+    B, H, HQ, N = 64, 8, 32, 8192
 ARENA = 0 if "--vmm" in sys.argv else 1   # BMC_OPT_ARENA: 0 VMM slots (premapped), 1 pool
 if "--reserve" in sys.argv:                # map the peak footprint into the pool up front
     bmc.load()
     bmc.bmc_pool_reserve(0, 2 * B * H * N * D * 2 * (L + L))
 k = [torch.randn(B, H, D, device="cuda").to(torch.bfloat16) for _ in range(L)]
-q = [torch.randn(B, H, 1, D, device="cuda").to(torch.bfloat16) for _ in range(L)]
-o = [torch.empty(B, H, 1, D, device="cuda") for _ in range(L)]
+q = [torch.randn(B, HQ, 1, D, device="cuda").to(torch.bfloat16) for _ in range(L)]
+o = [torch.empty(B, HQ, 1, D, device="cuda") for _ in range(L)]
 
 
 def gen(tag):
-    hs = [bmc.KVCache(B, H, H, D, r, N, dtype="bf16") for _ in range(L)]
+    hs = [bmc.KVCache(B, H, HQ, D, r, N, dtype="bf16") for _ in range(L)]
     for h in hs:
         h.set_option(bmc.BMC_OPT_ARENA, ARENA)
     plan = bmc.StepPlan(hs)
@@ -43,6 +46,8 @@ def gen(tag):
     grow = [n for n in range(2, N + 1) if (n - 1) % r == 0]
     gs = sum(g[n - 1] for n in grow)
     hg = sum(host[n] for n in grow) * 1e3
+    gb = sum(2 * B * H * D * 2 * L * ((n - 1) + (n - 1 + r)) for n in grow) / 1e9
+    print(f"{tag}: growth launches {gb / (gs / 1e3) :.0f} GB/s algorithmic (incl. host gaps)")
     print(f"{tag}: wall {1e3 * (T1 - T0):.0f} ms, gpu {sum(g):.0f} ms; {len(grow)} growth steps: "
           f"gpu {gs:.0f} ms, host {hg:.0f} ms; other steps: host {1e3 * sum(host) - hg:.0f} ms; "
           f"max growth host {max(host[n] for n in grow) * 1e3:.1f} ms", flush=True)
