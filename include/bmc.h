@@ -272,7 +272,10 @@ int bmc_sync(bmc_t h);
                               the lanes), 3 tcgen05 with queries on the lanes,
                               4 tcgen05 with keys on the lanes (G*t <= 80)
      3 BMC_OPT_ARENA          0 VMM ping-pong slots, 1 stream-ordered pool
-                              (default; takes effect at the next growth)
+                              (default), 2 the device's two-ended growth
+                              region (bmc_region_reserve; the pool when the
+                              region is absent or full); takes effect at the
+                              next growth
      4 BMC_OPT_SKIP_PADDING   1 = length-aware ABLATION: SDPA streams only the
                               rows some query sees instead of all cap rows
                               (not the method: P:L441, L853; results are
@@ -317,6 +320,21 @@ int bmc_set_option(bmc_t h, int key, long long value);
    process like a serving deployment's KV budget.  Errors: ARG (bytes < 0),
    OOM, CUDA. */
 int bmc_pool_reserve(int device, long long bytes);
+
+/* bmc_region_reserve: (re)create the two-ended growth region of `bytes` on
+   `device` (-1 = current; 0 bytes frees it) for handles with BMC_OPT_ARENA =
+   2.  All layers of a model grow in the same step,
+   so a growth places each new buffer at the end of the region opposite to
+   the buffer it replaces and pops the released old buffers off the other
+   end: no fragmentation, no driver call and no host wait per growth (the
+   stream-ordered pool stalled the host for up to ~1 s per growth step on the
+   L3-8B workload, profiles/r02_growth_cost_l3.txt).  Sized for the peak of
+   a copy growth: old + new buffers of every layer of a step, i.e. about
+   twice the final cache.  Space released on one stream is handed to
+   another only after that stream passed the release (events).  Errors: ARG
+   (bytes < 0), STATE (buffers of the current region are still live), OOM,
+   CUDA. */
+int bmc_region_reserve(int device, long long bytes);
 
 /* bmc_pool_trim: wait for the device, then return the growth pool's unused
    memory (blocks no live buffer uses, e.g. a previous workload's or a

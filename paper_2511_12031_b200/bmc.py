@@ -29,6 +29,7 @@ BMC_OPT_ATTN_CTAS, BMC_OPT_ATTN_PATH, BMC_OPT_ARENA, BMC_OPT_SKIP_PADDING = 1, 2
 BMC_OPT_COPY_ON_READ = 5
 BMC_OPT_TCK_GROUPS = 6
 BMC_OPT_FAULT_OOM = 7
+ARENA_VMM, ARENA_POOL, ARENA_REGION = 0, 1, 2
 BMC_OPT_TCK_PREFETCH = 8
 POLICIES = {"bmc": BMC_POLICY_BMC, "iterative": BMC_POLICY_ITERATIVE,
             "upfront": BMC_POLICY_UPFRONT}
@@ -40,7 +41,7 @@ _NAMES = {0: "OK", -1: "ARG", -2: "STATE", -3: "CAPACITY", -4: "OOM", -5: "CUDA"
 EXPORTS = ["bmc_create", "bmc_create_ex", "bmc_append", "bmc_append_n", "bmc_spec_write",
            "bmc_sdpa", "bmc_admissible", "bmc_spec_step",
            "bmc_commit", "bmc_commit_rows", "bmc_commit_step", "bmc_commit_path", "bmc_pool_reserve", "bmc_pool_trim", "bmc_spec_write_tree",
-           "bmc_spec_step_tree", "bmc_commit_path_step",
+           "bmc_spec_step_tree", "bmc_commit_path_step", "bmc_region_reserve",
            "bmc_decode_step", "bmc_destroy", "bmc_stats", "bmc_kv_view",
            "bmc_valid", "bmc_read_cache", "bmc_sync", "bmc_set_option", "bmc_launch_count", "bmc_host_profile", "bmc_last_error"]
 
@@ -86,7 +87,7 @@ def load(path: str = SO_PATH):
     L = ctypes.CDLL(path)
     if path != SO_PATH:   # experiment builds may predate newer diagnostics
         for name in ("bmc_pool_trim", "bmc_host_profile", "bmc_spec_step_tree",
-                     "bmc_commit_path_step"):
+                     "bmc_commit_path_step", "bmc_region_reserve"):
             if not hasattr(L, name):
                 setattr(L, name, _missing(name))
     vp, i, ll = ctypes.c_void_p, ctypes.c_int, ctypes.c_longlong
@@ -103,6 +104,7 @@ def load(path: str = SO_PATH):
     L.bmc_commit_step.argtypes = [vp, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
     L.bmc_pool_reserve.argtypes = [ctypes.c_int, ctypes.c_longlong]
     L.bmc_pool_trim.argtypes = [ctypes.c_int]
+    L.bmc_region_reserve.argtypes = [ctypes.c_int, ctypes.c_longlong]
     L.bmc_destroy.argtypes = [vp]
     L.bmc_spec_write_tree.argtypes = [vp, vp, vp, i, ctypes.POINTER(ctypes.c_int)]
     L.bmc_commit_path.argtypes = [vp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int), i]
@@ -183,6 +185,11 @@ def bmc_pool_reserve(device: int, nbytes: int) -> int:
 
 def bmc_pool_trim(device: int = -1) -> int:
     return _check(load().bmc_pool_trim(device), "bmc_pool_trim")
+
+
+def bmc_region_reserve(device: int, nbytes: int) -> int:
+    """(Re)create the two-ended growth region (BMC_OPT_ARENA = 2); 0 frees it."""
+    return _check(load().bmc_region_reserve(device, nbytes), "bmc_region_reserve")
 
 
 def bmc_commit(h, n_accepted: int) -> int:

@@ -22,6 +22,20 @@
 //     layer-growth on B200) leave the host's critical path.
 //   kind 1 (pool): cudaMallocFromPoolAsync / cudaFreeAsync on a per-device
 //     memory pool with an unbounded release threshold (stream-ordered reuse).
+//   kind 2 (region): a two-ended stack over one device region reserved up
+//     front (region_reserve).  All layers of a model grow in the same step,
+//     so a growth moves every buffer of a step to the end of the region
+//     opposite to the one holding the buffers it replaces: the new buffers
+//     are pushed onto that end, the old ones popped off the other end once
+//     released.  The region never fragments and a growth is pointer
+//     arithmetic (no driver call, no host wait), in a region of twice the
+//     final cache (the peak of a copy growth: old and new buffers of every
+//     layer of a step at once).  The stream-ordered pool and the VMM slots
+//     stalled the host for up to ~1 s at some L3-8B growth steps (a
+//     fragmented pool mapping memory and waiting for the device;
+//     cuMemMap ~5 ms per chunk under full HBM load), profiles/
+//     r02_growth_cost_l3.txt.  A request the region cannot hold falls back to
+//     the pool.
 #include <cstdlib>
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -118,6 +132,8 @@ struct Arena {
 };
 
 static int cu_ok(CUresult r) { return r == CUDA_SUCCESS ? 0 : BMC_ERR_CUDA; }
+static bool region_alloc(int device, size_t bytes, int pref, cudaStream_t s, Buffer* out);
+static int region_release(int device, Buffer* b, cudaStream_t s);
 
 static size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
@@ -266,6 +282,11 @@ int arena_alloc(Arena* a, int tensor, size_t bytes, int kind, const Buffer* keep
     a->live[tensor] = slot;
     return 0;
   }
+  if (kind == 2) {
+    // the end opposite to the live buffer (a copy growth: both live at once)
+    const int pref = (keep && keep->ptr && keep->kind == 2) ? 1 - keep->slot : 0;
+    if (region_alloc(a->device, bytes, pref, s, out)) return 0;
+  }
   cudaMemPool_t mp;
   {
     std::lock_guard<std::mutex> lk(g_mu);
@@ -291,6 +312,8 @@ int arena_release(Arena* a, Buffer* b, cudaStream_t s) {
   int rc = 0;
   if (b->kind == 1) {
     rc = cudaFreeAsync(b->ptr, s) == cudaSuccess ? 0 : BMC_ERR_CUDA;
+  } else if (b->kind == 2) {
+    rc = region_release(a->device, b, s);
   } else {
     // VMM slot: the mapping persists for the next growth (see header); nothing
     // to do until the arena is destroyed
@@ -428,6 +451,132 @@ void arena_destroy(Arena* a) {
   if (a->base) drv().addr_free(a->base, 4 * a->slot_bytes);
   g_arenas.erase(a);
   delete a;
+}
+
+// ------------------------------------------------- two-ended growth region
+namespace {
+struct RBlk {
+  size_t off, bytes;
+  bool freed;
+  cudaStream_t s;        // releasing stream
+  cudaEvent_t ev;        // recorded on s at the release
+};
+struct Region {
+  uint8_t* base = nullptr;
+  size_t size = 0;
+  std::vector<RBlk> stk[2];   // end 0 grows up from 0, end 1 down from size
+  size_t used[2] = {0, 0};
+  // latest popped release per stream: space it freed may be handed out on
+  // another stream only after it (same-stream reuse is ordered already)
+  std::vector<std::pair<cudaStream_t, cudaEvent_t>> fence;
+  std::vector<cudaEvent_t> spare;
+};
+std::mutex g_regmu;
+std::map<int, Region*> g_region;
+constexpr size_t kRegionAlign = 4096;
+
+cudaEvent_t region_event(Region* r) {
+  if (!r->spare.empty()) {
+    cudaEvent_t e = r->spare.back();
+    r->spare.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return e;
+}
+}  // namespace
+
+int region_reserve(int device, size_t bytes) {
+  std::lock_guard<std::mutex> lk(g_regmu);
+  Region*& r = g_region[device];
+  if (r && (!r->stk[0].empty() || !r->stk[1].empty())) return BMC_ERR_STATE;   // buffers live
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != device && cudaSetDevice(device) != cudaSuccess) return BMC_ERR_CUDA;
+  int rc = 0;
+  if (r) {
+    cudaDeviceSynchronize();
+    forget_range(r->base);
+    cudaFree(r->base);
+    for (auto& f : r->fence) cudaEventDestroy(f.second);
+    for (auto e : r->spare) cudaEventDestroy(e);
+    delete r;
+    r = nullptr;
+  }
+  if (bytes > 0) {
+    void* p = nullptr;
+    const cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      rc = e == cudaErrorMemoryAllocation ? BMC_ERR_OOM : BMC_ERR_CUDA;
+    } else {
+      r = new Region();
+      r->base = static_cast<uint8_t*>(p);
+      r->size = bytes / kRegionAlign * kRegionAlign;
+    }
+  }
+  if (prev != device) cudaSetDevice(prev);
+  return rc;
+}
+
+// A block of the region at end `pref` (else the other end) on stream s;
+// returns false when the region is absent or full.
+static bool region_alloc(int device, size_t bytes, int pref, cudaStream_t s, Buffer* out) {
+  std::lock_guard<std::mutex> lk(g_regmu);
+  auto it = g_region.find(device);
+  if (it == g_region.end() || !it->second) return false;
+  Region* r = it->second;
+  bytes = (bytes + kRegionAlign - 1) / kRegionAlign * kRegionAlign;
+  for (int k = 0; k < 2; ++k) {
+    const int e = k == 0 ? pref : 1 - pref;
+    if (r->used[0] + r->used[1] + bytes > r->size) continue;
+    const size_t off = e == 0 ? r->used[0] : r->size - r->used[1] - bytes;
+    r->used[e] += bytes;
+    r->stk[e].push_back(RBlk{off, bytes, false, nullptr, nullptr});
+    for (auto& f : r->fence)
+      if (f.first != s) cudaStreamWaitEvent(s, f.second, 0);
+    out->ptr = r->base + off;
+    out->bytes = bytes;
+    out->slot = e;
+    out->kind = 2;
+    return true;
+  }
+  return false;
+}
+
+static int region_release(int device, Buffer* b, cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(g_regmu);
+  auto it = g_region.find(device);
+  if (it == g_region.end() || !it->second) return BMC_ERR_CUDA;
+  Region* r = it->second;
+  const size_t off = static_cast<uint8_t*>(b->ptr) - r->base;
+  auto& st = r->stk[b->slot];
+  size_t i = st.size();
+  while (i > 0 && st[i - 1].off != off) --i;
+  if (i == 0) return BMC_ERR_CUDA;
+  RBlk& blk = st[i - 1];
+  blk.freed = true;
+  blk.s = s;
+  blk.ev = region_event(r);
+  if (!blk.ev || cudaEventRecord(blk.ev, s) != cudaSuccess) return BMC_ERR_CUDA;
+  while (!st.empty() && st.back().freed) {   // pop released blocks off this end
+    RBlk t = st.back();
+    st.pop_back();
+    r->used[b->slot] -= t.bytes;
+    bool seen = false;
+    for (auto& f : r->fence)
+      if (f.first == t.s) {   // a later release on the same stream covers the earlier one
+        r->spare.push_back(f.second);
+        f.second = t.ev;
+        seen = true;
+      }
+    if (!seen) r->fence.emplace_back(t.s, t.ev);
+  }
+  return 0;
 }
 
 // ------------------------------------------------------ pointer classes

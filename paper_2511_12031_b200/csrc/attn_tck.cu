@@ -48,7 +48,6 @@
 // realloc kernel and the new buffer is written once, never read back.
 #include <cuda.h>
 #include <cuda_bf16.h>
-#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <limits.h>
 #include <math.h>
@@ -101,11 +100,7 @@ struct Cfg {
   static constexpr int KS = (N <= 16 || QTMA) ? 3 : 2;      // K ring stages
 #else
   static constexpr int NBP = (N < 64 || QTMA) ? 2 : 1;      // P^T buffers
-#ifdef BMC_TCK_KS3
-  static constexpr int KS = (N <= 16 || QTMA) ? 3 : 2;      // K ring stages
-#else
   static constexpr int KS = N <= 16 ? 3 : 2;                // K ring stages
-#endif
 #endif
   static constexpr int VS = N <= 32 ? 3 : 2;                // V ring stages
   static constexpr int NQK = QTMA ? NS : N;                 // S^T MMA N (query columns)
@@ -117,13 +112,7 @@ struct Cfg {
   // P^T (MN-major SWIZZLE_32B): [NBP][2NS/16 query blocks][128 keys][32 B]
   static constexpr uint32_t OFF_P = OFF_Q + QB * kQBytes;
   static constexpr uint32_t kPBlock = KT * 32;                 // LBO: one 16-query block
-#ifdef BMC_TCK_PF16
-  // experiment: P as ONE fp16 term (scaled by 2^7) instead of bf16 hi + lo
-  static constexpr int PH = 1;
-#else
-  static constexpr int PH = 2;                                 // P terms: bf16 hi, lo
-#endif
-  static constexpr uint32_t kPBytes = (PH * NS + 15) / 16 * kPBlock;
+  static constexpr uint32_t kPBytes = 2 * NS / 16 * kPBlock;
   static constexpr uint32_t OFF_BAR = OFF_P + NBP * kPBytes;
   static constexpr uint32_t OFF_RED = OFF_BAR + 512;            // [NG][4 quadrants][NH] f32
   static constexpr uint32_t OFF_SUM = OFF_RED + NG * 4 * NH * 4;  // [NG][4][NH] f32
@@ -138,10 +127,10 @@ struct Cfg {
   static_assert(NH % 4 == 0, "8- or 16-byte P stores");
   static constexpr int CS = NH % 8 == 0 ? 8 : 4;               // column step of TMEM / P chunks
   static_assert(NBP * kPBytes >= (4 + 2) * N * 4, "combine scratch in the P area");
-  static_assert((PH * NS) % 8 == 0 && NQK % 8 == 0, "MMA N");
+  static_assert((2 * NS) % 16 == 0 && NQK % 8 == 0, "MMA N");
   // TMEM columns: S^T[b] at b*N, O^T (hi NS cols, lo NS cols) at NB*N
   static constexpr uint32_t TM_O = NB * N;
-  static constexpr uint32_t kTmemCols = (NB * N + PH * NS <= 256) ? 256 : 512;
+  static constexpr uint32_t kTmemCols = (NB * N + 2 * NS <= 256) ? 256 : 512;
 };
 
 #ifdef BMC_TC_TRACE
@@ -534,8 +523,7 @@ __global__ void __launch_bounds__(Cfg<N, NG, NS>::kThreads, 1)
   } else if (warp == C::kWarpPV) {
     // ------------------------------------------------------ O^T += V^T P^T issuer
     if (lane == 0) {
-      // A = V tile, B = P^T: MN-major (PF16: B is fp16, format 0 in bits 10-12)
-      constexpr uint32_t IPV = idesc_bf16(D, C::PH * NS, 1, 1) & ~(C::PH == 1 ? (1u << 10) : 0u);
+      constexpr uint32_t IPV = idesc_bf16(D, 2 * NS, 1, 1);  // A = V tile, B = P^T: MN-major
       int vs = 0;
       uint32_t vph = 0;
       long long i = t_begin;
@@ -757,7 +745,7 @@ __global__ void __launch_bounds__(Cfg<N, NG, NS>::kThreads, 1)
             mbar_wait(PEMPTY(tp % C::NBP), (tp / C::NBP) & 1);
             fence_after();
 #pragma unroll 1
-            for (int cc = 0; cc < C::PH * NH; cc += C::CS) {
+            for (int cc = 0; cc < 2 * NH; cc += C::CS) {
               const int hl = cc >= NH, c0 = cc - hl * NH;
               float ov[C::CS];
               const uint32_t ta = tmem + C::TM_O + hl * NS + h * NH + c0 + lane_addr;
@@ -782,14 +770,6 @@ __global__ void __launch_bounds__(Cfg<N, NG, NS>::kThreads, 1)
           for (int e = 0; e < 4; e += 2) {
             const int c = c0 + e;
             const float2 d = __fadd2_rn(make_float2(x[c], x[c + 1]), make_float2(-mr[e], -mr[e + 1]));
-#ifdef BMC_TCK_PF16
-            // 2^(d + 7) <= 2^15 (lazy max: d <= 8) in fp16; the row sums add the
-            // rounded values, so the weights of numerator and denominator agree
-            const __half2 ph = __floats2half2_rn(fast_exp2(d.x + 7.f), fast_exp2(d.y + 7.f));
-            phi[c / 2] = *reinterpret_cast<const uint32_t*>(&ph);
-            l2[c / 2] = __fadd2_rn(l2[c / 2], __half22float2(ph));
-            plo[c / 2] = 0;
-#else
             const float2 pv = make_float2(fast_exp2(d.x), fast_exp2(d.y));
             l2[c / 2] = __fadd2_rn(l2[c / 2], pv);
             const uint32_t bx = __float_as_uint(pv.x), by = __float_as_uint(pv.y);
@@ -798,7 +778,6 @@ __global__ void __launch_bounds__(Cfg<N, NG, NS>::kThreads, 1)
                                                           -__uint_as_float(by & 0xffff0000u)));
             const __nv_bfloat162 lb = __floats2bfloat162_rn(lo.x, lo.y);
             plo[c / 2] = *reinterpret_cast<const uint32_t*>(&lb);
-#endif
           }
         }
         // P^T[pb] was last read by the O^T MMAs of tile tc - NBP
@@ -811,9 +790,8 @@ __global__ void __launch_bounds__(Cfg<N, NG, NS>::kThreads, 1)
           for (int e = 0; e < NH / 8; ++e) {
             const int eh = h * (NH / 8) + e;             // hi chunk; lo chunks follow N / 8 later
             sts_v4(pbase + paddr(eh), phi[4 * e], phi[4 * e + 1], phi[4 * e + 2], phi[4 * e + 3]);
-            if constexpr (C::PH == 2)
-              sts_v4(pbase + paddr(eh + NS / 8), plo[4 * e], plo[4 * e + 1], plo[4 * e + 2],
-                     plo[4 * e + 3]);
+            sts_v4(pbase + paddr(eh + NS / 8), plo[4 * e], plo[4 * e + 1], plo[4 * e + 2],
+                   plo[4 * e + 3]);
           }
         } else {   // groups of 4 queries: 8-byte halves of the 16-byte chunks
 #pragma unroll
@@ -821,8 +799,7 @@ __global__ void __launch_bounds__(Cfg<N, NG, NS>::kThreads, 1)
             const int col = h * NH + 4 * e;
             const uint32_t half = (uint32_t)((col >> 2) & 1) * 8u;
             sts_v2(pbase + paddr(col >> 3) + half, phi[2 * e], phi[2 * e + 1]);
-            if constexpr (C::PH == 2)
-              sts_v2(pbase + paddr((col >> 3) + NS / 8) + half, plo[2 * e], plo[2 * e + 1]);
+            sts_v2(pbase + paddr((col >> 3) + NS / 8) + half, plo[2 * e], plo[2 * e + 1]);
           }
         }
         fence_proxy_smem();
@@ -852,15 +829,14 @@ __global__ void __launch_bounds__(Cfg<N, NG, NS>::kThreads, 1)
       for (int c0 = 0; c0 < NH; c0 += C::CS) {
         float o_hi[C::CS], o_lo[C::CS];
         tmem_ld_cols<C::CS>(tmem + C::TM_O + h * NH + c0 + lane_addr, o_hi);
-        if constexpr (C::PH == 2)
-          tmem_ld_cols<C::CS>(tmem + C::TM_O + NS + h * NH + c0 + lane_addr, o_lo);
+        tmem_ld_cols<C::CS>(tmem + C::TM_O + NS + h * NH + c0 + lane_addr, o_lo);
 #pragma unroll
         for (int e = 0; e < C::CS; ++e) {
           const int c = c0 + e;
           const int m = h * NH + c;
           if (m < p.M) {
             const float L = (sums[c] + sums[NH + c]) + (sums[2 * NH + c] + sums[3 * NH + c]);
-            const float o = C::PH == 2 ? o_hi[e] + o_lo[e] : o_hi[e];
+            const float o = o_hi[e] + o_lo[e];
             if (nseg == 1) {
               ly.O[(qrow0 + m) * D + kl] = o / L;
             } else {

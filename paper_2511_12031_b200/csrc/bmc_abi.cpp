@@ -1644,7 +1644,7 @@ int bmc_set_option(bmc_t h, int key, long long value) {
       h->attn_path = (int)value;
       return 0;
     case BMC_OPT_ARENA:
-      if (value < 0 || value > 1) return fail(BMC_ERR_ARG, "arena kind");
+      if (value < 0 || value > 2) return fail(BMC_ERR_ARG, "arena kind");
       h->arena_kind = (int)value;
       return 0;
     case BMC_OPT_SKIP_PADDING:
@@ -1680,6 +1680,16 @@ int bmc_pool_reserve(int device, long long bytes) {
   }
   const int rc = bmc::pool_reserve(device, (size_t)bytes);
   if (rc) return fail(rc, "pool_reserve(%lld bytes) failed", bytes);
+  return 0;
+}
+
+int bmc_region_reserve(int device, long long bytes) {
+  if (bytes < 0) return fail(BMC_ERR_ARG, "bytes=%lld < 0", bytes);
+  if (device < 0 && cudaGetDevice(&device) != cudaSuccess)
+    return fail(BMC_ERR_CUDA, "cudaGetDevice failed");
+  const int rc = bmc::region_reserve(device, (size_t)bytes);
+  if (rc == BMC_ERR_STATE) return fail(rc, "growth region still holds live buffers");
+  if (rc) return fail(rc, "region_reserve(%lld bytes) failed", bytes);
   return 0;
 }
 

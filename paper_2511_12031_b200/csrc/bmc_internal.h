@@ -125,15 +125,19 @@ struct Arena;
 struct Buffer {
   void* ptr = nullptr;
   size_t bytes = 0;
-  int slot = -1;        // arena slot (VMM), -1 = pool allocation
-  int kind = 0;         // 0 VMM, 1 pool
+  int slot = -1;        // arena slot (VMM) or region end, -1 = pool allocation
+  int kind = 0;         // 0 VMM, 1 pool, 2 two-ended region
 };
 Arena* arena_create(int device, size_t max_bytes_per_tensor, int* err);
 int pool_reserve(int device, size_t bytes);
 int pool_trim(int device);
+// (Re)create the device's two-ended growth region of `bytes` (0: free it);
+// STATE while buffers of the old region are live.
+int region_reserve(int device, size_t bytes);
 // Obtain a buffer of `bytes` for tensor (0 = K, 1 = V) in the slot not
 // holding `keep` (the tensor's live buffer).  kind 0 = VMM slot, 1 =
-// stream-ordered pool allocation (also the fallback when VMM is unsupported).
+// stream-ordered pool allocation (also the fallback when VMM is unsupported),
+// 2 = the end of the growth region opposite to `keep` (pool when full).
 int arena_alloc(Arena* a, int tensor, size_t bytes, int kind, const Buffer* keep,
                 cudaStream_t s, Buffer* out);
 // Release a buffer once all work enqueued so far on s has finished with it.

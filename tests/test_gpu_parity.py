@@ -185,6 +185,43 @@ def test_arena_kinds_agree():
         p.close()
 
 
+def test_growth_region_two_ended():
+    """BMC_OPT_ARENA = 2 (two-ended growth region, bmc_region_reserve): a
+    3-layer model (one stream) and a separate handle on its own stream share
+    the region; caches, ledgers and outputs match the oracle; a region too
+    small for the late growths falls back to the pool mid-run; the region
+    cannot be replaced while buffers live in it, and is freed at the end."""
+    import torch
+    from harness import Model
+    row = 4 * 128 * 2            # one row of all 4 units (B=2 x H_kv=2) of one tensor, bf16
+    # ample (both ends hold every buffer), then ~0.7 MB: the later growths
+    # no longer fit and come from the pool
+    for size in (64 << 20, 6 * 120 * row):
+        assert bmc.bmc_region_reserve(-1, size) == 0
+        m = Model(3, 2, 2, 8, 128, 16, 200, seed=23, options=((bmc.BMC_OPT_ARENA, 2),))
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):          # the side handle lives on stream s
+            side = Pair(2, 2, 2, 128, 8, 120, dtype="bf16", seed=21)
+            side.gpu.set_option(bmc.BMC_OPT_ARENA, 2)
+        for n in range(1, 201):
+            m.decode_step(check=(n % 17 == 0 or n in (16, 17, 200)))
+            if n <= 120:
+                with torch.cuda.stream(s):
+                    side.append()
+                    if n % 11 == 0:
+                        side.sdpa()
+        m.check_state()
+        with torch.cuda.stream(s):
+            side.check_state()
+        with pytest.raises(bmc.BMCError):
+            bmc.bmc_region_reserve(-1, 1 << 20)     # live buffers
+        m.close()
+        side.close()
+        torch.cuda.synchronize()
+        assert bmc.bmc_region_reserve(-1, 0) == 0
+        del s
+
+
 def test_launch_count_increments():
     n0 = bmc.bmc_launch_count()
     p = Pair(1, 2, 2, 128, 4, 16, dtype="bf16")

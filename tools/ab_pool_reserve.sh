@@ -11,6 +11,6 @@ python - <<'PY'
 import glob, json
 for f in sorted(glob.glob("gpurun_out/ab_reserve_*.json")):
     d = json.loads(open(f).read())
-    print(f, d["config"]["pool_reserve_bytes"], round(d["value"]), round(d["ms_per_step"]),
+    print(f, d["growth_memory"]["bytes"], round(d["value"]), round(d["ms_per_step"]),
           round(d["roofline"]["frac"], 3), d["clocks"]["sm_mhz"])
 PY

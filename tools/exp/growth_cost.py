@@ -16,6 +16,10 @@ HQ = H
 if "--l3" in sys.argv:      # BASELINE configs[3]: Llama-3-8B GQA, B=64, 0 -> 8192
     B, H, HQ, N = 64, 8, 32, 8192
 ARENA = 0 if "--vmm" in sys.argv else 1   # BMC_OPT_ARENA: 0 VMM slots (premapped), 1 pool
+if "--region" in sys.argv:                 # 2: two-ended growth region of twice the final cache
+    ARENA = 2
+    bmc.load()
+    bmc.bmc_region_reserve(0, 2 * (2 * B * H * N * D * 2) * L + (256 << 20))
 if "--reserve" in sys.argv:                # map the peak footprint into the pool up front
     bmc.load()
     bmc.bmc_pool_reserve(0, 2 * B * H * N * D * 2 * (L + L))
@@ -57,6 +61,6 @@ def gen(tag):
         h.close()
 
 
-print("arena:", "vmm (helper-thread premap)" if ARENA == 0 else "pool")
+print("arena:", {0: "vmm (helper-thread premap)", 1: "pool", 2: "two-ended region"}[ARENA])
 for i in range(3):
     gen(f"gen{i}")

@@ -24,22 +24,23 @@ from paper_2511_12031_b200 import bmc  # noqa: E402
 
 
 def run_point(cfg, policy, r, reps=1, skip_padding=False):
-    """One sweep point.  Each point starts from a trimmed growth pool with the
-    workload's peak footprint reserved (as bench.py does), so no point pays
-    (or inherits) the driver's pool-growth stalls."""
+    """One sweep point.  Each point sets up its growth memory as bench.py does
+    (the two-ended growth region when twice the final cache fits, else a
+    trimmed pool with the peak footprint reserved), so no point pays or
+    inherits another's allocator state."""
     dev = torch.device("cuda", 0)
     stream = torch.cuda.current_stream(dev)
     B = cfg["B"]
     torch.cuda.synchronize()
+    bmc.bmc_region_reserve(0, 0)
     bmc.bmc_pool_trim(0)
     ring = bench.make_ring(cfg, B, dev)
     t_all = 1 + cfg["k"]
     outs = {t: [torch.empty(B, cfg["H_q"], t, cfg["D"], dtype=torch.float32, device=dev)
                 for _ in range(cfg["L"])] for t in range(1, t_all + 1)}
-    eb = 2 if cfg["dtype"] == "bf16" else 4
-    per_layer = 2 * B * cfg["H_kv"] * cfg["N"] * cfg["D"] * eb
-    bmc.bmc_pool_reserve(0, bench.reserve_bytes(per_layer, cfg["L"], dev, margin=4 << 30))
+    kind, arena, _ = bench.growth_memory(cfg, B, dev, "auto", margin=4 << 30)
     gen = bench.Generation(cfg, B, r, policy, ring, outs, stream, 0)
+    gen.arena = kind
     gen.skip_padding = skip_padding
     gen.run()                                   # warm-up
     torch.cuda.synchronize()
@@ -51,7 +52,7 @@ def run_point(cfg, policy, r, reps=1, skip_padding=False):
     e1.record(stream)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
-    return {"policy": policy + ("+length-aware" if skip_padding else ""), "r": r, "T": -(-cfg["N"] // r) if policy == "bmc" else None,
+    return {"policy": policy + ("+length-aware" if skip_padding else ""), "r": r, "arena": arena, "T": -(-cfg["N"] // r) if policy == "bmc" else None,
             "tokens_per_s": tok / (ms / 1e3), "ms_per_generation": ms / reps}
 
 
