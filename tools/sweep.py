@@ -38,7 +38,7 @@ def run_point(cfg, policy, r, reps=1, skip_padding=False):
     t_all = 1 + cfg["k"]
     outs = {t: [torch.empty(B, cfg["H_q"], t, cfg["D"], dtype=torch.float32, device=dev)
                 for _ in range(cfg["L"])] for t in range(1, t_all + 1)}
-    kind, arena, _ = bench.growth_memory(cfg, B, dev, "auto", margin=4 << 30)
+    kind, arena, _ = bench.growth_memory(cfg, B, dev, "auto", margin=4 << 30, policy=policy)
     gen = bench.Generation(cfg, B, r, policy, ring, outs, stream, 0)
     gen.arena = kind
     gen.skip_padding = skip_padding
