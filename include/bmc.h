@@ -112,10 +112,12 @@ int bmc_admissible(bmc_t h, int k);
    [B][H_q][t][D] fp32 with t = 1 + bmc_admissible(hs[l], k) (every layer
    admits the same number).  Returns k_adm >= 0, or an error before anything
    is enqueued (ARG, STATE, CAPACITY, UNSUPPORTED; workspaces are allocated
-   for every layer before any layer changes).  OOM on a growth allocation:
-   the layers of the 32-layer chunks already launched (layers < 32c) have
-   taken the step, every other layer is rolled back to its state before the
-   call (a growth it completed stays: the retried step does not grow it
+   for every layer before any layer changes).  The 32-layer chunks are
+   launched in layer order, or in reverse order when the layers' buffers sit
+   at end 0 of the two-ended growth region (BMC_OPT_ARENA = 2: LIFO moves).
+   OOM on a growth allocation: the layers of the chunks already launched
+   have taken the step, every other layer is rolled back to its state before
+   the call (a growth it completed stays: the retried step does not grow it
    again); bmc_valid tells the two apart.  Commit afterwards with bmc_commit_step
    (or per layer with bmc_commit / bmc_commit_rows).
    All-host form (the end-to-end call): when every K, V, Q, O (and Kd, Vd for
@@ -328,9 +330,11 @@ int bmc_pool_reserve(int device, long long bytes);
    the buffer it replaces and pops the released old buffers off the other
    end: no fragmentation, no driver call and no host wait per growth (the
    stream-ordered pool stalled the host for up to ~1 s per growth step on the
-   L3-8B workload, profiles/r02_growth_cost_l3.txt).  Sized for the peak of
-   a copy growth: old + new buffers of every layer of a step, i.e. about
-   twice the final cache.  Space released on one stream is handed to
+   L3-8B workload, profiles/r02_growth_cost_l3.txt).  bmc_decode_step and
+   bmc_spec_step move the layers chunk by chunk in LIFO order, so a copy
+   growth's peak is the cache plus one 32-layer chunk of new buffers; size
+   the region for that (per-layer calls: the cache plus the new buffers of
+   the layers that grow before the first old buffer is released).  Space released on one stream is handed to
    another only after that stream passed the release (events).  Errors: ARG
    (bytes < 0), STATE (buffers of the current region are still live), OOM,
    CUDA. */

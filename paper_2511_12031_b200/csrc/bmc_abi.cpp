@@ -615,6 +615,18 @@ static int rollback_chunk(const bmc_t* hs, int l0, int l_end, int n_appended, in
   return rc;
 }
 
+// Chunk order of a fused step.  In the two-ended growth region a growth
+// pushes each chunk's new buffers onto one end and pops its old buffers off
+// the other; taking the chunks in the reverse of the order that pushed the
+// old buffers (last pushed = on top = first moved) lets every chunk's old
+// buffers leave the region before the next chunk's new ones arrive, so a
+// growth needs the cache plus ONE chunk of new buffers, not twice the cache.
+// The buffers sit at end 0 after odd-numbered growths (pushed in forward
+// order), at end 1 after even-numbered ones (pushed in reverse order).
+static bool chunks_reversed(bmc_t h0) {
+  return h0->kbuf.kind == 2 && h0->kbuf.slot == 0;
+}
+
 // One chunk's keys-on-lanes launch: all layers in one launch when they agree
 // on capacity, copy-on-read state and pending rows (the usual case: one r,
 // one step sequence), else one launch per layer (e.g. after an OOM fallback
@@ -999,7 +1011,10 @@ static int spec_step_impl(const bmc_t* hs, int L, const void* const* K, const vo
   // deferred to the attention, copy-on-read), the chunk's verify launch, then
   // the old buffers are released (at most one chunk holds old + new buffers).
   std::vector<bmc::AttnLayer> layers(L);
-  for (int l0 = 0; l0 < L; l0 += bmc::kMaxLayersPerLaunch) {
+  const int nchunks = (L + bmc::kMaxLayersPerLaunch - 1) / bmc::kMaxLayersPerLaunch;
+  const bool rev = chunks_reversed(h0);
+  for (int ci = 0; ci < nchunks; ++ci) {
+    const int l0 = (rev ? nchunks - 1 - ci : ci) * bmc::kMaxLayersPerLaunch;
     const int nl = std::min(bmc::kMaxLayersPerLaunch, L - l0);
     for (int l = l0; l < l0 + nl; ++l) {
       const bool defer = hs[l]->copy_on_read && !hs[l]->skip_padding;
@@ -1108,7 +1123,10 @@ int bmc_decode_step(const bmc_t* hs, int L, const void* const* K, const void* co
   // the attention, copy-on-read), then the chunk's launch, then the old
   // buffers are released -- so at most one chunk holds old + new buffers.
   std::vector<bmc::AttnLayer> layers(L);
-  for (int l0 = 0; l0 < L; l0 += bmc::kMaxLayersPerLaunch) {
+  const int nchunks = (L + bmc::kMaxLayersPerLaunch - 1) / bmc::kMaxLayersPerLaunch;
+  const bool rev = chunks_reversed(h0);
+  for (int ci = 0; ci < nchunks; ++ci) {
+    const int l0 = (rev ? nchunks - 1 - ci : ci) * bmc::kMaxLayersPerLaunch;
     const int nl = std::min(bmc::kMaxLayersPerLaunch, L - l0);
     for (int l = l0; l < l0 + nl; ++l) {
       // copy-on-read growth (BMC policy; CUDA-core or keys-on-lanes kernel;

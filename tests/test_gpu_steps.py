@@ -121,6 +121,37 @@ def test_tree_step_errors_leave_state():
     m.close()
 
 
+@pytest.mark.parametrize("spec", [False, True])
+def test_region_lifo_chunks(spec):
+    """34 layers (two fused chunks: 32 + 2) in a two-ended growth region of
+    only the final cache plus one 32-layer chunk: the fused steps move the
+    chunks in LIFO order (the chunk whose old buffers are on top first), so
+    every growth fits without the pool -- all buffers end inside one
+    region-sized span -- and outputs, caches and ledgers match the oracle."""
+    B, H_kv, L, N, r = 2, 4, 34, 96, 16
+    per_layer = 2 * B * H_kv * N * 128 * 2
+    size = (L + 32) * per_layer + (1 << 20)
+    assert bmc.bmc_region_reserve(-1, size) == 0
+    m = Model(L, B, H_kv, 8, 128, r, N, seed=34, options=((bmc.BMC_OPT_ARENA, 2),))
+    it = 0
+    while m.orc[0].stats()["valid_max"] < N - 6:
+        if spec:
+            k_adm = m.spec_step(4, check=(it % 4 == 0))
+            m.commit_step(synth.acceptance(5, it, B, k_adm))
+        else:
+            m.decode_step(check=(it % 9 == 0))
+        it += 1
+    m.check_state()
+    ptrs = []
+    for g in m.gpu:
+        k, v, cap = bmc.bmc_kv_view(g.h)
+        ptrs += [k, v]
+    assert max(ptrs) - min(ptrs) < size, "a growth fell back to the pool"
+    m.close()
+    torch.cuda.synchronize()
+    assert bmc.bmc_region_reserve(-1, 0) == 0
+
+
 @pytest.mark.parametrize("policy", ["iterative", "upfront"])
 @pytest.mark.parametrize("H_kv,H_q,k", [(2, 2, 4), (2, 16, 4), (1, 8, 8)])
 def test_baselines_under_speculation(policy, H_kv, H_q, k):
