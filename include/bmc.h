@@ -273,11 +273,13 @@ int bmc_sync(bmc_t h);
                               the TMEM lanes for G*t <= 80, else queries on
                               the lanes), 3 tcgen05 with queries on the lanes,
                               4 tcgen05 with keys on the lanes (G*t <= 80)
-     3 BMC_OPT_ARENA          0 VMM ping-pong slots, 1 stream-ordered pool
-                              (default), 2 the device's two-ended growth
-                              region (bmc_region_reserve; the pool when the
-                              region is absent or full); takes effect at the
-                              next growth
+     3 BMC_OPT_ARENA          0 VMM ping-pong slots, 1 stream-ordered pool,
+                              2 the device's two-ended growth region
+                              (bmc_region_reserve; the pool when the region is
+                              absent or full).  Default: 2 when the device has
+                              a region at bmc_create (the first buffer comes
+                              from it too), else 1.  Takes effect at the next
+                              growth
      4 BMC_OPT_SKIP_PADDING   1 = length-aware ABLATION: SDPA streams only the
                               rows some query sees instead of all cap rows
                               (not the method: P:L441, L853; results are

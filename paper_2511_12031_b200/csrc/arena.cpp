@@ -523,6 +523,12 @@ int region_reserve(int device, size_t bytes) {
   return rc;
 }
 
+bool region_present(int device) {
+  std::lock_guard<std::mutex> lk(g_regmu);
+  auto it = g_region.find(device);
+  return it != g_region.end() && it->second;
+}
+
 // A block of the region at end `pref` (else the other end) on stream s;
 // returns false when the region is absent or full.
 static bool region_alloc(int device, size_t bytes, int pref, cudaStream_t s, Buffer* out) {

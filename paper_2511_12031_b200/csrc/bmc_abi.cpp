@@ -511,6 +511,9 @@ int bmc_create_ex(int B, int H_kv, int H_q, int D, int r, int N_max, bmc_dtype d
   h->max_ctas = 4 * h->num_sms;
   int err = 0;
   h->arena = bmc::arena_create(device, (size_t)h->U * N_max * h->row_bytes, &err);
+  // a device with a growth region: the handle's buffers (the first one too)
+  // come from it
+  if (bmc::region_present(device)) h->arena_kind = 2;
   const size_t wsf = bmc::attn_workspace_floats(8, D, h->max_ctas);
   h->ws_floats = wsf;
   // stream-ordered: creating a handle never synchronises the device

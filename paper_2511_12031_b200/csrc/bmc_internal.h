@@ -134,6 +134,7 @@ int pool_trim(int device);
 // (Re)create the device's two-ended growth region of `bytes` (0: free it);
 // STATE while buffers of the old region are live.
 int region_reserve(int device, size_t bytes);
+bool region_present(int device);
 // Obtain a buffer of `bytes` for tensor (0 = K, 1 = V) in the slot not
 // holding `keep` (the tensor's live buffer).  kind 0 = VMM slot, 1 =
 // stream-ordered pool allocation (also the fallback when VMM is unsupported),
