@@ -1040,10 +1040,6 @@ static cudaError_t launch_layers(const AttnStepArgs& a, int l0, int nl, int num_
     if (p.M <= 16) return launch_n<16, MAXL>(p, ctas, s, a.tck_groups);
     if (p.M <= 32) return launch_n<32, MAXL>(p, ctas, s, a.tck_groups);
     if (p.M <= 48) return launch_n<48, MAXL>(p, ctas, s, a.tck_groups);
-#ifdef BMC_TCK_M64Q
-    if (p.M > 48 && p.M <= 64 && !a.tck_groups)   // experiment: the QTMA tile at NS = 64
-      return launch_ng<80, MAXL, BMC_TCK_M64Q, 64>(p, ctas, s);
-#endif
     if (p.M <= 64) return launch_n<64, MAXL>(p, ctas, s, a.tck_groups);
     if (p.M <= 72)   // 64 < M <= 72: the 70B verify tile (3 softmax groups; 2 for A/B)
       return a.tck_groups == 2 ? launch_ng<80, MAXL, 2, 72>(p, ctas, s)
@@ -1053,10 +1049,6 @@ static cudaError_t launch_layers(const AttnStepArgs& a, int l0, int nl, int num_
     if (p.M <= 16) return launch_n<16, 1>(p, ctas, s, a.tck_groups);
     if (p.M <= 32) return launch_n<32, 1>(p, ctas, s, a.tck_groups);
     if (p.M <= 48) return launch_n<48, 1>(p, ctas, s, a.tck_groups);
-#ifdef BMC_TCK_M64Q
-    if (p.M > 48 && p.M <= 64 && !a.tck_groups)   // experiment: the QTMA tile at NS = 64
-      return launch_ng<80, 1, BMC_TCK_M64Q, 64>(p, ctas, s);
-#endif
     if (p.M <= 64) return launch_n<64, 1>(p, ctas, s, a.tck_groups);
     if (p.M <= 72)   // 64 < M <= 72: the 70B verify tile (3 softmax groups; 2 for A/B)
       return a.tck_groups == 2 ? launch_ng<80, 1, 2, 72>(p, ctas, s)
