@@ -178,7 +178,19 @@ static int enter(bmc_t h) {
     cudaError_t e = cudaSetDevice(h->device);
     if (e != cudaSuccess) return cuda_fail(h, e, "cudaSetDevice");
   }
-  if (h->cor) return cor_materialize(h);   // never left pending by a successful call
+  if (h->cor) return cor_materialize(h);   // pending only between bmc_append and bmc_sdpa
+  return 0;
+}
+// enter() for bmc_sdpa: a copy-on-read growth left by bmc_append stays
+// pending for the attention launch to carry out
+static int enter_keep_growth(bmc_t h) {
+  if (!h || !h->cor) return enter(h);
+  if (h->sticky) return fail(h->sticky, "handle is in a sticky CUDA error state");
+  int cur = -1;
+  if (cudaGetDevice(&cur) != cudaSuccess || cur != h->device) {
+    cudaError_t e = cudaSetDevice(h->device);
+    if (e != cudaSuccess) return cuda_fail(h, e, "cudaSetDevice");
+  }
   return 0;
 }
 
@@ -666,7 +678,9 @@ int bmc_append(bmc_t h, const void* K, const void* V) {
   if (!K || !V) return fail(BMC_ERR_ARG, "K or V is null");
   if (h->staged > 0) return fail(BMC_ERR_STATE, "append while %d drafts are staged", h->staged);
   if (max_valid(h) >= h->N_max) return fail(BMC_ERR_CAPACITY, "cache full (N_max=%d)", h->N_max);
-  return append_impl(h, K, V);
+  // a BMC growth is left to the next bmc_sdpa's attention launch
+  // (copy-on-read); any other call carries it out first (enter)
+  return append_impl(h, K, V, h->copy_on_read && !h->skip_padding);
 }
 
 int bmc_append_n(bmc_t h, const void* K, const void* V, int n) {
@@ -787,6 +801,13 @@ static int launch_sdpa_layer(bmc_t h, const void* qd, float* od, int t) {
     rc = ensure_workspace(h, M);
     if (rc) return rc;
   }
+  // a pending copy-on-read growth (bmc_append -> bmc_sdpa): the CUDA-core and
+  // keys-on-lanes kernels copy while they stream, the queries-on-lanes one
+  // takes the separate realloc kernel first
+  if (h->cor && use_tc && !use_tck) {
+    rc = cor_materialize(h);
+    if (rc) return rc;
+  }
   bmc::AttnLayer layer;
   fill_layer(h, qd, od, &layer);
   bmc::AttnStepArgs a;
@@ -804,11 +825,13 @@ static int launch_sdpa_layer(bmc_t h, const void* qd, float* od, int t) {
   }
   h->n_app = h->n_draft = 0;
   account_sdpa(h, t);
+  rc = cor_release(h);
+  if (rc) return rc;
   return inputs_consumed(h);
 }
 
 int bmc_sdpa(bmc_t h, const void* Q, int n_valid, float* O) {
-  int rc = enter(h);
+  int rc = enter_keep_growth(h);
   if (rc) return rc;
   if (!Q || !O) return fail(BMC_ERR_ARG, "Q or O is null");
   if (n_valid == 0) return fail(BMC_ERR_ARG, "n_valid == 0");

@@ -76,13 +76,26 @@ def _tree_path(parent, k_adm, salt):
                                               (34, 1, 1, 2, 26, 64),    # 32 + 2 layers
                                               (3, 2, 2, 2, 32, 48)])    # largest tree
 def test_tree_step_fused(L, B, H_kv, H_q, k, r):
+    _tree_run(L, B, H_kv, H_q, k, r, "bmc")
+
+
+@pytest.mark.parametrize("policy", ["iterative", "upfront"])
+def test_tree_step_fused_baselines(policy):
+    """The fused token-tree step under the two baselines (ITERATIVE grows
+    exactly for the appended row and again for the admitted tree, reading
+    R17; UPFRONT never grows): outputs, caches and the whole ledger against
+    per-layer oracles."""
+    _tree_run(3, 2, 2, 8, 9, 1 if policy == "iterative" else 200, policy)
+
+
+def _tree_run(L, B, H_kv, H_q, k, r, policy):
     """bmc_spec_step_tree + bmc_commit_path_step (the token-tree bench
     mode's calls: every layer's append and k-node tree, one verify launch per
     32 layers, one path-compaction launch per 32 layers) against per-layer
     oracles: every output row (ancestor mask), then caches,
     lengths and ledgers bit-exact; per-row accepted paths of different
     lengths; topologies change every iteration."""
-    m = Model(L, B, H_kv, H_q, 128, r, 200, seed=26 + k)
+    m = Model(L, B, H_kv, H_q, 128, r, 200, seed=26 + k, policy=policy)
     it = 0
     while m.orc[0].stats()["valid_max"] < 200 - k - 2:
         parent = _bfs_tree(k, 100 + it)
@@ -147,6 +160,22 @@ def test_region_lifo_chunks(spec):
         k, v, cap = bmc.bmc_kv_view(g.h)
         ptrs += [k, v]
     assert max(ptrs) - min(ptrs) < size, "a growth fell back to the pool"
+    m.close()
+    torch.cuda.synchronize()
+    assert bmc.bmc_region_reserve(-1, 0) == 0
+
+
+@pytest.mark.parametrize("policy", ["iterative", "upfront"])
+def test_region_baseline_policies(policy):
+    """The two baselines in the growth region (handles created after
+    bmc_region_reserve take every buffer from it): ITERATIVE moves every
+    layer to the other end each step, UPFRONT holds its N_max buffers;
+    outputs, caches and ledgers against the oracle."""
+    assert bmc.bmc_region_reserve(-1, 32 << 20) == 0
+    m = Model(3, 2, 2, 8, 128, 1 if policy == "iterative" else 90, 90, policy=policy, seed=12)
+    for n in range(1, 91):
+        m.decode_step(check=(n % 13 == 0 or n == 90))
+    m.check_state()
     m.close()
     torch.cuda.synchronize()
     assert bmc.bmc_region_reserve(-1, 0) == 0

@@ -120,4 +120,21 @@ for groups, Hq, k in ((0, 16, 8), (4, 8, 3)):
         it += 1
     for c in caches:
         c.close()
+# round 2: the fused token-tree step (bmc_spec_step_tree + bmc_commit_path_step,
+# 34 layers = two verify launches, k = 9 tree) in the two-ended growth region
+# (LIFO chunk moves, copy-on-read growth), checked against per-layer oracles
+from harness import Model  # noqa: E402
+bmc.bmc_region_reserve(-1, 64 << 20)
+m = Model(34, 2, 1, 4, 128, 16, 64, seed=9, options=((bmc.BMC_OPT_ARENA, 2),))
+parent = [-1, 0, 0, 1, 1, 2, 3, 3, 5]
+it = 0
+while m.orc[0].stats()["valid_max"] < 50:
+    k_adm = m.spec_step_tree(9, parent, check=(it % 3 == 0))
+    acc = [x for x in (0, 1, 3, 6) if x < k_adm]
+    m.commit_path_step([acc[: it % 4], acc[: (it + 2) % 4]])
+    it += 1
+m.check_state()
+m.close()
+torch.cuda.synchronize()
+bmc.bmc_region_reserve(-1, 0)
 print("sanitize target ok")
