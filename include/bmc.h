@@ -91,7 +91,11 @@ int bmc_create_ex(int B, int H_kv, int H_q, int D, int r, int N_max, bmc_dtype d
    of batch row b, then valid_b += 1.  BMC: if max_b valid_b == cap first
    grows to min(cap + r, N_max): new buffer, strided copy of the cap old rows
    of every unit, zero-fill of the new rows.  ITERATIVE: always
-   reallocates to exactly max valid + 1 rows.  Errors: STATE if drafts are
+   reallocates to exactly max valid + 1 rows.  With BMC_OPT_COPY_ON_READ (the
+   default) a BMC growth is left pending for the next bmc_sdpa, whose
+   attention kernel copies the old rows while streaming them; any other call
+   on the handle first carries the growth out with the realloc kernel.
+   Contents and ledger are the same either way.  Errors: STATE if drafts are
    staged, CAPACITY if max valid == N_max. */
 int bmc_append(bmc_t h, const void* K, const void* V);
 
@@ -285,11 +289,14 @@ int bmc_sync(bmc_t h);
                               (not the method: P:L441, L853; results are
                               identical, bytes differ)
      5 BMC_OPT_COPY_ON_READ   1 (default) = a BMC growth inside bmc_decode_step
-                              (CUDA-core attention path) is copied by the
-                              attention kernel while it streams the old
-                              buffer (old rows read once, new
-                              buffer written once, no separate realloc
-                              kernel); 0 = separate realloc_copy_zero launch.
+                              / bmc_spec_step, or between bmc_append and
+                              bmc_sdpa, is copied by the attention kernel
+                              while it streams the old buffer (SURVEY
+                              NEXT-1: old rows read once, new buffer written
+                              once, no separate realloc kernel; the
+                              queries-on-lanes kernel, G*t > 80, still takes
+                              the realloc kernel); 0 = separate
+                              realloc_copy_zero launch.
                               Cache contents and ledger are identical.
      6 BMC_OPT_TCK_GROUPS     softmax column groups of the keys-on-lanes
                               tcgen05 kernel: 0 auto (4 for 16 < G*t <= 64,
