@@ -950,10 +950,21 @@ static cudaError_t cached_map(CUtensorMap* m, const void* base, long long rows,
       return base == o.base && rows == o.rows && units == o.units && box == o.box;
     }
   };
+  // splitmix64-mixed fields: the earlier XOR of (address, rows * 31, ...)
+  // collided for whole families of keys (4 KiB-aligned buffer addresses and
+  // capacities in steps of 128 rows), so lookups walked long bucket chains
   struct Hash {
+    static uint64_t mix(uint64_t x) {
+      x += 0x9e3779b97f4a7c15ull;
+      x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+      x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+      return x ^ (x >> 31);
+    }
     size_t operator()(const Key& k) const {
-      return std::hash<const void*>()(k.base) ^ (std::hash<long long>()(k.rows) * 31) ^
-             (std::hash<long long>()(k.units) * 131) ^ ((size_t)k.box * 1009);
+      uint64_t h = mix((uint64_t)(uintptr_t)k.base);
+      h = mix(h ^ (uint64_t)k.rows);
+      h = mix(h ^ (uint64_t)k.units);
+      return (size_t)mix(h ^ (uint64_t)k.box);
     }
   };
   static thread_local std::unordered_map<Key, CUtensorMap, Hash> cache;
